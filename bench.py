@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""AMSP model-state step benchmark (BASELINE.json metric: "AMSP step ms &
+params/s at 1/2/4/8 B200; collective bus GB/s vs NVLink").
+
+A step = one pass of the AMSP model-state pipeline over LLaMA-7B model states
+(bf16 P/G, fp32 master+m+v): cross-rank gradient reduce (fp32, fixed order)
+with 1/W scale -> AdamW on this rank's OS shard -> bf16 params gathered into
+every rank. Synthetic gradients (counter-based, oracle/amsp_oracle.c) are
+resident in HBM when the timed region starts (`value`); `e2e` repeats the
+step through the host-buffer C-ABI call (H2D of the step's gradients, D2H of
+the step statistics inside the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+--impl reference times the reference's CPU implementation of the path. The
+reference (`shardplan`) has no data plane, so that is the C/OpenMP
+restatement in oracle/ ("port"), run on this box's host cores on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "AMSP step ms & params/s at 1/2/4/8 B200; collective bus GB/s vs NVLink"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+NVLINK_P2P_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+NVLINK_NOMINAL_GBS = 900.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="llama-7b")
+    ap.add_argument("--plan", default="zero1",
+                    help="zero1 (P/G replica, OS over dp) | replica | 'p=AxB,g=AxB,os=AxB'")
+    ap.add_argument("--mesh", default=None, help="dp mesh per_node x nodes, default Nx1")
+    ap.add_argument("--layout", default="greedy", choices=["greedy", "contiguous"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def mesh_of(s, S):
+    a, b = s.lower().split("x")
+    return S.DeviceMesh(int(a), int(b))
+
+
+def plan_of(args, S, dp):
+    if args.plan == "zero1":
+        return S.ShardingPlan(S.DeviceMesh(1, 1), S.DeviceMesh(1, 1), dp)
+    if args.plan == "replica":
+        return S.ShardingPlan()
+    parts = dict(kv.split("=") for kv in args.plan.split(","))
+    return S.ShardingPlan(mesh_of(parts["p"], S), mesh_of(parts["g"], S), mesh_of(parts["os"], S))
+
+
+def peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured (MEASURED_PEAKS.json)"
+    return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.06)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def step_bytes(phi, owned, world, ndst):
+    """Algorithmic bytes of ONE fused launch on one rank.
+    HBM of this GPU: its OS shard read+written (24 B/elem), every rank's
+    reads of this GPU's bf16 gradients (2 B x Phi in total over the group)
+    and every owner's bf16 parameter stores into this GPU (2 B x Phi).
+    NVLink per direction: pulls of (W-1) peers' gradients for the owned
+    elements + pushes of the owned params to (ndst-1) peers."""
+    hbm = 24 * owned + 2 * phi + 2 * phi
+    nvl_in = 2 * owned * (world - 1)
+    nvl_out = 2 * owned * (ndst - 1)
+    return hbm, max(nvl_in, nvl_out)
+
+
+def cpu_baseline(phi_total, world, steps_budget_s=12.0, sample=None):
+    """The oracle's CPU step (C + OpenMP, all host cores) on a bounded sample
+    of the same workload: `sample` consecutive params of the flat model,
+    `world` ranks' gradients reduced, one OS owner per element (ZeRO-1)."""
+    import numpy as np
+
+    from oracle import cpu as O
+    from paper_2311_00257_b200.engine import DEFAULT_SEED
+    h = O.hyper()
+    n = sample or (64 << 20)
+    grads = [O.grads(0, n, DEFAULT_SEED, 1, r) for r in range(world)]
+    master = np.array([0.0], np.float32)
+    master = np.empty(n, np.float32)
+    O.lib()  # load
+    master[:] = 0.01
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    params = [np.zeros(n, np.uint16) for _ in range(world)]
+    segs = [(0, 0, n)]
+    times = []
+    t_start = time.perf_counter()
+    t = 1
+    while True:
+        s = O.scalars(t, world, h)
+        t0 = time.perf_counter()
+        O.step(grads, segs, master, m, v, params, s)
+        times.append(time.perf_counter() - t0)
+        t += 1
+        if time.perf_counter() - t_start > steps_budget_s or len(times) >= 5:
+            break
+    best = min(times)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": n / best, "unit": "params/s", "cores": cores, "kind": "port",
+            "sample": f"{n} consecutive params of the {phi_total}-param flat model, {world} "
+                      f"rank gradients reduced + AdamW + bf16 into {world} param copies; "
+                      f"best of {len(times)} steps, {best * 1e3:.1f} ms/step",
+            "ms_per_step_extrapolated": best * phi_total / n * 1e3}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2311_00257_b200 import shardplan as S
+    model = S.model(args.model)
+    phi = model.total_params
+    world = args.gpus
+    cpu = cpu_baseline(phi, world, steps_budget_s=5.0)
+    # K timed steps on the bounded sample (each step = one sample pass).
+    import numpy as np
+
+    from oracle import cpu as O
+    from paper_2311_00257_b200.engine import DEFAULT_SEED
+    n = 32 << 20
+    h = O.hyper()
+    grads = [O.grads(0, n, DEFAULT_SEED, 1, r) for r in range(world)]
+    master = np.full(n, 0.01, np.float32)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    params = [np.zeros(n, np.uint16) for _ in range(world)]
+    for t in range(1, args.warmup + 1):
+        O.step(grads, [(0, 0, n)], master, m, v, params, O.scalars(t, world, h))
+    t0 = time.perf_counter()
+    for t in range(args.warmup + 1, args.warmup + args.steps + 1):
+        O.step(grads, [(0, 0, n)], master, m, v, params, O.scalars(t, world, h))
+    dt = (time.perf_counter() - t0) / args.steps
+    value = n / dt
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "params/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * phi / n * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp32 (bf16 in/out)",
+        "data": "synthetic",
+        "config": {"workload": f"{args.model} model states, ZeRO-1 equiv over {world} ranks, "
+                               "AMSP optimizer step (CPU port, bounded sample)",
+                   "model": args.model, "phi": phi},
+        "cpu_baseline": {"value": value, "unit": "params/s", "cores": cores, "kind": "port",
+                         "sample": f"{n} consecutive params per step, {world} rank gradients"},
+        "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "note": "the reference (shardplan) is a CPU planner/simulator with no data plane; "
+                "its CPU path for this step is the oracle restatement (oracle/amsp_oracle.c)",
+        "cpu_baseline_detail": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_00257_b200 import shardplan as S
+    from paper_2311_00257_b200.engine import Engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
+    dp = mesh_of(args.mesh, S) if args.mesh else S.DeviceMesh(world, 1)
+    model = S.model(args.model)
+    plan = plan_of(args, S, dp)
+    eng = Engine(model, plan, dp, rank=rank, device=local, layout=args.layout)
+    eng.connect()
+    info = eng.info
+    stream = torch.cuda.Stream(device=local)
+    eng.init_state(stream)
+    eng.synth_grads(1, stream)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    step = 0
+    for _ in range(args.warmup):
+        step += 1
+        eng.step(step, stream)
+    torch.cuda.synchronize()
+    barrier()
+
+    # Timed region: K device-resident steps; per-step CUDA events on the
+    # engine stream for the step, and kernel-only events from the engine.
+    launches0 = eng.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    eng.time_kernel(True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step += 1
+            eng.step(step, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = eng.launch_count() - launches0
+    total_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_per_step = total_ms / args.steps
+
+    # The fused kernel alone (barriers excluded), bracketed by CUDA events on
+    # the engine stream inside the same timed region.
+    k_total, k_n = eng.kernel_ms()
+    eng.time_kernel(False)
+    kernel_ms = max_over_ranks(k_total / max(k_n, 1))
+
+    phi = info.total_params
+    value = phi / (ms_per_step * 1e-3)
+    pk, pk_src = peaks()
+    hbm_b, nvl_b = step_bytes(phi, info.owned, world, info.os_group_size)
+    hbm_ach = hbm_b / (kernel_ms * 1e-3) / 1e9
+    nvl_ach = nvl_b / (kernel_ms * 1e-3) / 1e9
+    t_hbm = hbm_b / (pk["hbm_gbs"] * 1e9)
+    t_nvl = nvl_b / (NVLINK_P2P_GBS * 1e9)
+    bound = "hbm" if t_hbm >= t_nvl else "nvlink"
+    roof = {
+        "bound": bound,
+        "achieved": round(hbm_ach if bound == "hbm" else nvl_ach, 1),
+        "peak": pk["hbm_gbs"] if bound == "hbm" else NVLINK_P2P_GBS,
+        "unit": "GB/s",
+        "frac": round((hbm_ach / pk["hbm_gbs"]) if bound == "hbm" else (nvl_ach / NVLINK_P2P_GBS), 4),
+        "traffic": None,
+        "kernel": "fused_step_kernel (reduce + AdamW + gather)",
+        "kernel_ms": round(kernel_ms, 4),
+        "algorithmic_bytes": {"hbm": hbm_b, "nvlink_per_direction": nvl_b},
+        "hbm": {"achieved": round(hbm_ach, 1), "peak": pk["hbm_gbs"],
+                "frac": round(hbm_ach / pk["hbm_gbs"], 4), "peak_source": pk_src},
+        "nvlink": {"achieved": round(nvl_ach, 1), "peak": NVLINK_P2P_GBS,
+                   "frac": round(nvl_ach / NVLINK_P2P_GBS, 4),
+                   "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md); "
+                                  "900 nominal"},
+        "lower_bound_ms": round(max(t_hbm, t_nvl) * 1e3, 3),
+        "frac_of_roofline_step": round(max(t_hbm, t_nvl) * 1e3 / ms_per_step, 4),
+    }
+    ncu_traffic = REPO / "profiles" / "r01_traffic.json"
+    if ncu_traffic.exists():
+        try:
+            d = json.loads(ncu_traffic.read_text())
+            key = f"{args.model}/{world}"
+            if key in d:
+                roof["traffic"] = d[key]
+        except Exception:
+            pass
+
+    # Busbw of the collective the fused kernel implements (nccl-tests
+    # convention: RS/AG (n-1)/n on the gathered size; AR 2(n-1)/n).
+    busbw = None
+    if world > 1:
+        busbw = {"reduce_scatter_equiv_gbs": round(2 * phi * (world - 1) / world / (kernel_ms * 1e-3) / 1e9, 1),
+                 "all_gather_equiv_gbs": round(2 * phi * (world - 1) / world / (kernel_ms * 1e-3) / 1e9, 1),
+                 "vs_nvlink_gbs": NVLINK_NOMINAL_GBS}
+
+    # End-to-end through the host-buffer C-ABI call.
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        host = torch.empty(phi, dtype=torch.int16, pin_memory=True)
+        grads_dev = torch.empty(phi, dtype=torch.int16, device=f"cuda:{local}")
+        # stage this rank's synthetic gradients into pinned host memory (setup)
+        from paper_2311_00257_b200 import _native as N
+        N.check(N.lib().amsp_k_synth_grad(grads_dev.data_ptr(), 0, phi, eng.seed, 1, rank,
+                                          None))
+        host.copy_(grads_dev)
+        del grads_dev
+        torch.cuda.synchronize()
+        barrier()
+        eng.step_host(step + 1, host.data_ptr(), stream)
+        step += 1
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            step += 1
+            eng.step_host(step, host.data_ptr(), stream)
+        barrier()
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
+        e2e = {"value": phi / e2e_s, "unit": "params/s", "ms_per_step": round(e2e_s * 1e3, 3),
+               "h2d_bytes_per_step": 2 * phi * world, "d2h_bytes_per_step": 8 * world,
+               "steps": args.e2e_steps,
+               "path": "amsp_engine_step_host: pinned host bf16 grads -> H2D -> step -> D2H stats"}
+        del host
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(phi, world)
+        except Exception as ex:  # the baseline is reported, never required
+            cpu = {"error": str(ex)}
+
+    if rank == 0:
+        clk = clocks.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "fp32 (bf16 grads/params)", "data": "synthetic",
+            "config": {"workload": f"{args.model} model states ({phi} params: bf16 P/G, fp32 "
+                                   f"master+m+v), AMSP step = grad reduce + AdamW + param gather",
+                       "model": args.model, "phi": phi, "plan": str(plan), "dp_mesh": str(dp),
+                       "layout": args.layout,
+                       "l2": f"inputs ({(16 * phi) / 1e9:.0f} GB of model state) >> 126 MB L2",
+                       "parallelism": f"dp{world}"},
+            "roofline": roof, "busbw": busbw, "e2e": e2e, "cpu_baseline": cpu,
+            "gpu_launches": launches, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,302 @@
+/* amsp_c.h — C-ABI of the B200-native AMSP model-state pipeline.
+ *
+ * Plain C: POD structs, plain pointers and sizes, opaque handles, no torch or
+ * C++ types. Every call returns an int status (AMSP_OK=0, AMSP_EINVAL=1 bad
+ * config, AMSP_EINFEASIBLE=2 nothing fits, AMSP_ECUDA=3 CUDA / peer error;
+ * the 0/1/2 meanings mirror the reference CLI exit codes) and
+ * amsp_last_error() returns a thread-local message. No C++ exception crosses
+ * this boundary.
+ *
+ * Two halves:
+ *  1. Planner (host only, no GPU needed). Each function is a drop-in for one
+ *     reference entry point of the `shardplan` C++ API, cited per function.
+ *     The full C++ API itself is include/amsp/plan.hpp (namespace shardplan).
+ *  2. Engine + kernels (B200, sm_100a). The reference has NO data plane
+ *     (SPEC.md:16); these entry points execute what its cost model and
+ *     overlap simulator describe (SURVEY.md §3 call stack 5):
+ *     gradient reduce (RS in the OS group + cross-replica sum) fused with
+ *     the bf16->fp32 upcast and 1/W scale, sharded AdamW on the local OS
+ *     shard, and the parameter gather fused with the fp32->bf16 downcast —
+ *     one kernel over NVLink peer memory (cudaIpc-mapped buffers of every
+ *     rank of the data-parallel group).
+ *
+ * Threading: planner calls are pure and thread-safe. One engine per GPU
+ * (one process per GPU); engine calls are not reentrant.
+ */
+#ifndef AMSP_C_H_
+#define AMSP_C_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AMSP_OK 0
+#define AMSP_EINVAL 1
+#define AMSP_EINFEASIBLE 2
+#define AMSP_ECUDA 3
+
+#define AMSP_ABI_VERSION 1
+
+int amsp_abi_version(void);
+const char* amsp_last_error(void);
+
+/* ------------------------------------------------------------ POD mirrors */
+
+/* shardplan::DeviceMesh (reference domain.hpp:39-46) */
+typedef struct { int per_node; int nodes; } amsp_mesh_t;
+
+/* shardplan::ShardingPlan (domain.hpp:93-113) */
+typedef struct {
+  amsp_mesh_t p, g, os;
+  int has_secondary;
+  amsp_mesh_t secondary;
+} amsp_plan_t;
+
+/* shardplan::ClusterSpec + Topology (domain.hpp:51-67) */
+typedef struct {
+  int gpus_per_node, node_count;
+  uint64_t gpu_memory_capacity;
+  amsp_mesh_t dp_mesh;
+  int leaf_count, nodes_per_leaf;
+  double inter_leaf_penalty;
+} amsp_cluster_t;
+
+/* shardplan::ModelSpec (domain.hpp:72-88); module_params has
+ * modules_per_layer entries and is only read during the call. */
+typedef struct {
+  uint64_t total_params;
+  int layer_count, modules_per_layer;
+  const uint64_t* module_params;
+  int hidden, seq_len, micro_batch, micro_batch_count, vocab;
+  int bytes_per_param, bytes_per_grad, bytes_per_os_per_param;
+} amsp_model_t;
+
+/* shardplan::CostConfig (cost_model.hpp:28-50); activation_mode 0 = None,
+ * 1 = FullRecompute. amsp_cost_config_default() fills the reference
+ * defaults. */
+typedef struct {
+  uint64_t bucket_size;
+  int activation_mode;
+  double activation_coeff_full, activation_coeff_recompute;
+  int tmp_in_flight_buckets, tmp_include_gather_buffer, exact_residual_buckets;
+  double flops_coeff_param, flops_coeff_attn;
+} amsp_cost_config_t;
+
+/* shardplan::TimeBreakdown / MemoryBreakdown (cost_model.hpp:52-68) */
+typedef struct { double t_p, t_g, t_os_allreduce, t_os_broadcast, total; } amsp_time_t;
+typedef struct {
+  double d_params, d_grads, d_os, d_modelstate, d_activation, d_tmp, d_total;
+} amsp_memory_t;
+
+/* shardplan::PlanResult (planner.hpp:27-33) */
+typedef struct {
+  amsp_plan_t plan;
+  amsp_time_t time;
+  amsp_memory_t memory;
+  int feasible;
+  int rank;
+} amsp_plan_result_t;
+
+/* shardplan::SimConfig (overlap_sim.hpp:66-80). tier: 0 none, 1 ag_rs,
+ * 2 ag_rs_ar, 3 ag_rs_ar_bc. time_source: 0 FLOPs, 1 table (the three
+ * per-module tables then hold modules_per_layer entries each). */
+typedef struct {
+  int overlap_tier, recompute, comm_streams, compute_time_source;
+  double peak_flops_per_gpu, compute_efficiency;
+  const double* fwd_times;
+  const double* bwd_grad_weight_times;
+  const double* bwd_grad_input_times;
+  double head_fwd_time, head_bwd_time;
+} amsp_sim_config_t;
+
+/* shardplan::BandwidthProfile, opaque. */
+typedef struct amsp_profile amsp_profile_t;
+
+void amsp_cost_config_default(amsp_cost_config_t* cfg);
+void amsp_sim_config_default(amsp_sim_config_t* cfg);
+
+/* ------------------------------------------------------------ planner */
+
+/* synthetic_profile (comm_model.cpp:129-160) */
+int amsp_profile_synthetic(double alpha_intra, double bw_intra,
+                           double alpha_inter, double bw_inter,
+                           const amsp_mesh_t* meshes, int n_meshes,
+                           const uint64_t* sizes, int n_sizes,
+                           amsp_profile_t** out);
+/* profile_from_csv (comm_model.cpp:182-228) / profile_from_json (:251-287) /
+ * load_profile (:289-297) */
+int amsp_profile_from_csv(const char* csv_text, amsp_profile_t** out);
+int amsp_profile_from_json(const char* json_text, amsp_profile_t** out);
+int amsp_profile_load(const char* path, amsp_profile_t** out);
+/* profile_to_canonical_json (comm_model.cpp:234-249). Writes up to cap bytes
+ * (NUL-terminated when it fits); *needed = length without NUL. */
+int amsp_profile_to_json(const amsp_profile_t* p, char* buf, size_t cap,
+                         size_t* needed);
+/* BandwidthProfile::collective_time (comm_model.cpp:121-127); kind 0 AG,
+ * 1 RS, 2 AR, 3 BC. */
+int amsp_collective_time(const amsp_profile_t* p, int kind, uint64_t size_bytes,
+                         amsp_mesh_t mesh, double* seconds);
+void amsp_profile_free(amsp_profile_t* p);
+
+/* ring_time (comm_model.cpp:45-55) */
+int amsp_ring_time(int kind, double size_bytes, int participants, double alpha,
+                   double link_bandwidth, double* seconds);
+
+/* validate_plan (domain.cpp:137-166). Violations are written as
+ * "constraint:detail\n" lines into buf. */
+int amsp_validate_plan(const amsp_plan_t* plan, const amsp_cluster_t* cluster,
+                       int* n_violations, char* buf, size_t cap);
+/* preset (domain.cpp:197-226); AMSP_EINFEASIBLE when it does not fit. */
+int amsp_preset(const char* name, const amsp_cluster_t* cluster, amsp_plan_t* out);
+
+/* memory_breakdown / total_comm_time / grad_bucket_count
+ * (cost_model.cpp:142-171, :128-140, :57-65) */
+int amsp_memory_breakdown(const amsp_model_t* model, const amsp_plan_t* plan,
+                          const amsp_cost_config_t* cfg, amsp_memory_t* out);
+int amsp_total_comm_time(const amsp_model_t* model, const amsp_cluster_t* cluster,
+                         const amsp_plan_t* plan, const amsp_profile_t* profile,
+                         const amsp_cost_config_t* cfg, amsp_time_t* out);
+int amsp_grad_bucket_count(const amsp_model_t* model, const amsp_plan_t* plan,
+                           const amsp_cost_config_t* cfg, uint64_t* out);
+
+/* partition_tensors_greedy (cost_model.cpp:189-219) */
+int amsp_partition_greedy(const uint64_t* sizes, int n, int shard_count,
+                          int* assignment, uint64_t* shard_sizes);
+
+/* enumerate_candidates (planner.cpp:110-129): up to cap plans; *n = total. */
+int amsp_enumerate_candidates(const amsp_cluster_t* cluster, amsp_plan_t* plans,
+                              int cap, int* n);
+/* solve (planner.cpp:144-166). On AMSP_EINFEASIBLE *best holds the
+ * minimal-memory candidate (NoFeasiblePlanError::closest). all/cap/n_all
+ * optionally receive the ranked candidate list. */
+int amsp_solve(const amsp_model_t* model, const amsp_cluster_t* cluster,
+               const amsp_profile_t* profile, const amsp_cost_config_t* cfg,
+               amsp_plan_result_t* best, uint64_t* evaluated, uint64_t* filtered,
+               amsp_plan_result_t* all, int cap, int* n_all);
+
+/* build_schedule + simulate_step + bubble_report + render_trace
+ * (overlap_sim.cpp:442-577). Any output pointer may be NULL. */
+int amsp_simulate(const amsp_model_t* model, const amsp_cluster_t* cluster,
+                  const amsp_plan_t* plan, const amsp_profile_t* profile,
+                  const amsp_cost_config_t* cfg, const amsp_sim_config_t* sim,
+                  double* step_time, double* compute_idle, int* n_events,
+                  char* trace, size_t trace_cap, size_t* trace_needed);
+
+/* ------------------------------------------------------------ layout */
+
+#define AMSP_LAYOUT_GREEDY 0     /* reference inter-tensor LPT index map */
+#define AMSP_LAYOUT_CONTIGUOUS 1 /* even contiguous split, 8-element aligned */
+
+/* One rank's optimizer-state segments over the flat parameter vector
+ * (tensors concatenated in forward order): segment s covers flat elements
+ * [flat[s], flat[s]+len[s]) stored at os[s] in the rank's fp32 shard. */
+int amsp_layout_segments(const uint64_t* tensor_sizes, int n_tensors,
+                         int shard_count, int shard, int layout,
+                         uint64_t* flat, uint64_t* os, uint64_t* len, int cap,
+                         int* n_segments, uint64_t* owned);
+
+/* Group of `rank` for component mesh `mesh` inside the DP mesh `dp`
+ * (ranks numbered node-major: rank = node*dp.per_node + local). Returns the
+ * block index, the rank's position in its block and the block's members in
+ * position order. */
+int amsp_mesh_group(amsp_mesh_t dp, amsp_mesh_t mesh, int rank, int* block,
+                    int* position, int* members, int cap, int* n_members);
+
+/* ------------------------------------------------------------ engine */
+
+typedef struct amsp_engine amsp_engine_t;
+
+typedef struct {
+  const uint64_t* tensor_sizes; /* flat order; read during create only */
+  int n_tensors;
+  amsp_plan_t plan;
+  amsp_mesh_t dp_mesh;          /* rank count = dp_mesh.per_node*dp_mesh.nodes */
+  int rank;
+  int device;                   /* CUDA ordinal */
+  int layout;                   /* AMSP_LAYOUT_* */
+  double lr, beta1, beta2, eps, weight_decay;
+  uint64_t seed;
+} amsp_engine_config_t;
+
+typedef struct {
+  uint64_t total_params;        /* Phi */
+  uint64_t owned;               /* elements of this rank's OS shard */
+  int n_segments;
+  int world, os_block, os_position, os_group_size, replica_count;
+  int ntiles, grid, block;      /* fused-kernel launch geometry */
+  void* grads;                  /* bf16 [Phi] */
+  void* params;                 /* bf16 [Phi] */
+  void* master;                 /* fp32 [owned] */
+  void* exp_avg;                /* fp32 [owned] */
+  void* exp_avg_sq;             /* fp32 [owned] */
+  uint64_t device_bytes;        /* allocated by the engine */
+} amsp_engine_info_t;
+
+#define AMSP_IPC_HANDLE_BYTES 64
+
+int amsp_engine_create(const amsp_engine_config_t* cfg, amsp_engine_t** out);
+int amsp_engine_info(const amsp_engine_t* e, amsp_engine_info_t* info);
+/* Export this rank's peer-shared buffer (grads | params | flags). */
+int amsp_engine_export_handle(amsp_engine_t* e, void* handle64);
+/* Map every other rank's buffer; handles = world * 64 bytes in rank order. */
+int amsp_engine_import_handles(amsp_engine_t* e, const void* handles, int world);
+/* Single-GPU emulation of a DP group (tests / smoke): link n engines created
+ * in this process on the SAME device as ranks 0..n-1 of one group. Linked
+ * engines skip the cross-GPU barriers, so the caller must run their steps
+ * one after another on one stream (synth all grads, then step every rank). */
+int amsp_engine_link_local(amsp_engine_t* const* engines, int n);
+/* master = 0.02*u(seed, i), m = v = 0, params = bf16(master) (all ranks
+ * derive the identical replicated initial parameters locally). */
+int amsp_engine_init_state(amsp_engine_t* e, void* stream);
+/* Synthetic bf16 gradients for this rank and step (oracle definition). */
+int amsp_engine_synth_grads(amsp_engine_t* e, int step, void* stream);
+/* One AMSP optimizer step (1-based step index) with device-resident grads:
+ * cross-GPU barrier, fused reduce+AdamW+gather kernel, cross-GPU barrier. */
+int amsp_engine_step(amsp_engine_t* e, int step, void* stream);
+/* Same step through host buffers: H2D of this rank's bf16 gradients
+ * (total_params elements; pinned for async), the step, and D2H of the step
+ * statistics (stats[0] = sum of squared reduced grads over the rank's shard).
+ * Synchronizes the stream before returning. */
+int amsp_engine_step_host(amsp_engine_t* e, int step, const void* host_grads,
+                          float* host_stats, void* stream);
+/* Device step statistics of the last step (synchronous). */
+int amsp_engine_stats(amsp_engine_t* e, float* stats2);
+/* Copy `count` elements at `offset` of a buffer to host (synchronous).
+ * which: 0 grads(bf16) 1 params(bf16) 2 master 3 exp_avg 4 exp_avg_sq. */
+int amsp_engine_read(amsp_engine_t* e, int which, uint64_t offset, uint64_t count,
+                     void* host_dst);
+int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t count,
+                      const void* host_src);
+/* Bracket every fused launch with CUDA events on the step's stream (enable
+ * != 0), then read the summed kernel time of the launches since enabling
+ * (synchronous; resets the count). */
+int amsp_engine_time_kernel(amsp_engine_t* e, int enable);
+int amsp_engine_kernel_ms(amsp_engine_t* e, double* total_ms, int* launches);
+/* Number of kernels this engine launched so far. */
+int amsp_engine_launch_count(const amsp_engine_t* e, uint64_t* n);
+void amsp_engine_destroy(amsp_engine_t* e);
+
+/* ------------------------------------------------------------ kernels */
+/* Raw launchers (device pointers + cudaStream_t passed as void*). */
+
+/* dst[k] = grad(seed, step, rank, start+k) as bf16, k < n */
+int amsp_k_synth_grad(void* dst_bf16, uint64_t start, uint64_t n, uint64_t seed,
+                      int step, int rank, void* stream);
+/* Plain fused AdamW on a contiguous shard: fp32 or bf16 grads (grad_is_bf16),
+ * grad_scale applied, bf16 copy of the updated master written to param_out
+ * (may be NULL). */
+int amsp_k_adamw(const void* grad, int grad_is_bf16, float* master, float* m,
+                 float* v, void* param_out_bf16, uint64_t n, int step,
+                 double lr, double beta1, double beta2, double eps,
+                 double weight_decay, double grad_scale, void* stream);
+/* bf16 -> fp32 upcast with scale (the NCCL-path gradient epilogue). */
+int amsp_k_upcast_scale(const void* src_bf16, float* dst, uint64_t n, float scale,
+                        void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AMSP_C_H_ */

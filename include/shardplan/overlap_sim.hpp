@@ -1,0 +1,4 @@
+// Drop-in forwarding header: the reference path shardplan/overlap_sim.hpp maps onto
+// the single AMSP planner header.
+#pragma once
+#include "amsp/plan.hpp"

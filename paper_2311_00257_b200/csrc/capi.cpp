@@ -1,0 +1,380 @@
+// C-ABI of the planner half (include/amsp_c.h): POD <-> shardplan types and
+// exception -> status translation. Host only; loads without a GPU.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "amsp/plan.hpp"
+#include "amsp_c.h"
+#include "engine/layout.h"
+#include "status.h"
+
+using namespace shardplan;
+
+namespace amsp {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+}  // namespace amsp
+
+struct amsp_profile {
+  BandwidthProfile p;
+};
+
+namespace {
+
+DeviceMesh mesh_in(amsp_mesh_t m) { return {m.per_node, m.nodes}; }
+amsp_mesh_t mesh_out(DeviceMesh m) { return {m.per_node, m.nodes}; }
+
+ShardingPlan plan_in(const amsp_plan_t* p) {
+  if (!p) throw Error("null plan");
+  ShardingPlan s{mesh_in(p->p), mesh_in(p->g), mesh_in(p->os), std::nullopt};
+  if (p->has_secondary) s.secondary_params = mesh_in(p->secondary);
+  return s;
+}
+
+amsp_plan_t plan_out(const ShardingPlan& s) {
+  amsp_plan_t p{};
+  p.p = mesh_out(s.p);
+  p.g = mesh_out(s.g);
+  p.os = mesh_out(s.os);
+  p.has_secondary = s.secondary_params.has_value();
+  if (s.secondary_params) p.secondary = mesh_out(*s.secondary_params);
+  return p;
+}
+
+ClusterSpec cluster_in(const amsp_cluster_t* c) {
+  if (!c) throw Error("null cluster");
+  ClusterSpec s;
+  s.gpus_per_node = c->gpus_per_node;
+  s.node_count = c->node_count;
+  s.gpu_memory_capacity = c->gpu_memory_capacity;
+  s.dp_mesh = mesh_in(c->dp_mesh);
+  s.topology = {c->leaf_count, c->nodes_per_leaf, c->inter_leaf_penalty};
+  return s;
+}
+
+ModelSpec model_in(const amsp_model_t* m) {
+  if (!m) throw Error("null model");
+  ModelSpec s;
+  s.total_params = m->total_params;
+  s.layer_count = m->layer_count;
+  s.modules_per_layer = m->modules_per_layer;
+  if (m->modules_per_layer > 0 && m->module_params)
+    s.module_params.assign(m->module_params, m->module_params + m->modules_per_layer);
+  s.hidden = m->hidden;
+  s.seq_len = m->seq_len;
+  s.micro_batch = m->micro_batch;
+  s.micro_batch_count = m->micro_batch_count;
+  s.vocab = m->vocab;
+  s.bytes_per_param = m->bytes_per_param;
+  s.bytes_per_grad = m->bytes_per_grad;
+  s.bytes_per_os_per_param = m->bytes_per_os_per_param;
+  return s;
+}
+
+CostConfig cost_in(const amsp_cost_config_t* c) {
+  CostConfig s;
+  if (!c) return s;
+  s.bucket_size = c->bucket_size;
+  s.activation_mode = c->activation_mode ? ActivationMode::FullRecompute : ActivationMode::None;
+  s.activation_coeff_full = c->activation_coeff_full;
+  s.activation_coeff_recompute = c->activation_coeff_recompute;
+  s.tmp_in_flight_buckets = c->tmp_in_flight_buckets;
+  s.tmp_include_gather_buffer = c->tmp_include_gather_buffer != 0;
+  s.exact_residual_buckets = c->exact_residual_buckets != 0;
+  s.flops_coeff_param = c->flops_coeff_param;
+  s.flops_coeff_attn = c->flops_coeff_attn;
+  return s;
+}
+
+SimConfig sim_in(const amsp_sim_config_t* c, int k) {
+  SimConfig s;
+  if (!c) return s;
+  if (c->overlap_tier < 0 || c->overlap_tier > 3) throw Error("sim: bad overlap tier");
+  s.overlap_tier = static_cast<OverlapTier>(c->overlap_tier);
+  s.recompute = c->recompute != 0;
+  s.comm_streams = c->comm_streams;
+  s.compute_time_source = c->compute_time_source ? ComputeTimeSource::Table : ComputeTimeSource::Flops;
+  s.peak_flops_per_gpu = c->peak_flops_per_gpu;
+  s.compute_efficiency = c->compute_efficiency;
+  auto take = [k](const double* v) {
+    return v ? std::vector<double>(v, v + k) : std::vector<double>{};
+  };
+  s.fwd_times = take(c->fwd_times);
+  s.bwd_grad_weight_times = take(c->bwd_grad_weight_times);
+  s.bwd_grad_input_times = take(c->bwd_grad_input_times);
+  s.head_fwd_time = c->head_fwd_time;
+  s.head_bwd_time = c->head_bwd_time;
+  return s;
+}
+
+amsp_time_t time_out(const TimeBreakdown& t) {
+  return {t.t_p, t.t_g, t.t_os_allreduce, t.t_os_broadcast, t.total};
+}
+
+amsp_memory_t mem_out(const MemoryBreakdown& m) {
+  return {m.d_params, m.d_grads, m.d_os, m.d_modelstate, m.d_activation, m.d_tmp, m.d_total};
+}
+
+amsp_plan_result_t result_out(const PlanResult& r) {
+  amsp_plan_result_t o{};
+  o.plan = plan_out(r.plan);
+  o.time = time_out(r.time);
+  o.memory = mem_out(r.memory);
+  o.feasible = r.feasible;
+  o.rank = r.rank;
+  return o;
+}
+
+CollectiveKind kind_in(int k) {
+  if (k < 0 || k > 3) throw Error("unknown collective kind " + std::to_string(k));
+  return static_cast<CollectiveKind>(k);
+}
+
+void write_text(const std::string& s, char* buf, size_t cap, size_t* needed) {
+  if (needed) *needed = s.size();
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int amsp_abi_version(void) { return AMSP_ABI_VERSION; }
+
+const char* amsp_last_error(void) { return amsp::g_last_error.c_str(); }
+
+void amsp_cost_config_default(amsp_cost_config_t* c) {
+  if (!c) return;
+  const CostConfig d;
+  c->bucket_size = d.bucket_size;
+  c->activation_mode = 0;
+  c->activation_coeff_full = d.activation_coeff_full;
+  c->activation_coeff_recompute = d.activation_coeff_recompute;
+  c->tmp_in_flight_buckets = d.tmp_in_flight_buckets;
+  c->tmp_include_gather_buffer = d.tmp_include_gather_buffer;
+  c->exact_residual_buckets = d.exact_residual_buckets;
+  c->flops_coeff_param = d.flops_coeff_param;
+  c->flops_coeff_attn = d.flops_coeff_attn;
+}
+
+void amsp_sim_config_default(amsp_sim_config_t* c) {
+  if (!c) return;
+  const SimConfig d;
+  std::memset(c, 0, sizeof(*c));
+  c->overlap_tier = static_cast<int>(d.overlap_tier);
+  c->recompute = d.recompute;
+  c->comm_streams = d.comm_streams;
+  c->compute_time_source = 0;
+  c->peak_flops_per_gpu = d.peak_flops_per_gpu;
+  c->compute_efficiency = d.compute_efficiency;
+}
+
+int amsp_profile_synthetic(double ai, double bi, double ao, double bo,
+                           const amsp_mesh_t* meshes, int n_meshes, const uint64_t* sizes,
+                           int n_sizes, amsp_profile_t** out) {
+  return amsp::guarded([&] {
+    if (!out || n_meshes < 0 || n_sizes < 0) throw Error("null argument");
+    std::vector<DeviceMesh> ms;
+    for (int i = 0; i < n_meshes; ++i) ms.push_back(mesh_in(meshes[i]));
+    std::vector<std::uint64_t> sz(sizes, sizes + n_sizes);
+    auto p = new amsp_profile{synthetic_profile({ai, bi}, {ao, bo}, ms, sz)};
+    *out = p;
+  });
+}
+
+int amsp_profile_from_csv(const char* text, amsp_profile_t** out) {
+  return amsp::guarded([&] {
+    if (!text || !out) throw Error("null argument");
+    *out = new amsp_profile{profile_from_csv(text)};
+  });
+}
+
+int amsp_profile_from_json(const char* text, amsp_profile_t** out) {
+  return amsp::guarded([&] {
+    if (!text || !out) throw Error("null argument");
+    *out = new amsp_profile{profile_from_json(text)};
+  });
+}
+
+int amsp_profile_load(const char* path, amsp_profile_t** out) {
+  return amsp::guarded([&] {
+    if (!path || !out) throw Error("null argument");
+    *out = new amsp_profile{load_profile(path)};
+  });
+}
+
+int amsp_profile_to_json(const amsp_profile_t* p, char* buf, size_t cap, size_t* needed) {
+  return amsp::guarded([&] {
+    if (!p) throw Error("null profile");
+    write_text(profile_to_canonical_json(p->p), buf, cap, needed);
+  });
+}
+
+int amsp_collective_time(const amsp_profile_t* p, int kind, uint64_t size_bytes,
+                         amsp_mesh_t mesh, double* seconds) {
+  return amsp::guarded([&] {
+    if (!p || !seconds) throw Error("null argument");
+    *seconds = p->p.collective_time(kind_in(kind), size_bytes, mesh_in(mesh));
+  });
+}
+
+void amsp_profile_free(amsp_profile_t* p) { delete p; }
+
+int amsp_ring_time(int kind, double size_bytes, int participants, double alpha,
+                   double link_bandwidth, double* seconds) {
+  return amsp::guarded([&] {
+    if (!seconds) throw Error("null argument");
+    *seconds = ring_time(kind_in(kind), size_bytes, participants, {alpha, link_bandwidth});
+  });
+}
+
+int amsp_validate_plan(const amsp_plan_t* plan, const amsp_cluster_t* cluster,
+                       int* n_violations, char* buf, size_t cap) {
+  return amsp::guarded([&] {
+    const ValidationResult v = validate_plan(plan_in(plan), cluster_in(cluster));
+    if (n_violations) *n_violations = static_cast<int>(v.violations.size());
+    std::string text;
+    for (const auto& x : v.violations) text += x.constraint + ":" + x.detail + "\n";
+    write_text(text, buf, cap, nullptr);
+  });
+}
+
+int amsp_preset(const char* name, const amsp_cluster_t* cluster, amsp_plan_t* out) {
+  return amsp::guarded([&] {
+    if (!name || !out) throw Error("null argument");
+    *out = plan_out(preset(name, cluster_in(cluster)));
+  });
+}
+
+int amsp_memory_breakdown(const amsp_model_t* model, const amsp_plan_t* plan,
+                          const amsp_cost_config_t* cfg, amsp_memory_t* out) {
+  return amsp::guarded([&] {
+    if (!out) throw Error("null argument");
+    *out = mem_out(memory_breakdown(model_in(model), plan_in(plan), cost_in(cfg)));
+  });
+}
+
+int amsp_total_comm_time(const amsp_model_t* model, const amsp_cluster_t* cluster,
+                         const amsp_plan_t* plan, const amsp_profile_t* profile,
+                         const amsp_cost_config_t* cfg, amsp_time_t* out) {
+  return amsp::guarded([&] {
+    if (!out || !profile) throw Error("null argument");
+    *out = time_out(total_comm_time(model_in(model), cluster_in(cluster), plan_in(plan),
+                                    profile->p, cost_in(cfg)));
+  });
+}
+
+int amsp_grad_bucket_count(const amsp_model_t* model, const amsp_plan_t* plan,
+                           const amsp_cost_config_t* cfg, uint64_t* out) {
+  return amsp::guarded([&] {
+    if (!out) throw Error("null argument");
+    *out = grad_bucket_count(model_in(model), plan_in(plan), cost_in(cfg));
+  });
+}
+
+int amsp_partition_greedy(const uint64_t* sizes, int n, int shard_count, int* assignment,
+                          uint64_t* shard_sizes) {
+  return amsp::guarded([&] {
+    if (n < 0 || (n > 0 && !sizes)) throw Error("null argument");
+    const TensorPartition p =
+        partition_tensors_greedy(std::vector<std::uint64_t>(sizes, sizes + n), shard_count);
+    if (assignment) std::copy(p.assignment.begin(), p.assignment.end(), assignment);
+    if (shard_sizes) std::copy(p.shard_sizes.begin(), p.shard_sizes.end(), shard_sizes);
+  });
+}
+
+int amsp_enumerate_candidates(const amsp_cluster_t* cluster, amsp_plan_t* plans, int cap,
+                              int* n) {
+  return amsp::guarded([&] {
+    const auto v = enumerate_candidates(cluster_in(cluster));
+    if (n) *n = static_cast<int>(v.size());
+    for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i) plans[i] = plan_out(v[i]);
+  });
+}
+
+int amsp_solve(const amsp_model_t* model, const amsp_cluster_t* cluster,
+               const amsp_profile_t* profile, const amsp_cost_config_t* cfg,
+               amsp_plan_result_t* best, uint64_t* evaluated, uint64_t* filtered,
+               amsp_plan_result_t* all, int cap, int* n_all) {
+  return amsp::guarded([&] {
+    if (!profile) throw Error("null profile");
+    SolveOptions o;
+    o.keep_all_results = all != nullptr || n_all != nullptr;
+    try {
+      const SearchReport r = solve(model_in(model), cluster_in(cluster), profile->p,
+                                   cost_in(cfg), o);
+      if (best) *best = result_out(r.best);
+      if (evaluated) *evaluated = r.candidates_evaluated;
+      if (filtered) *filtered = r.candidates_filtered;
+      if (r.all_results) {
+        if (n_all) *n_all = static_cast<int>(r.all_results->size());
+        for (int i = 0; all && i < cap && i < static_cast<int>(r.all_results->size()); ++i)
+          all[i] = result_out((*r.all_results)[i]);
+      }
+    } catch (const NoFeasiblePlanError& e) {
+      if (best) *best = result_out(e.closest());
+      throw;
+    }
+  });
+}
+
+int amsp_simulate(const amsp_model_t* model, const amsp_cluster_t* cluster,
+                  const amsp_plan_t* plan, const amsp_profile_t* profile,
+                  const amsp_cost_config_t* cfg, const amsp_sim_config_t* sim,
+                  double* step_time, double* compute_idle, int* n_events, char* trace,
+                  size_t trace_cap, size_t* trace_needed) {
+  return amsp::guarded([&] {
+    if (!profile || !model) throw Error("null argument");
+    const ModelSpec m = model_in(model);
+    const EventGraph g = build_schedule(m, cluster_in(cluster), plan_in(plan), profile->p,
+                                        cost_in(cfg), sim_in(sim, m.modules_per_layer));
+    const Timeline t = simulate_step(g);
+    if (step_time) *step_time = t.step_time;
+    if (compute_idle) *compute_idle = bubble_report(t).compute_idle_total;
+    if (n_events) *n_events = static_cast<int>(g.events.size());
+    if (trace || trace_needed) write_text(render_trace(t), trace, trace_cap, trace_needed);
+  });
+}
+
+int amsp_layout_segments(const uint64_t* tensor_sizes, int n_tensors, int shard_count,
+                         int shard, int layout, uint64_t* flat, uint64_t* os, uint64_t* len,
+                         int cap, int* n_segments, uint64_t* owned) {
+  return amsp::guarded([&] {
+    if (n_tensors < 0 || (n_tensors > 0 && !tensor_sizes)) throw Error("null argument");
+    const amsp::ShardLayout L = amsp::shard_layout(
+        std::vector<std::uint64_t>(tensor_sizes, tensor_sizes + n_tensors), shard_count,
+        shard, layout);
+    if (n_segments) *n_segments = static_cast<int>(L.segs.size());
+    if (owned) *owned = L.owned;
+    for (int i = 0; i < cap && i < static_cast<int>(L.segs.size()); ++i) {
+      if (flat) flat[i] = L.segs[i].flat;
+      if (os) os[i] = L.segs[i].os;
+      if (len) len[i] = L.segs[i].len;
+    }
+  });
+}
+
+int amsp_mesh_group(amsp_mesh_t dp, amsp_mesh_t mesh, int rank, int* block, int* position,
+                    int* members, int cap, int* n_members) {
+  return amsp::guarded([&] {
+    const amsp::MeshGroup g = amsp::mesh_group(mesh_in(dp), mesh_in(mesh), rank);
+    if (block) *block = g.block;
+    if (position) *position = g.position;
+    if (n_members) *n_members = static_cast<int>(g.members.size());
+    for (int i = 0; members && i < cap && i < static_cast<int>(g.members.size()); ++i)
+      members[i] = g.members[i];
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,519 @@
+// The AMSP step engine: owns one rank's model-state buffers on its B200,
+// maps the peers' buffers over NVLink (cudaIpc), and runs the step
+//   barrier -> fused reduce + AdamW + gather kernel -> barrier
+// on a CUDA stream. One engine per GPU / process.
+//
+// Memory layout per rank (s_p = 1 plans: ZeRO-1 / ZeRO-2 / AMSP partial OS):
+//   shared allocation (exported to peers):
+//     grads  bf16 [Phi]   this rank's local gradient (backward output)
+//     params bf16 [Phi]   replicated parameters, written by the OS owners
+//     flags  u32 [64]     cross-GPU barrier slots (slot r written by rank r)
+//   private allocation:
+//     master, exp_avg, exp_avg_sq fp32 [owned]  the rank's OS shard
+//     segment table, stats, error flag
+// Φ = 6.74e9 (LLaMA-7B) => 27 GB shared + 81 GB / s_os private; fits the
+// 180 GB of one B200 even unsharded (s_os = 1).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "amsp_c.h"
+#include "kernels.h"
+#include "layout.h"
+#include "../status.h"
+
+using shardplan::DeviceMesh;
+using shardplan::Error;
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw amsp::CudaFailure(std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
+}
+
+constexpr std::size_t kAlign = 256;
+std::size_t align_up(std::size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+DeviceMesh to_mesh(amsp_mesh_t m) { return DeviceMesh{m.per_node, m.nodes}; }
+
+}  // namespace
+
+struct amsp_engine {
+  amsp_engine_config_t cfg{};
+  std::vector<std::uint64_t> tensor_sizes;
+  std::uint64_t phi = 0;
+  int world = 1, rank = 0;
+  amsp::ShardLayout layout;
+  amsp::MeshGroup os_group;
+  int replicas = 1;
+
+  // Shared region and its offsets (identical on every rank).
+  char* shared = nullptr;
+  std::size_t shared_bytes = 0, off_grads = 0, off_params = 0, off_flags = 0;
+  void* peer_base[amsp::kMaxRanks] = {};
+  bool imported = false;
+  bool local_linked = false;  // single-GPU emulation: no barriers
+
+  float* master = nullptr;
+  float* exp_avg = nullptr;
+  float* exp_avg_sq = nullptr;
+  char* priv = nullptr;
+  amsp::Seg* d_segs = nullptr;
+  float* stats = nullptr;
+  int* err = nullptr;
+  uint32_t** d_peer_flags = nullptr;
+  int nseg = 0, ntiles = 0, grid = 0;
+  std::uint64_t device_bytes = 0;
+
+  cudaStream_t own_stream = nullptr;
+  uint32_t epoch = 0;
+  // Optional CUDA-event bracketing of every fused launch (bench roofline).
+  bool time_kernel = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kernel_events;
+  std::size_t kernel_events_used = 0;
+  std::uint64_t launches = 0;
+
+  uint16_t* grads_of(int r) const {
+    return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_grads);
+  }
+  uint16_t* params_of(int r) const {
+    return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_params);
+  }
+  uint32_t* flags_of(int r) const {
+    return reinterpret_cast<uint32_t*>(static_cast<char*>(peer_base[r]) + off_flags);
+  }
+  cudaStream_t pick(void* s) const {
+    return s ? static_cast<cudaStream_t>(s) : own_stream;
+  }
+  void use_device() const { ck(cudaSetDevice(cfg.device), "cudaSetDevice"); }
+
+  void publish_peer_flags() {
+    uint32_t* h[amsp::kMaxRanks] = {};
+    for (int r = 0; r < world; ++r) h[r] = flags_of(r);
+    ck(cudaMemcpy(d_peer_flags, h, sizeof(h), cudaMemcpyHostToDevice),
+       "copy peer flag table");
+  }
+
+  void barrier(cudaStream_t s) {
+    if (world == 1 || local_linked) return;
+    ++epoch;
+    ck(amsp::launch_barrier(d_peer_flags, world, rank, epoch, err, s), "barrier launch");
+    ++launches;
+  }
+
+  void check_err() {
+    int h = 0;
+    ck(cudaMemcpy(&h, err, sizeof(int), cudaMemcpyDeviceToHost), "read error flag");
+    if (h) throw amsp::CudaFailure("cross-GPU barrier timed out (a peer did not arrive)");
+  }
+
+  void step(int t, cudaStream_t s) {
+    if (t < 1) throw Error("engine: step index must be >= 1");
+    if (world > 1 && !imported)
+      throw Error("engine: peers not imported (amsp_engine_import_handles)");
+    amsp::FusedArgs a{};
+    a.segs = d_segs;
+    a.nseg = nseg;
+    a.ntiles = ntiles;
+    for (int r = 0; r < world; ++r) a.grads[r] = grads_of(r);
+    a.ndst = static_cast<int>(os_group.members.size());
+    for (int d = 0; d < a.ndst; ++d) a.dsts[d] = params_of(os_group.members[d]);
+    a.master = master;
+    a.exp_avg = exp_avg;
+    a.exp_avg_sq = exp_avg_sq;
+    a.s = amsp::make_adam_scalars(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
+                                  cfg.weight_decay, t, 1.0 / world);
+    a.stats = stats;
+    ck(cudaMemsetAsync(stats, 0, 2 * sizeof(float), s), "reset stats");
+    barrier(s);  // every rank's gradients are complete
+    cudaEvent_t t_end = nullptr;
+    if (time_kernel && ntiles > 0) {
+      if (kernel_events_used == kernel_events.size()) {
+        cudaEvent_t x, y;
+        ck(cudaEventCreate(&x), "event");
+        ck(cudaEventCreate(&y), "event");
+        kernel_events.emplace_back(x, y);
+      }
+      auto& ev = kernel_events[kernel_events_used++];
+      ck(cudaEventRecord(ev.first, s), "event record");
+      t_end = ev.second;
+    }
+    ck(amsp::launch_fused_step(a, world, grid, s), "fused step launch");
+    if (t_end) ck(cudaEventRecord(t_end, s), "event record");
+    if (ntiles > 0) ++launches;
+    barrier(s);  // every owner's parameter stores have landed
+  }
+};
+
+namespace {
+
+void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
+  if (!cfg || !out) throw Error("engine: null argument");
+  auto e = std::make_unique<amsp_engine>();
+  e->cfg = *cfg;
+  if (cfg->n_tensors < 1 || !cfg->tensor_sizes) throw Error("engine: no tensors");
+  e->tensor_sizes.assign(cfg->tensor_sizes, cfg->tensor_sizes + cfg->n_tensors);
+  for (auto s : e->tensor_sizes) {
+    if (s == 0) throw Error("engine: tensor sizes must be positive");
+    e->phi += s;
+  }
+  e->cfg.tensor_sizes = nullptr;
+  const DeviceMesh dp = to_mesh(cfg->dp_mesh);
+  e->world = dp.size();
+  e->rank = cfg->rank;
+  if (e->world < 1 || e->world > amsp::kMaxRanks)
+    throw Error("engine: dp mesh " + shardplan::to_string(dp) +
+                " outside the 1..8 GPU NVSwitch domain of one node");
+  if (e->rank < 0 || e->rank >= e->world) throw Error("engine: rank out of range");
+
+  // Plan semantics come from the planner's own validator.
+  shardplan::ShardingPlan plan{to_mesh(cfg->plan.p), to_mesh(cfg->plan.g),
+                               to_mesh(cfg->plan.os), std::nullopt};
+  shardplan::ClusterSpec cl;
+  cl.gpus_per_node = dp.per_node;
+  cl.node_count = dp.nodes;
+  cl.gpu_memory_capacity = 1;
+  cl.dp_mesh = dp;
+  cl.topology = {dp.nodes, 1, 1.0};
+  const auto v = shardplan::validate_plan(plan, cl);
+  if (!v.ok())
+    throw Error("engine: plan " + shardplan::to_string(plan) + " violates " +
+                v.violations.front().constraint);
+  if (plan.sp() != 1)
+    throw Error("engine: parameter sharding (s_p > 1) is not implemented by the "
+                "B200 engine yet; plan " + shardplan::to_string(plan));
+
+  e->os_group = amsp::mesh_group(dp, plan.os, e->rank);
+  e->replicas = e->world / plan.sos();
+  e->layout = amsp::shard_layout(e->tensor_sizes, plan.sos(), e->os_group.position,
+                                 cfg->layout);
+
+  e->use_device();
+  ck(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "stream");
+
+  // Shared region.
+  e->off_grads = 0;
+  e->off_params = align_up(e->phi * 2);
+  e->off_flags = e->off_params + align_up(e->phi * 2);
+  e->shared_bytes = e->off_flags + align_up(64 * sizeof(uint32_t));
+  ck(cudaMalloc(&e->shared, e->shared_bytes), "cudaMalloc shared");
+  ck(cudaMemset(e->shared + e->off_flags, 0, 64 * sizeof(uint32_t)), "zero flags");
+  for (int r = 0; r < e->world; ++r) e->peer_base[r] = e->shared;
+
+  // Private region: OS shard + segment table + stats + error flag + flags table.
+  std::vector<amsp::Seg> segs;
+  long long tiles = 0;
+  for (const auto& s : e->layout.segs) {
+    segs.push_back({s.flat, s.os, s.len, static_cast<unsigned long long>(tiles)});
+    tiles += static_cast<long long>((s.len + amsp::kTile - 1) / amsp::kTile);
+  }
+  if (tiles > 0x7fffffffLL) throw Error("engine: shard too large");
+  e->nseg = static_cast<int>(segs.size());
+  e->ntiles = static_cast<int>(tiles);
+  const std::size_t n = e->layout.owned;
+  const std::size_t off_m = align_up(n * 4), off_v = off_m + align_up(n * 4);
+  const std::size_t off_seg = off_v + align_up(n * 4);
+  const std::size_t off_stats = off_seg + align_up(std::max<std::size_t>(segs.size(), 1) * sizeof(amsp::Seg));
+  const std::size_t off_err = off_stats + kAlign;
+  const std::size_t off_tab = off_err + kAlign;
+  const std::size_t priv_bytes = off_tab + kAlign;
+  ck(cudaMalloc(&e->priv, priv_bytes), "cudaMalloc optimizer state");
+  e->master = reinterpret_cast<float*>(e->priv);
+  e->exp_avg = reinterpret_cast<float*>(e->priv + off_m);
+  e->exp_avg_sq = reinterpret_cast<float*>(e->priv + off_v);
+  e->d_segs = reinterpret_cast<amsp::Seg*>(e->priv + off_seg);
+  e->stats = reinterpret_cast<float*>(e->priv + off_stats);
+  e->err = reinterpret_cast<int*>(e->priv + off_err);
+  e->d_peer_flags = reinterpret_cast<uint32_t**>(e->priv + off_tab);
+  if (!segs.empty())
+    ck(cudaMemcpy(e->d_segs, segs.data(), segs.size() * sizeof(amsp::Seg),
+                  cudaMemcpyHostToDevice),
+       "copy segments");
+  ck(cudaMemset(e->priv + off_stats, 0, 2 * kAlign), "zero stats/err");
+  e->publish_peer_flags();
+  e->device_bytes = e->shared_bytes + priv_bytes;
+
+  int sms = 148;
+  ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device), "sm count");
+  const int per_sm = amsp::fused_blocks_per_sm(e->world);
+  e->grid = std::max(1, std::min(e->ntiles, sms * per_sm));
+  *out = e.release();
+}
+
+}  // namespace
+
+extern "C" {
+
+int amsp_engine_create(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
+  return amsp::guarded([&] { create_engine(cfg, out); });
+}
+
+int amsp_engine_info(const amsp_engine_t* e, amsp_engine_info_t* info) {
+  return amsp::guarded([&] {
+    if (!e || !info) throw Error("engine: null argument");
+    info->total_params = e->phi;
+    info->owned = e->layout.owned;
+    info->n_segments = e->nseg;
+    info->world = e->world;
+    info->os_block = e->os_group.block;
+    info->os_position = e->os_group.position;
+    info->os_group_size = static_cast<int>(e->os_group.members.size());
+    info->replica_count = e->replicas;
+    info->ntiles = e->ntiles;
+    info->grid = e->grid;
+    info->block = amsp::kBlock;
+    info->grads = e->grads_of(e->rank);
+    info->params = e->params_of(e->rank);
+    info->master = e->master;
+    info->exp_avg = e->exp_avg;
+    info->exp_avg_sq = e->exp_avg_sq;
+    info->device_bytes = e->device_bytes;
+  });
+}
+
+int amsp_engine_export_handle(amsp_engine_t* e, void* handle64) {
+  return amsp::guarded([&] {
+    if (!e || !handle64) throw Error("engine: null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == AMSP_IPC_HANDLE_BYTES);
+    e->use_device();
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, e->shared), "cudaIpcGetMemHandle");
+    std::memcpy(handle64, &h, sizeof(h));
+  });
+}
+
+int amsp_engine_import_handles(amsp_engine_t* e, const void* handles, int world) {
+  return amsp::guarded([&] {
+    if (!e || !handles) throw Error("engine: null argument");
+    if (world != e->world)
+      throw Error("engine: got " + std::to_string(world) + " handles for a world of " +
+                  std::to_string(e->world));
+    e->use_device();
+    for (int r = 0; r < world; ++r) {
+      if (r == e->rank) continue;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const char*>(handles) + r * AMSP_IPC_HANDLE_BYTES, sizeof(h));
+      void* p = nullptr;
+      ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      e->peer_base[r] = p;
+    }
+    e->publish_peer_flags();
+    e->imported = true;
+  });
+}
+
+int amsp_engine_link_local(amsp_engine_t* const* engines, int n) {
+  return amsp::guarded([&] {
+    if (!engines || n < 1) throw Error("engine: null argument");
+    for (int r = 0; r < n; ++r) {
+      const amsp_engine* e = engines[r];
+      if (!e || e->world != n || e->rank != r || e->cfg.device != engines[0]->cfg.device ||
+          e->phi != engines[0]->phi)
+        throw Error("engine: link_local needs ranks 0..n-1 of one group on one device");
+    }
+    for (int r = 0; r < n; ++r) {
+      amsp_engine* e = engines[r];
+      for (int q = 0; q < n; ++q) e->peer_base[q] = engines[q]->shared;
+      e->use_device();
+      e->publish_peer_flags();
+      e->imported = true;
+      e->local_linked = true;
+    }
+  });
+}
+
+int amsp_engine_init_state(amsp_engine_t* e, void* stream) {
+  return amsp::guarded([&] {
+    if (!e) throw Error("engine: null argument");
+    e->use_device();
+    cudaStream_t s = e->pick(stream);
+    ck(amsp::launch_init_params(e->params_of(e->rank), e->phi, e->cfg.seed, s), "init params");
+    ck(amsp::launch_init_state(e->d_segs, e->nseg, e->ntiles, e->master, e->exp_avg,
+                               e->exp_avg_sq, e->cfg.seed, std::max(e->grid, 1), s),
+       "init state");
+    e->launches += 2;
+  });
+}
+
+int amsp_engine_synth_grads(amsp_engine_t* e, int step, void* stream) {
+  return amsp::guarded([&] {
+    if (!e) throw Error("engine: null argument");
+    e->use_device();
+    ck(amsp::launch_synth_grad(e->grads_of(e->rank), 0, e->phi, e->cfg.seed, step,
+                               e->rank, e->pick(stream)),
+       "synth grads");
+    ++e->launches;
+  });
+}
+
+int amsp_engine_step(amsp_engine_t* e, int step, void* stream) {
+  return amsp::guarded([&] {
+    if (!e) throw Error("engine: null argument");
+    e->use_device();
+    e->step(step, e->pick(stream));
+  });
+}
+
+int amsp_engine_step_host(amsp_engine_t* e, int step, const void* host_grads,
+                          float* host_stats, void* stream) {
+  return amsp::guarded([&] {
+    if (!e || !host_grads) throw Error("engine: null argument");
+    e->use_device();
+    cudaStream_t s = e->pick(stream);
+    const std::size_t total = e->phi * 2, chunk = std::size_t{1} << 30;
+    char* dst = reinterpret_cast<char*>(e->grads_of(e->rank));
+    const char* src = static_cast<const char*>(host_grads);
+    for (std::size_t off = 0; off < total; off += chunk)
+      ck(cudaMemcpyAsync(dst + off, src + off, std::min(chunk, total - off),
+                         cudaMemcpyHostToDevice, s),
+         "H2D gradients");
+    e->step(step, s);
+    if (host_stats)
+      ck(cudaMemcpyAsync(host_stats, e->stats, 2 * sizeof(float), cudaMemcpyDeviceToHost, s),
+         "D2H stats");
+    ck(cudaStreamSynchronize(s), "step sync");
+    e->check_err();
+  });
+}
+
+int amsp_engine_stats(amsp_engine_t* e, float* stats2) {
+  return amsp::guarded([&] {
+    if (!e || !stats2) throw Error("engine: null argument");
+    e->use_device();
+    ck(cudaDeviceSynchronize(), "sync");
+    e->check_err();
+    ck(cudaMemcpy(stats2, e->stats, 2 * sizeof(float), cudaMemcpyDeviceToHost), "read stats");
+  });
+}
+
+static void* buffer_ptr(amsp_engine_t* e, int which, std::size_t* elem, std::uint64_t* count) {
+  switch (which) {
+    case 0: *elem = 2; *count = e->phi; return e->grads_of(e->rank);
+    case 1: *elem = 2; *count = e->phi; return e->params_of(e->rank);
+    case 2: *elem = 4; *count = e->layout.owned; return e->master;
+    case 3: *elem = 4; *count = e->layout.owned; return e->exp_avg;
+    case 4: *elem = 4; *count = e->layout.owned; return e->exp_avg_sq;
+    default: throw Error("engine: unknown buffer id " + std::to_string(which));
+  }
+}
+
+int amsp_engine_read(amsp_engine_t* e, int which, uint64_t offset, uint64_t count,
+                     void* host_dst) {
+  return amsp::guarded([&] {
+    if (!e || (!host_dst && count)) throw Error("engine: null argument");
+    std::size_t elem = 0;
+    std::uint64_t n = 0;
+    char* p = static_cast<char*>(buffer_ptr(e, which, &elem, &n));
+    if (offset > n || count > n - offset) throw Error("engine: read out of range");
+    e->use_device();
+    ck(cudaDeviceSynchronize(), "sync");
+    e->check_err();
+    if (count) ck(cudaMemcpy(host_dst, p + offset * elem, count * elem, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t count,
+                      const void* host_src) {
+  return amsp::guarded([&] {
+    if (!e || (!host_src && count)) throw Error("engine: null argument");
+    std::size_t elem = 0;
+    std::uint64_t n = 0;
+    char* p = static_cast<char*>(buffer_ptr(e, which, &elem, &n));
+    if (offset > n || count > n - offset) throw Error("engine: write out of range");
+    e->use_device();
+    ck(cudaDeviceSynchronize(), "sync");
+    if (count) ck(cudaMemcpy(p + offset * elem, host_src, count * elem, cudaMemcpyHostToDevice), "H2D");
+  });
+}
+
+int amsp_engine_time_kernel(amsp_engine_t* e, int enable) {
+  return amsp::guarded([&] {
+    if (!e) throw Error("engine: null argument");
+    e->time_kernel = enable != 0;
+    e->kernel_events_used = 0;
+  });
+}
+
+int amsp_engine_kernel_ms(amsp_engine_t* e, double* total_ms, int* launches) {
+  return amsp::guarded([&] {
+    if (!e || !total_ms) throw Error("engine: null argument");
+    e->use_device();
+    double sum = 0.0;
+    for (std::size_t i = 0; i < e->kernel_events_used; ++i) {
+      ck(cudaEventSynchronize(e->kernel_events[i].second), "event sync");
+      float ms = 0.0f;
+      ck(cudaEventElapsedTime(&ms, e->kernel_events[i].first, e->kernel_events[i].second),
+         "event elapsed");
+      sum += ms;
+    }
+    *total_ms = sum;
+    if (launches) *launches = static_cast<int>(e->kernel_events_used);
+    e->kernel_events_used = 0;
+  });
+}
+
+int amsp_engine_launch_count(const amsp_engine_t* e, uint64_t* n) {
+  return amsp::guarded([&] {
+    if (!e || !n) throw Error("engine: null argument");
+    *n = e->launches;
+  });
+}
+
+void amsp_engine_destroy(amsp_engine_t* e) {
+  if (!e) return;
+  cudaSetDevice(e->cfg.device);
+  cudaDeviceSynchronize();
+  for (int r = 0; r < e->world; ++r)
+    if (!e->local_linked && r != e->rank && e->peer_base[r] && e->peer_base[r] != e->shared)
+      cudaIpcCloseMemHandle(e->peer_base[r]);
+  cudaFree(e->shared);
+  cudaFree(e->priv);
+  if (e->own_stream) cudaStreamDestroy(e->own_stream);
+  for (auto& ev : e->kernel_events) {
+    cudaEventDestroy(ev.first);
+    cudaEventDestroy(ev.second);
+  }
+  delete e;
+}
+
+// ------------------------------------------------------------ raw kernels
+
+int amsp_k_synth_grad(void* dst_bf16, uint64_t start, uint64_t n, uint64_t seed,
+                      int step, int rank, void* stream) {
+  return amsp::guarded([&] {
+    ck(amsp::launch_synth_grad(static_cast<uint16_t*>(dst_bf16), start, n, seed, step,
+                               rank, static_cast<cudaStream_t>(stream)),
+       "synth grad");
+  });
+}
+
+int amsp_k_adamw(const void* grad, int grad_is_bf16, float* master, float* m, float* v,
+                 void* param_out_bf16, uint64_t n, int step, double lr, double beta1,
+                 double beta2, double eps, double weight_decay, double grad_scale,
+                 void* stream) {
+  return amsp::guarded([&] {
+    if (step < 1) throw Error("adamw: step index must be >= 1");
+    const amsp::AdamScalars s =
+        amsp::make_adam_scalars(lr, beta1, beta2, eps, weight_decay, step, grad_scale);
+    ck(amsp::launch_adamw_flat(grad, grad_is_bf16 != 0, master, m, v,
+                               static_cast<uint16_t*>(param_out_bf16), n, s,
+                               static_cast<cudaStream_t>(stream)),
+       "adamw");
+  });
+}
+
+int amsp_k_upcast_scale(const void* src_bf16, float* dst, uint64_t n, float scale,
+                        void* stream) {
+  return amsp::guarded([&] {
+    ck(amsp::launch_upcast_scale(static_cast<const uint16_t*>(src_bf16), dst, n, scale,
+                                 static_cast<cudaStream_t>(stream)),
+       "upcast");
+  });
+}
+
+}  // extern "C"

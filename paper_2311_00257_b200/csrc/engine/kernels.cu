@@ -1,0 +1,408 @@
+// AMSP step kernels for B200 (sm_100a).
+//
+// The hot op is fused_step_kernel: for every element of this rank's
+// optimizer-state shard it
+//   1. pulls the bf16 gradient of every data-parallel rank over NVLink
+//      (peer pointers mapped with cudaIpc), sums them in fp32 in a fixed
+//      rank order and scales by 1/W  — the reduce-scatter inside the OS
+//      group plus the cross-replica sum, with select & drop implicit
+//      (cost_model.cpp:98-105 charges it as AR + drop);
+//   2. applies AdamW to the fp32 master / m / v shard (HBM-bound);
+//   3. downcasts the new master to bf16 and stores it into the parameter
+//      buffer of every rank of the OS group — the all-gather / inter-tensor
+//      broadcast of updated shards (cost_model.cpp:107-117), written
+//      straight into each peer's gathered buffer.
+// One launch therefore replaces AR(or RS) + upcast + Adam + downcast + AG.
+// There is no tensor-core work (no contraction): the kernel is bounded by
+// HBM and NVLink bandwidth and is written as a persistent grid of 256-thread
+// CTAs streaming 128-bit vectors with several independent loads in flight.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace amsp {
+
+AdamScalars make_adam_scalars(double lr, double beta1, double beta2, double eps,
+                              double weight_decay, int step, double grad_scale) {
+  const double bc1 = 1.0 - std::pow(beta1, static_cast<double>(step));
+  const double bc2 = 1.0 - std::pow(beta2, static_cast<double>(step));
+  AdamScalars s;
+  s.beta1 = static_cast<float>(beta1);
+  s.omb1 = static_cast<float>(1.0 - beta1);
+  s.beta2 = static_cast<float>(beta2);
+  s.omb2 = static_cast<float>(1.0 - beta2);
+  s.step_size = static_cast<float>(lr / bc1);
+  s.inv_sqrt_bc2 = static_cast<float>(1.0 / std::sqrt(bc2));
+  s.eps = static_cast<float>(eps);
+  s.decay = static_cast<float>(1.0 - lr * weight_decay);
+  s.grad_scale = static_cast<float>(grad_scale);
+  return s;
+}
+
+namespace {
+
+// Segment owning `tile` (largest s with segs[s].tile0 <= tile).
+__device__ __forceinline__ Seg find_seg(const Seg* segs, int nseg, int tile) {
+  int lo = 0, hi = nseg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(&segs[mid].tile0) <= static_cast<unsigned long long>(tile))
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  Seg s;
+  s.flat = __ldg(&segs[lo].flat);
+  s.os = __ldg(&segs[lo].os);
+  s.len = __ldg(&segs[lo].len);
+  s.tile0 = __ldg(&segs[lo].tile0);
+  return s;
+}
+
+template <int W>
+__device__ __forceinline__ float reduce_scalar(const FusedArgs& a,
+                                               unsigned long long idx) {
+  float g = bf16_at(a.grads[0][idx]);
+#pragma unroll
+  for (int r = 1; r < W; ++r) g = __fadd_rn(g, bf16_at(a.grads[r][idx]));
+  return __fmul_rn(g, a.s.grad_scale);
+}
+
+// Element-wise path for ragged tails and unaligned segments.
+template <int W>
+__device__ void scalar_elems(const FusedArgs& a, const Seg& sg,
+                             unsigned long long e, float& sq) {
+  const unsigned long long end = e + 8 < sg.len ? e + 8 : sg.len;
+  for (; e < end; ++e) {
+    const unsigned long long f = sg.flat + e, o = sg.os + e;
+    const float g = reduce_scalar<W>(a, f);
+    float p = a.master[o], m = a.exp_avg[o], v = a.exp_avg_sq[o];
+    adamw(a.s, g, p, m, v);
+    a.master[o] = p;
+    a.exp_avg[o] = m;
+    a.exp_avg_sq[o] = v;
+    const uint16_t b = to_bf16(p);
+    for (int d = 0; d < a.ndst; ++d) a.dsts[d][f] = b;
+    sq += g * g;
+  }
+}
+
+// U = 8-element vectors with all loads in flight before any math.
+template <int W, int U>
+__global__ void __launch_bounds__(kBlock)
+fused_step_kernel(const FusedArgs a) {
+  float sq = 0.0f;
+  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    const Seg sg = find_seg(a.segs, a.nseg, tile);
+    const unsigned long long base =
+        (static_cast<unsigned long long>(tile) - sg.tile0) * kTile;
+    const bool aligned = ((sg.flat | sg.os) & 7ull) == 0;
+#pragma unroll 1
+    for (int it = 0; it < kVecPerThread; it += U) {
+      unsigned long long e[U];
+      bool full[U];
+      uint4 graw[U][W];
+      float4 p[U][2], m[U][2], v[U][2];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        e[u] = base + (static_cast<unsigned long long>(it + u) * kBlock + threadIdx.x) * 8ull;
+        full[u] = aligned && e[u] + 8 <= sg.len;
+        if (full[u]) {
+          const unsigned long long f = sg.flat + e[u], o = sg.os + e[u];
+#pragma unroll
+          for (int r = 0; r < W; ++r) graw[u][r] = ld_ro_v4(a.grads[r] + f);
+          p[u][0] = ld_state_v4(a.master + o);
+          p[u][1] = ld_state_v4(a.master + o + 4);
+          m[u][0] = ld_state_v4(a.exp_avg + o);
+          m[u][1] = ld_state_v4(a.exp_avg + o + 4);
+          v[u][0] = ld_state_v4(a.exp_avg_sq + o);
+          v[u][1] = ld_state_v4(a.exp_avg_sq + o + 4);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (full[u]) {
+          const unsigned long long f = sg.flat + e[u], o = sg.os + e[u];
+          float* pf = reinterpret_cast<float*>(&p[u][0]);
+          float* mf = reinterpret_cast<float*>(&m[u][0]);
+          float* vf = reinterpret_cast<float*>(&v[u][0]);
+          uint32_t packed[4];
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const uint32_t* g0 = reinterpret_cast<const uint32_t*>(&graw[u][0]);
+            float glo = bf16_lo(g0[w]), ghi = bf16_hi(g0[w]);
+#pragma unroll
+            for (int r = 1; r < W; ++r) {
+              const uint32_t* gr = reinterpret_cast<const uint32_t*>(&graw[u][r]);
+              glo = __fadd_rn(glo, bf16_lo(gr[w]));
+              ghi = __fadd_rn(ghi, bf16_hi(gr[w]));
+            }
+            glo = __fmul_rn(glo, a.s.grad_scale);
+            ghi = __fmul_rn(ghi, a.s.grad_scale);
+            sq += glo * glo + ghi * ghi;
+            // Element order inside the vector: 2w, 2w+1 (p/m/v are float4 x2
+            // laid out contiguously in registers).
+            const int j = 2 * w;
+            adamw(a.s, glo, pf[j], mf[j], vf[j]);
+            adamw(a.s, ghi, pf[j + 1], mf[j + 1], vf[j + 1]);
+            packed[w] = pack_bf16x2(pf[j], pf[j + 1]);
+          }
+          st_stream_v4(a.master + o, p[u][0]);
+          st_stream_v4(a.master + o + 4, p[u][1]);
+          st_stream_v4(a.exp_avg + o, m[u][0]);
+          st_stream_v4(a.exp_avg + o + 4, m[u][1]);
+          st_stream_v4(a.exp_avg_sq + o, v[u][0]);
+          st_stream_v4(a.exp_avg_sq + o + 4, v[u][1]);
+          const uint4 out = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+          for (int d = 0; d < a.ndst; ++d) st_v4(a.dsts[d] + f, out);
+        } else if (e[u] < sg.len) {
+          scalar_elems<W>(a, sg, e[u], sq);
+        }
+      }
+    }
+  }
+  // Peer parameter stores must be visible system-wide before the trailing
+  // cross-GPU barrier releases the other ranks.
+  __threadfence_system();
+  if (a.stats != nullptr) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    __shared__ float part[kBlock / 32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.0f;
+      for (int i = 0; i < kBlock / 32; ++i) t += part[i];
+      atomicAdd(a.stats, t);
+    }
+  }
+}
+
+// Cross-GPU barrier over NVLink: thread r publishes this rank's epoch into
+// rank r's flag array (slot `rank`) and waits for rank r's epoch in its own
+// array. Bounded wait: after ~20 s it raises *err instead of hanging.
+__global__ void barrier_kernel(uint32_t* const* peer_flags, int world, int rank,
+                               uint32_t epoch, int* err) {
+  const int t = threadIdx.x;
+  __threadfence_system();
+  if (t < world) {
+    uint32_t* slot = peer_flags[t] + rank;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch)
+                 : "memory");
+    const uint32_t* mine = peer_flags[rank] + t;
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      uint32_t seen;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];"
+                   : "=r"(seen)
+                   : "l"(mine)
+                   : "memory");
+      if (static_cast<int32_t>(seen - epoch) >= 0) break;
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 20000000000ull) {
+        atomicExch(err, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void init_params_kernel(uint16_t* __restrict__ p, unsigned long long n,
+                                   uint64_t seed) {
+  const unsigned long long stride = 8ull * gridDim.x * blockDim.x;
+  for (unsigned long long i = 8ull * (blockIdx.x * blockDim.x + threadIdx.x); i < n;
+       i += stride) {
+    if (i + 8 <= n) {
+      uint32_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        w[k] = pack_bf16x2(master_init(seed, i + 2 * k), master_init(seed, i + 2 * k + 1));
+      st_v4(p + i, make_uint4(w[0], w[1], w[2], w[3]));
+    } else {
+      for (unsigned long long k = i; k < n; ++k) p[k] = to_bf16(master_init(seed, k));
+    }
+  }
+}
+
+__global__ void init_state_kernel(const Seg* segs, int nseg, int ntiles,
+                                  float* master, float* m, float* v, uint64_t seed) {
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const Seg sg = find_seg(segs, nseg, tile);
+    const unsigned long long base =
+        (static_cast<unsigned long long>(tile) - sg.tile0) * kTile;
+    for (unsigned long long e = base + threadIdx.x;
+         e < base + kTile && e < sg.len; e += blockDim.x) {
+      master[sg.os + e] = master_init(seed, sg.flat + e);
+      m[sg.os + e] = 0.0f;
+      v[sg.os + e] = 0.0f;
+    }
+  }
+}
+
+__global__ void synth_grad_kernel(uint16_t* __restrict__ dst, unsigned long long start,
+                                  unsigned long long n, uint64_t seed, uint32_t step,
+                                  uint32_t rank) {
+  const unsigned long long stride = 8ull * gridDim.x * blockDim.x;
+  for (unsigned long long i = 8ull * (blockIdx.x * blockDim.x + threadIdx.x); i < n;
+       i += stride) {
+    if (i + 8 <= n && ((reinterpret_cast<uintptr_t>(dst + i) & 15) == 0)) {
+      uint32_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        w[k] = pack_bf16x2(grad_value(seed, step, rank, start + i + 2 * k),
+                           grad_value(seed, step, rank, start + i + 2 * k + 1));
+      st_v4(dst + i, make_uint4(w[0], w[1], w[2], w[3]));
+    } else {
+      const unsigned long long end = i + 8 < n ? i + 8 : n;
+      for (unsigned long long k = i; k < end; ++k)
+        dst[k] = to_bf16(grad_value(seed, step, rank, start + k));
+    }
+  }
+}
+
+// Plain AdamW over a contiguous shard (the NCCL-path optimizer and the raw
+// amsp_k_adamw launcher).
+template <bool kBf16Grad>
+__global__ void adamw_flat_kernel(const void* __restrict__ grad, float* master, float* m,
+                                  float* v, uint16_t* param_out, unsigned long long n,
+                                  AdamScalars s) {
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float g = kBf16Grad ? bf16_at(static_cast<const uint16_t*>(grad)[i])
+                        : static_cast<const float*>(grad)[i];
+    g = __fmul_rn(g, s.grad_scale);
+    float p = master[i], mm = m[i], vv = v[i];
+    adamw(s, g, p, mm, vv);
+    master[i] = p;
+    m[i] = mm;
+    v[i] = vv;
+    if (param_out) param_out[i] = to_bf16(p);
+  }
+}
+
+__global__ void upcast_scale_kernel(const uint16_t* __restrict__ src, float* __restrict__ dst,
+                                    unsigned long long n, float scale) {
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = __fmul_rn(bf16_at(src[i]), scale);
+}
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, c = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    return c;
+  }();
+  return n;
+}
+
+template <int W, int U>
+int occupancy_of() {
+  int blocks = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fused_step_kernel<W, U>, kBlock, 0);
+  return blocks > 0 ? blocks : 1;
+}
+
+}  // namespace
+
+// Wide reductions (W > 4) keep one vector in flight per thread to stay
+// within the register budget; W <= 4 keeps two.
+#define AMSP_FOR_WORLD(W_, CALL)           \
+  switch (W_) {                            \
+    case 1: CALL(1, 2); break;             \
+    case 2: CALL(2, 2); break;             \
+    case 3: CALL(3, 2); break;             \
+    case 4: CALL(4, 2); break;             \
+    case 5: CALL(5, 1); break;             \
+    case 6: CALL(6, 1); break;             \
+    case 7: CALL(7, 1); break;             \
+    case 8: CALL(8, 1); break;             \
+    default: return cudaErrorInvalidValue; \
+  }
+
+int fused_blocks_per_sm(int world) {
+  int b = 1;
+  auto get = [&](auto f) { b = f(); };
+#define AMSP_OCC(W, U) get([] { return occupancy_of<W, U>(); })
+  switch (world) {
+    case 1: AMSP_OCC(1, 2); break;
+    case 2: AMSP_OCC(2, 2); break;
+    case 3: AMSP_OCC(3, 2); break;
+    case 4: AMSP_OCC(4, 2); break;
+    case 5: AMSP_OCC(5, 1); break;
+    case 6: AMSP_OCC(6, 1); break;
+    case 7: AMSP_OCC(7, 1); break;
+    case 8: AMSP_OCC(8, 1); break;
+    default: break;
+  }
+#undef AMSP_OCC
+  return b;
+}
+
+cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid,
+                              cudaStream_t stream) {
+  if (a.ntiles == 0) return cudaSuccess;
+#define AMSP_LAUNCH(W, U) fused_step_kernel<W, U><<<grid, kBlock, 0, stream>>>(a)
+  AMSP_FOR_WORLD(world, AMSP_LAUNCH)
+#undef AMSP_LAUNCH
+  return cudaGetLastError();
+}
+
+cudaError_t launch_barrier(uint32_t* const* peer_flags, int world, int rank,
+                           uint32_t epoch, int* err, cudaStream_t stream) {
+  barrier_kernel<<<1, 32, 0, stream>>>(peer_flags, world, rank, epoch, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_params(uint16_t* params, unsigned long long n, uint64_t seed,
+                               cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  init_params_kernel<<<sm_count() * 8, 256, 0, stream>>>(params, n, seed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_state(const Seg* segs, int nseg, int ntiles, float* master,
+                              float* m, float* v, uint64_t seed, int grid,
+                              cudaStream_t stream) {
+  if (ntiles == 0) return cudaSuccess;
+  init_state_kernel<<<grid, 256, 0, stream>>>(segs, nseg, ntiles, master, m, v, seed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth_grad(uint16_t* dst, unsigned long long start,
+                              unsigned long long n, uint64_t seed, int step, int rank,
+                              cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  synth_grad_kernel<<<sm_count() * 8, 256, 0, stream>>>(
+      dst, start, n, seed, static_cast<uint32_t>(step), static_cast<uint32_t>(rank));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adamw_flat(const void* grad, bool bf16_grad, float* master, float* m,
+                              float* v, uint16_t* param_out, unsigned long long n,
+                              const AdamScalars& s, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  const int grid = sm_count() * 8;
+  if (bf16_grad)
+    adamw_flat_kernel<true><<<grid, 256, 0, stream>>>(grad, master, m, v, param_out, n, s);
+  else
+    adamw_flat_kernel<false><<<grid, 256, 0, stream>>>(grad, master, m, v, param_out, n, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_upcast_scale(const uint16_t* src, float* dst, unsigned long long n,
+                                float scale, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  upcast_scale_kernel<<<sm_count() * 8, 256, 0, stream>>>(src, dst, n, scale);
+  return cudaGetLastError();
+}
+
+}  // namespace amsp

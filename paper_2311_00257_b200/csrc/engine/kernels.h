@@ -1,0 +1,72 @@
+// Host-side interface of the AMSP step kernels (kernels.cu), used by the
+// engine (engine.cpp) and the raw C-ABI launchers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+
+namespace amsp {
+
+// Step-constant AdamW scalars, computed on the host in double and rounded
+// once to float (same expression as amsp_o_adam_scalars()).
+struct AdamScalars {
+  float beta1, omb1, beta2, omb2;
+  float step_size, inv_sqrt_bc2, eps, decay, grad_scale;
+};
+
+// One contiguous run of a rank's optimizer-state shard: flat elements
+// [flat, flat+len) of the parameter vector, stored at os..os+len of the
+// shard; tile0 = index of the segment's first kTile-element tile.
+struct Seg {
+  unsigned long long flat, os, len, tile0;
+};
+
+constexpr int kBlock = 256;
+constexpr int kVecPerThread = 2;               // 8-element vectors per thread per tile
+constexpr unsigned long long kTile = kBlock * 8ull * kVecPerThread;  // 4096
+constexpr int kMaxRanks = 8;                   // NVSwitch domain of one HGX B200
+
+// Arguments of the fused reduce + AdamW + gather kernel.
+struct FusedArgs {
+  const Seg* segs;
+  int nseg;
+  int ntiles;
+  const uint16_t* grads[kMaxRanks];  // bf16 [Phi] of every DP rank, DP order
+  uint16_t* dsts[kMaxRanks];         // bf16 [Phi] params of every OS-group rank
+  int ndst;
+  float* master;
+  float* exp_avg;
+  float* exp_avg_sq;
+  AdamScalars s;
+  float* stats;                      // += sum(g^2); may be null
+};
+
+AdamScalars make_adam_scalars(double lr, double beta1, double beta2, double eps,
+                              double weight_decay, int step, double grad_scale);
+
+// Blocks per SM the fused kernel sustains for `world` gradient sources.
+int fused_blocks_per_sm(int world);
+
+cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid,
+                              cudaStream_t stream);
+cudaError_t launch_barrier(uint32_t* const* peer_flags, int world, int rank,
+                           uint32_t epoch, int* err, cudaStream_t stream);
+cudaError_t launch_init_params(uint16_t* params, unsigned long long n,
+                               uint64_t seed, cudaStream_t stream);
+cudaError_t launch_init_state(const Seg* segs, int nseg, int ntiles, float* master,
+                              float* m, float* v, uint64_t seed, int grid,
+                              cudaStream_t stream);
+cudaError_t launch_synth_grad(uint16_t* dst, unsigned long long start,
+                              unsigned long long n, uint64_t seed, int step,
+                              int rank, cudaStream_t stream);
+cudaError_t launch_adamw_flat(const void* grad, bool bf16_grad, float* master,
+                              float* m, float* v, uint16_t* param_out,
+                              unsigned long long n, const AdamScalars& s,
+                              cudaStream_t stream);
+cudaError_t launch_upcast_scale(const uint16_t* src, float* dst,
+                                unsigned long long n, float scale,
+                                cudaStream_t stream);
+
+}  // namespace amsp

@@ -1,0 +1,178 @@
+"""AMSP step engine (the B200 data plane) over the C-ABI.
+
+One Engine per GPU / process. The engine owns the rank's model-state
+buffers; peers are connected by exchanging cudaIpc handles (64 bytes per
+rank) through any all-gather — torch.distributed is used here purely as
+plumbing. There is no CPU path: every method launches sm_100a kernels in
+libamsp.so or raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .shardplan import DeviceMesh, ModelSpec, ShardingPlan, llama_tensors
+
+LAYOUTS = {"greedy": 0, "contiguous": 1}
+BUFFERS = {"grads": (0, np.uint16), "params": (1, np.uint16), "master": (2, np.float32),
+           "exp_avg": (3, np.float32), "exp_avg_sq": (4, np.float32)}
+DEFAULT_SEED = 0x414D5350  # "AMSP"
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)  # torch.cuda.Stream
+
+
+class Engine:
+    def __init__(self, tensors: Sequence[int] | ModelSpec, plan: ShardingPlan,
+                 dp_mesh: DeviceMesh, rank: int = 0, device: int = 0,
+                 layout: str = "greedy", lr: float = 1e-3, betas=(0.9, 0.95),
+                 eps: float = 1e-8, weight_decay: float = 0.1, seed: int = DEFAULT_SEED):
+        if isinstance(tensors, ModelSpec):
+            tensors = llama_tensors(tensors)
+        self.tensor_sizes = [int(t) for t in tensors]
+        self.plan, self.dp_mesh, self.rank = plan, dp_mesh, rank
+        self.hyper = dict(lr=lr, beta1=betas[0], beta2=betas[1], eps=eps,
+                          weight_decay=weight_decay)
+        self.seed = seed
+        self.layout = layout
+        arr = (C.c_uint64 * len(self.tensor_sizes))(*self.tensor_sizes)
+        cfg = N.EngineConfig(C.cast(arr, C.POINTER(C.c_uint64)), len(self.tensor_sizes),
+                             plan._c(), dp_mesh._c(), rank, device, LAYOUTS[layout], lr,
+                             betas[0], betas[1], eps, weight_decay, seed)
+        self._h = C.c_void_p()
+        N.check(N.lib().amsp_engine_create(C.byref(cfg), C.byref(self._h)))
+        self.info = self._info()
+
+    def _info(self) -> N.EngineInfo:
+        info = N.EngineInfo()
+        N.check(N.lib().amsp_engine_info(self._h, C.byref(info)))
+        return info
+
+    @property
+    def world(self) -> int:
+        return self.info.world
+
+    # ---------------------------------------------------------- peers
+    def export_handle(self) -> bytes:
+        buf = (C.c_char * 64)()
+        N.check(N.lib().amsp_engine_export_handle(self._h, buf))
+        return bytes(buf)
+
+    def import_handles(self, handles: Sequence[bytes]) -> None:
+        blob = b"".join(handles)
+        N.check(N.lib().amsp_engine_import_handles(self._h, blob, len(handles)))
+
+    def connect(self, group=None) -> None:
+        """Exchange IPC handles with every DP rank via torch.distributed."""
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+        handles = [None] * self.world
+        dist.all_gather_object(handles, self.export_handle(), group=group)
+        self.import_handles(handles)
+
+    # ---------------------------------------------------------- work
+    def init_state(self, stream=None) -> None:
+        N.check(N.lib().amsp_engine_init_state(self._h, _stream_ptr(stream)))
+
+    def synth_grads(self, step: int, stream=None) -> None:
+        N.check(N.lib().amsp_engine_synth_grads(self._h, step, _stream_ptr(stream)))
+
+    def step(self, step: int, stream=None) -> None:
+        N.check(N.lib().amsp_engine_step(self._h, step, _stream_ptr(stream)))
+
+    def step_host(self, step: int, host_grads_ptr: int, stream=None) -> np.ndarray:
+        stats = (C.c_float * 2)()
+        N.check(N.lib().amsp_engine_step_host(self._h, step, C.c_void_p(host_grads_ptr),
+                                              stats, _stream_ptr(stream)))
+        return np.array(stats, dtype=np.float32)
+
+    def stats(self) -> np.ndarray:
+        s = (C.c_float * 2)()
+        N.check(N.lib().amsp_engine_stats(self._h, s))
+        return np.array(s, dtype=np.float32)
+
+    def read(self, which: str, offset: int = 0, count: Optional[int] = None) -> np.ndarray:
+        idx, dt = BUFFERS[which]
+        total = self.info.total_params if idx < 2 else self.info.owned
+        count = total - offset if count is None else count
+        out = np.empty(count, dtype=dt)
+        N.check(N.lib().amsp_engine_read(self._h, idx, offset, count,
+                                         out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def write(self, which: str, data: np.ndarray, offset: int = 0) -> None:
+        idx, dt = BUFFERS[which]
+        data = np.ascontiguousarray(data, dtype=dt)
+        N.check(N.lib().amsp_engine_write(self._h, idx, offset, data.size,
+                                          data.ctypes.data_as(C.c_void_p)))
+
+    def launch_count(self) -> int:
+        n = C.c_uint64()
+        N.check(N.lib().amsp_engine_launch_count(self._h, C.byref(n)))
+        return n.value
+
+    def time_kernel(self, enable: bool = True) -> None:
+        N.check(N.lib().amsp_engine_time_kernel(self._h, int(enable)))
+
+    def kernel_ms(self):
+        """(summed fused-kernel ms, launches) since time_kernel(True)."""
+        ms, n = C.c_double(), C.c_int()
+        N.check(N.lib().amsp_engine_kernel_ms(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def segments(self):
+        """(flat, os, len) triples of this rank's optimizer-state shard."""
+        return layout_segments(self.tensor_sizes, self.plan.sos(), self.info.os_position,
+                               self.layout)
+
+    def close(self) -> None:
+        if self._h:
+            N.lib().amsp_engine_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def link_local(engines: Sequence[Engine]) -> None:
+    """Emulate one DP group on a single GPU (tests/smoke): engines must be
+    ranks 0..n-1 created on the same device; steps then run one after
+    another on one stream without cross-GPU barriers."""
+    arr = (C.c_void_p * len(engines))(*[e._h.value for e in engines])
+    N.check(N.lib().amsp_engine_link_local(arr, len(engines)))
+    for e in engines:
+        e._linked = engines  # keep peers alive while linked
+
+
+def layout_segments(tensor_sizes: Sequence[int], shard_count: int, shard: int,
+                    layout: str = "greedy"):
+    n = len(tensor_sizes)
+    arr = (C.c_uint64 * max(n, 1))(*tensor_sizes)
+    nseg, owned = C.c_int(), C.c_uint64()
+    N.check(N.lib().amsp_layout_segments(arr, n, shard_count, shard, LAYOUTS[layout], None,
+                                         None, None, 0, C.byref(nseg), C.byref(owned)))
+    k = max(nseg.value, 1)
+    f, o, ln = (C.c_uint64 * k)(), (C.c_uint64 * k)(), (C.c_uint64 * k)()
+    N.check(N.lib().amsp_layout_segments(arr, n, shard_count, shard, LAYOUTS[layout], f, o,
+                                         ln, k, C.byref(nseg), C.byref(owned)))
+    return [(f[i], o[i], ln[i]) for i in range(nseg.value)], owned.value
+
+
+def mesh_group(dp: DeviceMesh, mesh: DeviceMesh, rank: int):
+    blk, pos, n = C.c_int(), C.c_int(), C.c_int()
+    mem = (C.c_int * 64)()
+    N.check(N.lib().amsp_mesh_group(dp._c(), mesh._c(), rank, C.byref(blk), C.byref(pos), mem,
+                                    64, C.byref(n)))
+    return blk.value, pos.value, list(mem)[:n.value]

@@ -1,0 +1,168 @@
+"""Pins the CPU oracle (oracle/amsp_oracle.c) before it is trusted as the
+GPU checker, and checks the engine's host-side index maps.
+
+Floating-point parity is "unpinned" by the reference (no data plane, SPEC.md
+:16), so the oracle's arithmetic is checked against an independent numpy
+float32 restatement of the same definitions; the index maps (greedy
+inter-tensor OS layout) ARE pinned to golden output of the compiled
+reference."""
+import gzip
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import cpu as O
+from paper_2311_00257_b200 import shardplan as S
+from paper_2311_00257_b200.engine import layout_segments, mesh_group
+
+REPO = Path(__file__).resolve().parents[1]
+SEED = 0x414D5350
+
+
+def bf16_rne(x: np.ndarray) -> np.ndarray:
+    u = x.astype(np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    return u.astype(np.uint16)
+
+
+def test_bf16_matches_torch_rne():
+    import torch
+    rng = np.random.default_rng(0)
+    x = (rng.standard_normal(100000) * np.exp(rng.uniform(-20, 20, 100000))).astype(np.float32)
+    want = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(bf16_rne(x), want)
+    # oracle's own conversion, through the master->param path
+    idx = np.arange(5000, dtype=np.uint64)
+    master, _, _, param = O.trajectory(idx, SEED, 0, 1, O.hyper())
+    assert np.array_equal(param, bf16_rne(master))
+
+
+def numpy_trajectory(idx, steps, world, h):
+    """Independent float32 restatement of the oracle definitions."""
+    f32 = np.float32
+    p = np.array([O.master_init(SEED, int(i)) for i in idx], np.float32)
+    m = np.zeros_like(p)
+    v = np.zeros_like(p)
+    for t in range(1, steps + 1):
+        bc1 = 1.0 - h.beta1 ** t
+        bc2 = 1.0 - h.beta2 ** t
+        b1, omb1 = f32(h.beta1), f32(1.0 - h.beta1)
+        b2, omb2 = f32(h.beta2), f32(1.0 - h.beta2)
+        step_size = f32(h.lr / bc1)
+        inv = f32(1.0 / np.sqrt(bc2))
+        eps, decay, scale = f32(h.eps), f32(1.0 - h.lr * h.weight_decay), f32(1.0 / world)
+        g = None
+        for r in range(world):
+            gr = np.array([O.lib().amsp_o_grad_bf16(SEED, t, r, int(i)) for i in idx],
+                          np.uint16).astype(np.uint32) << 16
+            gr = gr.view(np.float32)
+            g = gr if g is None else (g + gr).astype(np.float32)
+        g = (g * scale).astype(np.float32)
+        m = (b1 * m + omb1 * g).astype(np.float32)
+        v = (b2 * v + (omb2 * g) * g).astype(np.float32)
+        d = (np.sqrt(v) * inv + eps).astype(np.float32)
+        p = (p * decay).astype(np.float32)
+        p = (p - step_size * (m / d)).astype(np.float32)
+    return p, m, v, bf16_rne(p)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_oracle_matches_numpy_restatement(world):
+    idx = np.concatenate([np.arange(0, 300), np.array([2**33 + 5, 6_738_415_615])]).astype(np.uint64)
+    h = O.hyper()
+    got = O.trajectory(idx, SEED, 4, world, h)
+    want = numpy_trajectory(idx, 4, world, h)
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
+
+
+def test_gradient_definition():
+    g = O.grads(0, 100000, SEED, 3, 1).astype(np.uint32) << 16
+    f = g.view(np.float32)
+    assert np.all(np.abs(f) <= 2.0 ** -7)
+    assert abs(f.mean()) < 1e-4 and f.std() > 1e-3
+    # distinct ranks / steps give distinct streams
+    assert not np.array_equal(O.grads(0, 64, SEED, 3, 0), O.grads(0, 64, SEED, 3, 1))
+    assert not np.array_equal(O.grads(0, 64, SEED, 3, 0), O.grads(0, 64, SEED, 4, 0))
+
+
+def _golden_greedy():
+    text = gzip.decompress((REPO / "tests/golden/plan_dump.txt.gz").read_bytes()).decode()
+    out = {}
+    for line in text.splitlines():
+        if line.startswith("greedy ") and " assign " in line and "rnd" not in line:
+            head, assign = line.split(" assign ")
+            parts = head.split()
+            name, k = parts[1], int(parts[2][2:])
+            sizes = [int(x) for x in head.split(" sizes ")[1].split()]
+            out[(name, k)] = ([int(a) for a in assign.split()], sizes)
+    return out
+
+
+@pytest.mark.parametrize("name,model", [("tiny", "tiny"), ("1B", "llama-1b"),
+                                        ("7B", "llama-7b"), ("13B", "llama-13b")])
+def test_index_map_pinned_to_reference(name, model):
+    gold = _golden_greedy()
+    tensors = S.llama_tensors(S.model(model))
+    for k in (1, 2, 3, 4, 8, 16):
+        want_assign, want_sizes = gold[(name, k)]
+        assert O.partition_greedy(tensors, k) == (want_assign, want_sizes)
+        assert S.partition_tensors_greedy(tensors, k) == (want_assign, want_sizes)
+        # the engine's per-rank segments realise exactly that assignment
+        offsets = np.concatenate([[0], np.cumsum(tensors)])
+        for shard in range(k):
+            segs, owned = layout_segments(tensors, k, shard, "greedy")
+            assert owned == want_sizes[shard]
+            covered = set()
+            for f, o, ln in segs:
+                t0 = int(np.searchsorted(offsets, f))
+                end = f + ln
+                t = t0
+                while offsets[t] < end:
+                    assert want_assign[t] == shard
+                    covered.add(t)
+                    t += 1
+            assert covered == {t for t, a in enumerate(want_assign) if a == shard}
+
+
+@pytest.mark.parametrize("layout", ["greedy", "contiguous"])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 8])
+def test_layout_partitions_flat_vector(layout, k):
+    tensors = S.llama_tensors(S.model("llama-7b"))
+    phi = sum(tensors)
+    spans = []
+    for shard in range(k):
+        segs, owned = layout_segments(tensors, k, shard, layout)
+        assert sum(s[2] for s in segs) == owned
+        assert [s[1] for s in segs] == list(np.cumsum([0] + [s[2] for s in segs[:-1]]))
+        spans += [(f, f + ln) for f, _, ln in segs]
+    spans.sort()
+    assert spans[0][0] == 0 and spans[-1][1] == phi
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    if layout == "contiguous":
+        assert all(f % 8 == 0 for f, _ in spans)
+
+
+def test_ragged_and_degenerate_layouts():
+    tensors = [3, 5, 7, 1, 9]
+    for k in (1, 2, 5, 7):
+        total = 0
+        for shard in range(k):
+            _, owned = layout_segments(tensors, k, shard, "greedy")
+            total += owned
+        assert total == sum(tensors)
+    with pytest.raises(Exception):
+        layout_segments(tensors, 2, 2, "greedy")
+
+
+def test_mesh_groups():
+    dp = S.DeviceMesh(2, 4)
+    seen = {}
+    for r in range(8):
+        blk, pos, mem = mesh_group(dp, S.DeviceMesh(2, 2), r)
+        assert mem[pos] == r
+        seen.setdefault(blk, set()).update(mem)
+    assert sorted(map(sorted, seen.values())) == [[0, 1, 2, 3], [4, 5, 6, 7]]
+    blk, pos, mem = mesh_group(S.DeviceMesh(4, 1), S.DeviceMesh(2, 1), 3)
+    assert (blk, pos, mem) == (1, 1, [2, 3])
