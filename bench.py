@@ -50,6 +50,8 @@ def parse():
                     help="zero1 (P/G replica, OS over dp) | replica | 'p=AxB,g=AxB,os=AxB'")
     ap.add_argument("--mesh", default=None, help="dp mesh per_node x nodes, default Nx1")
     ap.add_argument("--layout", default="greedy", choices=["greedy", "contiguous"])
+    ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (0 auto)")
+    ap.add_argument("--grid", type=int, default=0, help="fused-kernel grid (0 auto)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -138,15 +140,22 @@ class ClockSampler:
 
 
 def step_bytes(phi, owned, world, ndst):
-    """Algorithmic bytes of ONE fused launch on one rank.
+    """Algorithmic bytes per GPU of ONE step (all ranks' fused launches run
+    concurrently).
     HBM of this GPU: its OS shard read+written (24 B/elem), every rank's
-    reads of this GPU's bf16 gradients (2 B x Phi in total over the group)
-    and every owner's bf16 parameter stores into this GPU (2 B x Phi).
-    NVLink per direction: pulls of (W-1) peers' gradients for the owned
-    elements + pushes of the owned params to (ndst-1) peers."""
-    hbm = 24 * owned + 2 * phi + 2 * phi
-    nvl_in = 2 * owned * (world - 1)
-    nvl_out = 2 * owned * (ndst - 1)
+    reads of this GPU's bf16 gradients (2 B x Phi x replicas... = 2 B for
+    each element some owner pulls from here) and every owner's bf16
+    parameter stores into this GPU (2 B x Phi).
+    NVLink per direction of this GPU:
+      in  = my pulls of (W-1) peers' grads for my elements
+            + the other OS-group owners' param pushes into me
+      out = peers' pulls of my grads + my param pushes to (ndst-1) peers."""
+    replicas = world // ndst
+    hbm = 24 * owned + 2 * phi * replicas + 2 * phi
+    nvl_in = 2 * owned * (world - 1) + 2 * (phi - owned)
+    nvl_out = 2 * (replicas * phi - owned) + 2 * owned * (ndst - 1)
+    if world == 1:
+        nvl_in = nvl_out = 0
     return hbm, max(nvl_in, nvl_out)
 
 
@@ -259,6 +268,8 @@ def run_ours(args):
     plan = plan_of(args, S, dp)
     eng = Engine(model, plan, dp, rank=rank, device=local, layout=args.layout)
     eng.connect()
+    if args.variant or args.grid:
+        eng.tune(args.variant, args.grid)
     info = eng.info
     stream = torch.cuda.Stream(device=local)
     eng.init_state(stream)

@@ -270,6 +270,10 @@ int amsp_engine_read(amsp_engine_t* e, int which, uint64_t offset, uint64_t coun
                      void* host_dst);
 int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t count,
                       const void* host_src);
+/* Fused-kernel tuning: variant 0 auto, 1 one vector in flight per thread,
+ * 2 two vectors, 3 two vectors + >=3 CTAs/SM, 4 one vector + >=4 CTAs/SM;
+ * grid 0 = SMs x resident CTAs (persistent). */
+int amsp_engine_tune(amsp_engine_t* e, int variant, int grid);
 /* Bracket every fused launch with CUDA events on the step's stream (enable
  * != 0), then read the summed kernel time of the launches since enabling
  * (synchronous; resets the count). */

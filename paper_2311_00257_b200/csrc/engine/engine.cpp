@@ -67,7 +67,21 @@ struct amsp_engine {
   float* stats = nullptr;
   int* err = nullptr;
   uint32_t** d_peer_flags = nullptr;
-  int nseg = 0, ntiles = 0, grid = 0;
+  int nseg = 0, ntiles = 0, grid = 0, variant = 0, sms = 148;
+
+  // Persistent grid: SMs x resident CTAs of the chosen variant, unless the
+  // caller forces a grid (tuning).
+  // Auto (v = 0) for one rank: one 8-element vector in flight per thread,
+  // <= 64 registers, 2 CTAs per SM — the best point of the r01 sweep on
+  // LLaMA-7B (tools/tune_fused.py, profiles/r01_tune_7b.jsonl).
+  void retune(int v, int forced_grid) {
+    variant = (v == 0 && world == 1) ? 4 : v;
+    const int per_sm = amsp::fused_blocks_per_sm(world, variant);
+    int g = sms * per_sm;
+    if (v == 0 && world == 1) g = 2 * sms;
+    grid = forced_grid > 0 ? forced_grid : g;
+    grid = std::max(1, std::min(ntiles, grid));
+  }
   std::uint64_t device_bytes = 0;
 
   cudaStream_t own_stream = nullptr;
@@ -87,8 +101,12 @@ struct amsp_engine {
   uint32_t* flags_of(int r) const {
     return reinterpret_cast<uint32_t*>(static_cast<char*>(peer_base[r]) + off_flags);
   }
+  // Linked (single-GPU emulated) engines share rank 0's stream so that one
+  // rank's step is ordered after every rank's gradient production.
+  cudaStream_t shared_default = nullptr;
   cudaStream_t pick(void* s) const {
-    return s ? static_cast<cudaStream_t>(s) : own_stream;
+    if (s) return static_cast<cudaStream_t>(s);
+    return shared_default ? shared_default : own_stream;
   }
   void use_device() const { ck(cudaSetDevice(cfg.device), "cudaSetDevice"); }
 
@@ -129,6 +147,7 @@ struct amsp_engine {
     a.s = amsp::make_adam_scalars(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
                                   cfg.weight_decay, t, 1.0 / world);
     a.stats = stats;
+    a.fence_peers = (world > 1 && !local_linked) ? 1 : 0;
     ck(cudaMemsetAsync(stats, 0, 2 * sizeof(float), s), "reset stats");
     barrier(s);  // every rank's gradients are complete
     cudaEvent_t t_end = nullptr;
@@ -143,7 +162,7 @@ struct amsp_engine {
       ck(cudaEventRecord(ev.first, s), "event record");
       t_end = ev.second;
     }
-    ck(amsp::launch_fused_step(a, world, grid, s), "fused step launch");
+    ck(amsp::launch_fused_step(a, world, grid, variant, s), "fused step launch");
     if (t_end) ck(cudaEventRecord(t_end, s), "event record");
     if (ntiles > 0) ++launches;
     barrier(s);  // every owner's parameter stores have landed
@@ -240,8 +259,8 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
 
   int sms = 148;
   ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device), "sm count");
-  const int per_sm = amsp::fused_blocks_per_sm(e->world);
-  e->grid = std::max(1, std::min(e->ntiles, sms * per_sm));
+  e->sms = sms;
+  e->retune(0, 0);
   *out = e.release();
 }
 
@@ -323,6 +342,7 @@ int amsp_engine_link_local(amsp_engine_t* const* engines, int n) {
       e->publish_peer_flags();
       e->imported = true;
       e->local_linked = true;
+      e->shared_default = engines[0]->own_stream;
     }
   });
 }
@@ -428,6 +448,15 @@ int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t cou
     e->use_device();
     ck(cudaDeviceSynchronize(), "sync");
     if (count) ck(cudaMemcpy(p + offset * elem, host_src, count * elem, cudaMemcpyHostToDevice), "H2D");
+  });
+}
+
+int amsp_engine_tune(amsp_engine_t* e, int variant, int grid) {
+  return amsp::guarded([&] {
+    if (!e) throw Error("engine: null argument");
+    if (variant < 0 || variant > 4) throw Error("engine: unknown kernel variant");
+    e->use_device();
+    e->retune(variant, grid);
   });
 }
 

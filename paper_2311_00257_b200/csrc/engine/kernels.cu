@@ -91,8 +91,8 @@ __device__ void scalar_elems(const FusedArgs& a, const Seg& sg,
 }
 
 // U = 8-element vectors with all loads in flight before any math.
-template <int W, int U>
-__global__ void __launch_bounds__(kBlock)
+template <int W, int U, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB)
 fused_step_kernel(const FusedArgs a) {
   float sq = 0.0f;
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
@@ -166,7 +166,7 @@ fused_step_kernel(const FusedArgs a) {
   }
   // Peer parameter stores must be visible system-wide before the trailing
   // cross-GPU barrier releases the other ranks.
-  __threadfence_system();
+  if (a.fence_peers) __threadfence_system();
   if (a.stats != nullptr) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
@@ -304,55 +304,51 @@ int sm_count() {
   return n;
 }
 
-template <int W, int U>
-int occupancy_of() {
-  int blocks = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fused_step_kernel<W, U>, kBlock, 0);
-  return blocks > 0 ? blocks : 1;
+using FusedFn = void (*)(const FusedArgs);
+
+// Tuning variants of the fused kernel: U = vectors with loads in flight per
+// thread, MINB = minimum resident CTAs per SM requested from ptxas.
+//   0 auto (U=2 for W<=4, else U=1)  1 U=1  2 U=2  3 U=2,minB=3  4 U=1,minB=4
+template <int W>
+FusedFn pick_variant(int variant) {
+  switch (variant) {
+    case 1: return fused_step_kernel<W, 1, 1>;
+    case 2: return fused_step_kernel<W, 2, 1>;
+    case 3: return fused_step_kernel<W, 2, 3>;
+    case 4: return fused_step_kernel<W, 1, 4>;
+    default: return W <= 4 ? fused_step_kernel<W, 2, 1> : fused_step_kernel<W, 1, 1>;
+  }
+}
+
+FusedFn select_fused(int world, int variant) {
+  switch (world) {
+    case 1: return pick_variant<1>(variant);
+    case 2: return pick_variant<2>(variant);
+    case 3: return pick_variant<3>(variant);
+    case 4: return pick_variant<4>(variant);
+    case 5: return pick_variant<5>(variant);
+    case 6: return pick_variant<6>(variant);
+    case 7: return pick_variant<7>(variant);
+    case 8: return pick_variant<8>(variant);
+    default: return nullptr;
+  }
 }
 
 }  // namespace
 
-// Wide reductions (W > 4) keep one vector in flight per thread to stay
-// within the register budget; W <= 4 keeps two.
-#define AMSP_FOR_WORLD(W_, CALL)           \
-  switch (W_) {                            \
-    case 1: CALL(1, 2); break;             \
-    case 2: CALL(2, 2); break;             \
-    case 3: CALL(3, 2); break;             \
-    case 4: CALL(4, 2); break;             \
-    case 5: CALL(5, 1); break;             \
-    case 6: CALL(6, 1); break;             \
-    case 7: CALL(7, 1); break;             \
-    case 8: CALL(8, 1); break;             \
-    default: return cudaErrorInvalidValue; \
-  }
-
-int fused_blocks_per_sm(int world) {
-  int b = 1;
-  auto get = [&](auto f) { b = f(); };
-#define AMSP_OCC(W, U) get([] { return occupancy_of<W, U>(); })
-  switch (world) {
-    case 1: AMSP_OCC(1, 2); break;
-    case 2: AMSP_OCC(2, 2); break;
-    case 3: AMSP_OCC(3, 2); break;
-    case 4: AMSP_OCC(4, 2); break;
-    case 5: AMSP_OCC(5, 1); break;
-    case 6: AMSP_OCC(6, 1); break;
-    case 7: AMSP_OCC(7, 1); break;
-    case 8: AMSP_OCC(8, 1); break;
-    default: break;
-  }
-#undef AMSP_OCC
-  return b;
+int fused_blocks_per_sm(int world, int variant) {
+  FusedFn f = select_fused(world, variant);
+  int blocks = 0;
+  if (f) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f, kBlock, 0);
+  return blocks > 0 ? blocks : 1;
 }
 
-cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid,
+cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int variant,
                               cudaStream_t stream) {
   if (a.ntiles == 0) return cudaSuccess;
-#define AMSP_LAUNCH(W, U) fused_step_kernel<W, U><<<grid, kBlock, 0, stream>>>(a)
-  AMSP_FOR_WORLD(world, AMSP_LAUNCH)
-#undef AMSP_LAUNCH
+  FusedFn f = select_fused(world, variant);
+  if (!f) return cudaErrorInvalidValue;
+  f<<<grid, kBlock, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

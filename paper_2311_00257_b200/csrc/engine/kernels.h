@@ -41,15 +41,17 @@ struct FusedArgs {
   float* exp_avg_sq;
   AdamScalars s;
   float* stats;                      // += sum(g^2); may be null
+  int fence_peers;                   // membar.sys before exit (peer stores)
 };
 
 AdamScalars make_adam_scalars(double lr, double beta1, double beta2, double eps,
                               double weight_decay, int step, double grad_scale);
 
-// Blocks per SM the fused kernel sustains for `world` gradient sources.
-int fused_blocks_per_sm(int world);
+// Blocks per SM the fused kernel sustains for `world` gradient sources and
+// tuning `variant` (kernels.cu: 0 = auto).
+int fused_blocks_per_sm(int world, int variant);
 
-cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid,
+cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int variant,
                               cudaStream_t stream);
 cudaError_t launch_barrier(uint32_t* const* peer_flags, int world, int rank,
                            uint32_t epoch, int* err, cudaStream_t stream);

@@ -74,10 +74,7 @@ class Engine:
         """Exchange IPC handles with every DP rank via torch.distributed."""
         if self.world == 1:
             return
-        import torch.distributed as dist
-        handles = [None] * self.world
-        dist.all_gather_object(handles, self.export_handle(), group=group)
-        self.import_handles(handles)
+        self.import_handles(exchange_handles(self.export_handle(), self.world, group))
 
     # ---------------------------------------------------------- work
     def init_state(self, stream=None) -> None:
@@ -120,6 +117,10 @@ class Engine:
         N.check(N.lib().amsp_engine_launch_count(self._h, C.byref(n)))
         return n.value
 
+    def tune(self, variant: int = 0, grid: int = 0) -> None:
+        N.check(N.lib().amsp_engine_tune(self._h, variant, grid))
+        self.info = self._info()
+
     def time_kernel(self, enable: bool = True) -> None:
         N.check(N.lib().amsp_engine_time_kernel(self._h, int(enable)))
 
@@ -144,6 +145,18 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+
+def exchange_handles(handle: bytes, world: int, group=None) -> list:
+    """All-gather every rank's 64-byte cudaIpc handle, in rank order."""
+    import torch.distributed as dist
+    if len(handle) != 64:
+        raise ValueError("IPC handles are 64 bytes")
+    handles = [None] * world
+    dist.all_gather_object(handles, handle, group=group)
+    if any(not isinstance(h, bytes) or len(h) != 64 for h in handles):
+        raise RuntimeError("malformed IPC handle received from a peer")
+    return handles
 
 
 def link_local(engines: Sequence[Engine]) -> None:

@@ -1,0 +1,72 @@
+"""torchrun worker for the multi-GPU parity test (one process per GPU).
+
+  torchrun --nproc-per-node N tests/mp_worker.py --os-mesh Kx1 [--layout greedy]
+
+Each rank runs the AMSP step over real NVLink peer memory (cudaIpc-mapped
+buffers, device-side barriers) and checks its optimizer-state shard and its
+full bf16 parameter copy bit-exactly against the CPU oracle."""
+import argparse
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import cpu as O  # noqa: E402
+from paper_2311_00257_b200 import shardplan as S  # noqa: E402
+from paper_2311_00257_b200.engine import DEFAULT_SEED, Engine  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--os-mesh", default=None)
+    ap.add_argument("--dp-mesh", default=None)
+    ap.add_argument("--layout", default="greedy")
+    ap.add_argument("--model", default="tiny")
+    ap.add_argument("--steps", type=int, default=4)
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    M = S.DeviceMesh
+    mesh = lambda s: M(*map(int, s.split("x")))  # noqa: E731
+    dp = mesh(args.dp_mesh) if args.dp_mesh else M(world, 1)
+    os_mesh = mesh(args.os_mesh) if args.os_mesh else dp
+    plan = S.ShardingPlan(M(1, 1), M(1, 1), os_mesh)
+    e = Engine(S.model(args.model), plan, dp, rank=rank, device=local, layout=args.layout)
+    e.connect()
+    e.init_state()
+    for t in range(1, args.steps + 1):
+        e.synth_grads(t)
+        e.step(t)
+    torch.cuda.synchronize()
+    phi = e.info.total_params
+    segs, owned = e.segments()
+    idx = np.concatenate([np.arange(f, f + ln, dtype=np.uint64) for f, _, ln in segs])
+    want = O.trajectory(idx, DEFAULT_SEED, args.steps, world, O.hyper())
+    ok = True
+    for name, ref in zip(("master", "exp_avg", "exp_avg_sq"), want[:3]):
+        got = e.read(name)
+        if not np.array_equal(got.view(np.uint32), ref.view(np.uint32)):
+            print(f"RANK {rank} MISMATCH {name}: {int(np.sum(got != ref))}", flush=True)
+            ok = False
+    params = e.read("params")
+    full = O.trajectory_range(0, phi, DEFAULT_SEED, args.steps, world, O.hyper())[3]
+    if not np.array_equal(params, full):
+        print(f"RANK {rank} MISMATCH params: {int(np.sum(params != full))}", flush=True)
+        ok = False
+    st = e.stats()
+    e.close()
+    dist.barrier()
+    print(f"RANK {rank} {'OK' if ok else 'FAIL'} owned={owned} stats={st[0]:.4e}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
