@@ -198,6 +198,15 @@ int amsp_layout_segments(const uint64_t* tensor_sizes, int n_tensors,
                          uint64_t* flat, uint64_t* os, uint64_t* len, int cap,
                          int* n_segments, uint64_t* owned);
 
+/* Parameter-sharded variant (s_p > 1, ZeRO-3 intra-tensor split): P
+ * position p_pos holds slice p_pos of every tensor (tensors must be
+ * multiples of s_p); its P shard is split over the k ranks of the OS group
+ * sharing that P position. dst[s] is the segment's offset in the P shard. */
+int amsp_pshard_layout(const uint64_t* tensor_sizes, int n_tensors, int sp, int p_pos,
+                       int k, int os_pos, int layout, uint64_t* flat, uint64_t* os,
+                       uint64_t* dst, uint64_t* len, int cap, int* n_segments,
+                       uint64_t* owned);
+
 /* Group of `rank` for component mesh `mesh` inside the DP mesh `dp`
  * (ranks numbered node-major: rank = node*dp.per_node + local). Returns the
  * block index, the rank's position in its block and the block's members in
@@ -219,6 +228,10 @@ typedef struct {
   int layout;                   /* AMSP_LAYOUT_* */
   double lr, beta1, beta2, eps, weight_decay;
   uint64_t seed;
+  int skip_gathers;             /* s_p > 1: 0 = amsp_engine_step runs the
+                                   forward + backward parameter all-gathers
+                                   itself; 1 = the caller schedules
+                                   amsp_engine_gather (overlap scheduler) */
 } amsp_engine_config_t;
 
 typedef struct {
@@ -233,6 +246,11 @@ typedef struct {
   void* exp_avg;                /* fp32 [owned] */
   void* exp_avg_sq;             /* fp32 [owned] */
   uint64_t device_bytes;        /* allocated by the engine */
+  int sp;                       /* parameter shard factor s_p */
+  int p_position;               /* position in the P group */
+  uint64_t param_elems;         /* elements of `params` (Phi / s_p) */
+  int n_units;                  /* all-gather units (s_p > 1) */
+  uint64_t slot_elems;          /* gathered-unit slot capacity */
 } amsp_engine_info_t;
 
 #define AMSP_IPC_HANDLE_BYTES 64
@@ -241,6 +259,13 @@ int amsp_engine_create(const amsp_engine_config_t* cfg, amsp_engine_t** out);
 int amsp_engine_info(const amsp_engine_t* e, amsp_engine_info_t* info);
 /* Export this rank's peer-shared buffer (grads | params | flags). */
 int amsp_engine_export_handle(amsp_engine_t* e, void* handle64);
+/* s_p > 1: gather unit u = a run of consecutive tensors; its parameters are
+ * all-gathered (NVLink pulls from the P group's P shards, the paper's per-
+ * module AllGather, cost_model.cpp:46-49) into gathered slot `slot` (0/1)
+ * as the full tensors concatenated in flat order. */
+int amsp_engine_unit(const amsp_engine_t* e, int unit, int* first_tensor, int* n_tensors,
+                     uint64_t* elems);
+int amsp_engine_gather(amsp_engine_t* e, int unit, int slot, void* stream);
 /* Map every other rank's buffer; handles = world * 64 bytes in rank order. */
 int amsp_engine_import_handles(amsp_engine_t* e, const void* handles, int world);
 /* Single-GPU emulation of a DP group (tests / smoke): link n engines created
@@ -265,7 +290,8 @@ int amsp_engine_step_host(amsp_engine_t* e, int step, const void* host_grads,
 /* Device step statistics of the last step (synchronous). */
 int amsp_engine_stats(amsp_engine_t* e, float* stats2);
 /* Copy `count` elements at `offset` of a buffer to host (synchronous).
- * which: 0 grads(bf16) 1 params(bf16) 2 master 3 exp_avg 4 exp_avg_sq. */
+ * which: 0 grads(bf16) 1 params(bf16, the P shard) 2 master 3 exp_avg
+ * 4 exp_avg_sq 5/6 gathered slot 0/1 (bf16). */
 int amsp_engine_read(amsp_engine_t* e, int which, uint64_t offset, uint64_t count,
                      void* host_dst);
 int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t count,

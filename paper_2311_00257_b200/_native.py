@@ -99,7 +99,7 @@ class EngineConfig(C.Structure):
                 ("plan", Plan), ("dp_mesh", Mesh), ("rank", C.c_int), ("device", C.c_int),
                 ("layout", C.c_int), ("lr", C.c_double), ("beta1", C.c_double),
                 ("beta2", C.c_double), ("eps", C.c_double), ("weight_decay", C.c_double),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("skip_gathers", C.c_int)]
 
 
 class EngineInfo(C.Structure):
@@ -109,7 +109,9 @@ class EngineInfo(C.Structure):
                 ("replica_count", C.c_int), ("ntiles", C.c_int), ("grid", C.c_int),
                 ("block", C.c_int), ("grads", C.c_void_p), ("params", C.c_void_p),
                 ("master", C.c_void_p), ("exp_avg", C.c_void_p),
-                ("exp_avg_sq", C.c_void_p), ("device_bytes", C.c_uint64)]
+                ("exp_avg_sq", C.c_void_p), ("device_bytes", C.c_uint64),
+                ("sp", C.c_int), ("p_position", C.c_int), ("param_elems", C.c_uint64),
+                ("n_units", C.c_int), ("slot_elems", C.c_uint64)]
 
 
 P = C.POINTER
@@ -151,10 +153,15 @@ SIGNATURES = {
                                        P(u64), P(u64), C.c_int, P(C.c_int), P(u64)]),
     "amsp_mesh_group": (C.c_int, [Mesh, Mesh, C.c_int, P(C.c_int), P(C.c_int), P(C.c_int),
                                   C.c_int, P(C.c_int)]),
+    "amsp_pshard_layout": (C.c_int, [P(u64), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                     C.c_int, P(u64), P(u64), P(u64), P(u64), C.c_int,
+                                     P(C.c_int), P(u64)]),
     "amsp_engine_create": (C.c_int, [P(EngineConfig), P(vp)]),
     "amsp_engine_info": (C.c_int, [vp, P(EngineInfo)]),
     "amsp_engine_export_handle": (C.c_int, [vp, vp]),
     "amsp_engine_import_handles": (C.c_int, [vp, vp, C.c_int]),
+    "amsp_engine_unit": (C.c_int, [vp, C.c_int, P(C.c_int), P(C.c_int), P(u64)]),
+    "amsp_engine_gather": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "amsp_engine_link_local": (C.c_int, [P(vp), C.c_int]),
     "amsp_engine_init_state": (C.c_int, [vp, vp]),
     "amsp_engine_synth_grads": (C.c_int, [vp, C.c_int, vp]),

@@ -365,6 +365,25 @@ int amsp_layout_segments(const uint64_t* tensor_sizes, int n_tensors, int shard_
   });
 }
 
+int amsp_pshard_layout(const uint64_t* tensor_sizes, int n_tensors, int sp, int p_pos, int k,
+                       int os_pos, int layout, uint64_t* flat, uint64_t* os, uint64_t* dst,
+                       uint64_t* len, int cap, int* n_segments, uint64_t* owned) {
+  return amsp::guarded([&] {
+    if (n_tensors < 0 || (n_tensors > 0 && !tensor_sizes)) throw Error("null argument");
+    const amsp::ShardLayout L = amsp::pshard_layout(
+        std::vector<std::uint64_t>(tensor_sizes, tensor_sizes + n_tensors), sp, p_pos, k,
+        os_pos, layout);
+    if (n_segments) *n_segments = static_cast<int>(L.segs.size());
+    if (owned) *owned = L.owned;
+    for (int i = 0; i < cap && i < static_cast<int>(L.segs.size()); ++i) {
+      if (flat) flat[i] = L.segs[i].flat;
+      if (os) os[i] = L.segs[i].os;
+      if (dst) dst[i] = L.segs[i].dst;
+      if (len) len[i] = L.segs[i].len;
+    }
+  });
+}
+
 int amsp_mesh_group(amsp_mesh_t dp, amsp_mesh_t mesh, int rank, int* block, int* position,
                     int* members, int cap, int* n_members) {
   return amsp::guarded([&] {

@@ -1,18 +1,22 @@
 // The AMSP step engine: owns one rank's model-state buffers on its B200,
-// maps the peers' buffers over NVLink (cudaIpc), and runs the step
-//   barrier -> fused reduce + AdamW + gather kernel -> barrier
-// on a CUDA stream. One engine per GPU / process.
+// maps the peers' buffers over NVLink (cudaIpc), and runs the step on a
+// CUDA stream. One engine per GPU / process.
 //
-// Memory layout per rank (s_p = 1 plans: ZeRO-1 / ZeRO-2 / AMSP partial OS):
+// Step (paper Fig 7 / SURVEY.md §3 call stack 5, pipeline-only form):
+//   [s_p > 1] AG of every gather unit (forward order) then again (backward
+//             order): NVLink pulls of the P-group's P shards;
+//   barrier  -> fused reduce + AdamW + gather kernel ->  barrier.
+//
+// Memory layout per rank:
 //   shared allocation (exported to peers):
-//     grads  bf16 [Phi]   this rank's local gradient (backward output)
-//     params bf16 [Phi]   replicated parameters, written by the OS owners
-//     flags  u32 [64]     cross-GPU barrier slots (slot r written by rank r)
+//     grads  bf16 [Phi]      this rank's local gradient (backward output)
+//     params bf16 [Phi/s_p]  this rank's P shard (= all params when s_p = 1),
+//                            written by the OS owners of its elements
+//     flags  u32 [64]        cross-GPU barrier slots (slot r written by rank r)
 //   private allocation:
 //     master, exp_avg, exp_avg_sq fp32 [owned]  the rank's OS shard
-//     segment table, stats, error flag
-// Φ = 6.74e9 (LLaMA-7B) => 27 GB shared + 81 GB / s_os private; fits the
-// 180 GB of one B200 even unsharded (s_os = 1).
+//     segment tables, 2 gathered-unit slots (s_p > 1), stats, error flag
+// LLaMA-7B at s_p = 1: 27 GB shared + 81 GB / s_os private (fits 180 GB).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -41,20 +45,42 @@ std::size_t align_up(std::size_t x) { return (x + kAlign - 1) / kAlign * kAlign;
 
 DeviceMesh to_mesh(amsp_mesh_t m) { return DeviceMesh{m.per_node, m.nodes}; }
 
+// Device segment table with tile prefix sums.
+template <class T>
+int tile_prefix(std::vector<T>& segs) {
+  long long tiles = 0;
+  for (auto& s : segs) {
+    s.tile0 = static_cast<unsigned long long>(tiles);
+    tiles += static_cast<long long>((s.len + amsp::kTile - 1) / amsp::kTile);
+  }
+  if (tiles > 0x7fffffffLL) throw Error("engine: shard too large");
+  return static_cast<int>(tiles);
+}
+
+// A run of consecutive tensors all-gathered by one launch.
+struct GatherUnit {
+  int first_tensor = 0, n_tensors = 0;
+  std::uint64_t elems = 0;
+  int seg_begin = 0, nseg = 0, ntiles = 0;
+};
+
 }  // namespace
 
 struct amsp_engine {
   amsp_engine_config_t cfg{};
   std::vector<std::uint64_t> tensor_sizes;
   std::uint64_t phi = 0;
-  int world = 1, rank = 0;
+  int world = 1, rank = 0, sp = 1;
   amsp::ShardLayout layout;
-  amsp::MeshGroup os_group;
+  amsp::PShardMap pmap;
+  amsp::MeshGroup os_group, p_group;
+  std::vector<int> dst_members;  // OS-block ranks holding my P position
   int replicas = 1;
 
   // Shared region and its offsets (identical on every rank).
   char* shared = nullptr;
   std::size_t shared_bytes = 0, off_grads = 0, off_params = 0, off_flags = 0;
+  std::uint64_t param_elems = 0;
   void* peer_base[amsp::kMaxRanks] = {};
   bool imported = false;
   bool local_linked = false;  // single-GPU emulation: no barriers
@@ -64,27 +90,22 @@ struct amsp_engine {
   float* exp_avg_sq = nullptr;
   char* priv = nullptr;
   amsp::Seg* d_segs = nullptr;
+  amsp::Seg* d_psegs = nullptr;
+  amsp::CopySeg* d_copy = nullptr;
+  uint16_t* slots[2] = {nullptr, nullptr};
+  std::uint64_t slot_elems = 0;
+  std::vector<GatherUnit> units;
   float* stats = nullptr;
   int* err = nullptr;
   uint32_t** d_peer_flags = nullptr;
-  int nseg = 0, ntiles = 0, grid = 0, variant = 0, sms = 148;
-
-  // Persistent grid: SMs x resident CTAs of the chosen variant, unless the
-  // caller forces a grid (tuning).
-  // Auto (v = 0) for one rank: one 8-element vector in flight per thread,
-  // <= 64 registers, 2 CTAs per SM — the best point of the r01 sweep on
-  // LLaMA-7B (tools/tune_fused.py, profiles/r01_tune_7b.jsonl).
-  void retune(int v, int forced_grid) {
-    variant = (v == 0 && world == 1) ? 4 : v;
-    const int per_sm = amsp::fused_blocks_per_sm(world, variant);
-    int g = sms * per_sm;
-    if (v == 0 && world == 1) g = 2 * sms;
-    grid = forced_grid > 0 ? forced_grid : g;
-    grid = std::max(1, std::min(ntiles, grid));
-  }
+  int nseg = 0, ntiles = 0, npseg = 0, nptiles = 0;
+  int grid = 0, variant = 0, sms = 148;
   std::uint64_t device_bytes = 0;
 
   cudaStream_t own_stream = nullptr;
+  // Linked (single-GPU emulated) engines share rank 0's stream so that one
+  // rank's step is ordered after every rank's gradient production.
+  cudaStream_t shared_default = nullptr;
   uint32_t epoch = 0;
   // Optional CUDA-event bracketing of every fused launch (bench roofline).
   bool time_kernel = false;
@@ -101,14 +122,23 @@ struct amsp_engine {
   uint32_t* flags_of(int r) const {
     return reinterpret_cast<uint32_t*>(static_cast<char*>(peer_base[r]) + off_flags);
   }
-  // Linked (single-GPU emulated) engines share rank 0's stream so that one
-  // rank's step is ordered after every rank's gradient production.
-  cudaStream_t shared_default = nullptr;
   cudaStream_t pick(void* s) const {
     if (s) return static_cast<cudaStream_t>(s);
     return shared_default ? shared_default : own_stream;
   }
   void use_device() const { ck(cudaSetDevice(cfg.device), "cudaSetDevice"); }
+
+  // Auto (v = 0) for one rank: one 8-element vector in flight per thread,
+  // <= 64 registers, 2 CTAs per SM — the best point of the r01 sweep on
+  // LLaMA-7B (tools/tune_fused.py, profiles/r01_tune_7b.jsonl).
+  void retune(int v, int forced_grid) {
+    variant = (v == 0 && world == 1) ? 4 : v;
+    const int per_sm = amsp::fused_blocks_per_sm(world, variant);
+    int g = sms * per_sm;
+    if (v == 0 && world == 1) g = 2 * sms;
+    grid = forced_grid > 0 ? forced_grid : g;
+    grid = std::max(1, std::min(ntiles, grid));
+  }
 
   void publish_peer_flags() {
     uint32_t* h[amsp::kMaxRanks] = {};
@@ -130,17 +160,45 @@ struct amsp_engine {
     if (h) throw amsp::CudaFailure("cross-GPU barrier timed out (a peer did not arrive)");
   }
 
-  void step(int t, cudaStream_t s) {
-    if (t < 1) throw Error("engine: step index must be >= 1");
+  void require_peers() const {
     if (world > 1 && !imported)
       throw Error("engine: peers not imported (amsp_engine_import_handles)");
+  }
+
+  // AG of one gather unit into slot `slot` (s_p > 1).
+  void gather(int unit, int slot, cudaStream_t s) {
+    if (sp == 1) throw Error("engine: gather needs parameter sharding (s_p > 1)");
+    if (unit < 0 || unit >= static_cast<int>(units.size()))
+      throw Error("engine: gather unit out of range");
+    require_peers();
+    const GatherUnit& u = units[unit];
+    amsp::GatherArgs g{};
+    g.segs = d_copy + u.seg_begin;
+    g.nseg = u.nseg;
+    g.ntiles = u.ntiles;
+    for (int q = 0; q < sp; ++q) g.src[q] = params_of(p_group.members[q]);
+    g.dst = slots[slot & 1];
+    ck(amsp::launch_gather(g, s), "gather launch");
+    ++launches;
+  }
+
+  void step(int t, cudaStream_t s) {
+    if (t < 1) throw Error("engine: step index must be >= 1");
+    require_peers();
+    if (sp > 1 && !cfg.skip_gathers) {
+      // Forward then backward parameter all-gathers (T_p's two AG terms,
+      // cost_model.cpp:46-49); RS is fused into the optimizer kernel below.
+      const int n = static_cast<int>(units.size());
+      for (int u = 0; u < n; ++u) gather(u, u, s);
+      for (int u = n - 1; u >= 0; --u) gather(u, u, s);
+    }
     amsp::FusedArgs a{};
     a.segs = d_segs;
     a.nseg = nseg;
     a.ntiles = ntiles;
     for (int r = 0; r < world; ++r) a.grads[r] = grads_of(r);
-    a.ndst = static_cast<int>(os_group.members.size());
-    for (int d = 0; d < a.ndst; ++d) a.dsts[d] = params_of(os_group.members[d]);
+    a.ndst = static_cast<int>(dst_members.size());
+    for (int d = 0; d < a.ndst; ++d) a.dsts[d] = params_of(dst_members[d]);
     a.master = master;
     a.exp_avg = exp_avg;
     a.exp_avg_sq = exp_avg_sq;
@@ -170,6 +228,65 @@ struct amsp_engine {
 };
 
 namespace {
+
+void plan_groups(amsp_engine* e, const DeviceMesh& dp, const shardplan::ShardingPlan& plan) {
+  e->sp = plan.sp();
+  e->p_group = amsp::mesh_group(dp, plan.p, e->rank);
+  e->os_group = amsp::mesh_group(dp, plan.os, e->rank);
+  int my_k = -1;
+  for (int m : e->os_group.members) {
+    if (amsp::mesh_group(dp, plan.p, m).position == e->p_group.position) {
+      if (m == e->rank) my_k = static_cast<int>(e->dst_members.size());
+      e->dst_members.push_back(m);
+    }
+  }
+  if (my_k < 0) throw Error("engine: rank missing from its own OS group");
+  e->replicas = e->world / plan.sos();
+  e->pmap = amsp::pshard_map(e->tensor_sizes, e->sp);
+  e->param_elems = e->pmap.pshard_elems;
+  e->layout = amsp::pshard_layout(e->tensor_sizes, e->sp, e->p_group.position,
+                                  static_cast<int>(e->dst_members.size()), my_k,
+                                  e->cfg.layout);
+}
+
+// Gather units: consecutive tensors up to max(largest tensor, 2^27 elems).
+void plan_units(amsp_engine* e, std::vector<amsp::CopySeg>& copy) {
+  if (e->sp == 1) return;
+  const std::size_t n = e->tensor_sizes.size();
+  const std::uint64_t biggest =
+      *std::max_element(e->tensor_sizes.begin(), e->tensor_sizes.end());
+  const std::uint64_t cap = std::max<std::uint64_t>(biggest, std::uint64_t{1} << 27);
+  std::size_t t = 0;
+  while (t < n) {
+    GatherUnit u;
+    u.first_tensor = static_cast<int>(t);
+    while (t < n && (u.n_tensors == 0 || u.elems + e->tensor_sizes[t] <= cap)) {
+      u.elems += e->tensor_sizes[t];
+      ++u.n_tensors;
+      ++t;
+    }
+    std::vector<amsp::CopySeg> segs;
+    const std::uint64_t base = e->pmap.tensor_offset[u.first_tensor];
+    for (int i = 0; i < u.n_tensors; ++i) {
+      const std::size_t ti = static_cast<std::size_t>(u.first_tensor + i);
+      const std::uint64_t slice = e->pmap.slice_len[ti];
+      for (int q = 0; q < e->sp; ++q) {
+        amsp::CopySeg c{};
+        c.dst = e->pmap.tensor_offset[ti] - base + static_cast<std::uint64_t>(q) * slice;
+        c.src = e->pmap.pshard_offset[ti];
+        c.len = slice;
+        c.rank = q;
+        segs.push_back(c);
+      }
+    }
+    u.ntiles = tile_prefix(segs);
+    u.seg_begin = static_cast<int>(copy.size());
+    u.nseg = static_cast<int>(segs.size());
+    copy.insert(copy.end(), segs.begin(), segs.end());
+    e->slot_elems = std::max(e->slot_elems, u.elems);
+    e->units.push_back(u);
+  }
+}
 
 void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   if (!cfg || !out) throw Error("engine: null argument");
@@ -203,14 +320,11 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   if (!v.ok())
     throw Error("engine: plan " + shardplan::to_string(plan) + " violates " +
                 v.violations.front().constraint);
-  if (plan.sp() != 1)
-    throw Error("engine: parameter sharding (s_p > 1) is not implemented by the "
-                "B200 engine yet; plan " + shardplan::to_string(plan));
-
-  e->os_group = amsp::mesh_group(dp, plan.os, e->rank);
-  e->replicas = e->world / plan.sos();
-  e->layout = amsp::shard_layout(e->tensor_sizes, plan.sos(), e->os_group.position,
-                                 cfg->layout);
+  if (cfg->plan.has_secondary)
+    throw Error("engine: ZeRO++ secondary parameter meshes are not supported");
+  plan_groups(e.get(), dp, plan);
+  std::vector<amsp::CopySeg> copy;
+  plan_units(e.get(), copy);
 
   e->use_device();
   ck(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "stream");
@@ -218,50 +332,77 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   // Shared region.
   e->off_grads = 0;
   e->off_params = align_up(e->phi * 2);
-  e->off_flags = e->off_params + align_up(e->phi * 2);
+  e->off_flags = e->off_params + align_up(e->param_elems * 2);
   e->shared_bytes = e->off_flags + align_up(64 * sizeof(uint32_t));
   ck(cudaMalloc(&e->shared, e->shared_bytes), "cudaMalloc shared");
   ck(cudaMemset(e->shared + e->off_flags, 0, 64 * sizeof(uint32_t)), "zero flags");
   for (int r = 0; r < e->world; ++r) e->peer_base[r] = e->shared;
 
-  // Private region: OS shard + segment table + stats + error flag + flags table.
-  std::vector<amsp::Seg> segs;
-  long long tiles = 0;
-  for (const auto& s : e->layout.segs) {
-    segs.push_back({s.flat, s.os, s.len, static_cast<unsigned long long>(tiles)});
-    tiles += static_cast<long long>((s.len + amsp::kTile - 1) / amsp::kTile);
-  }
-  if (tiles > 0x7fffffffLL) throw Error("engine: shard too large");
+  // Segment tables: the OS shard, and the whole P shard (for init).
+  std::vector<amsp::Seg> segs, psegs;
+  for (const auto& s : e->layout.segs) segs.push_back({s.flat, s.os, s.dst, s.len, 0});
+  e->ntiles = tile_prefix(segs);
   e->nseg = static_cast<int>(segs.size());
-  e->ntiles = static_cast<int>(tiles);
+  for (const auto& s : amsp::pshard_layout(e->tensor_sizes, e->sp, e->p_group.position, 1, 0,
+                                           amsp::kLayoutContiguous).segs)
+    psegs.push_back({s.flat, s.os, s.dst, s.len, 0});
+  e->nptiles = tile_prefix(psegs);
+  e->npseg = static_cast<int>(psegs.size());
+
+  // Private region.
   const std::size_t n = e->layout.owned;
-  const std::size_t off_m = align_up(n * 4), off_v = off_m + align_up(n * 4);
-  const std::size_t off_seg = off_v + align_up(n * 4);
-  const std::size_t off_stats = off_seg + align_up(std::max<std::size_t>(segs.size(), 1) * sizeof(amsp::Seg));
-  const std::size_t off_err = off_stats + kAlign;
-  const std::size_t off_tab = off_err + kAlign;
-  const std::size_t priv_bytes = off_tab + kAlign;
-  ck(cudaMalloc(&e->priv, priv_bytes), "cudaMalloc optimizer state");
-  e->master = reinterpret_cast<float*>(e->priv);
-  e->exp_avg = reinterpret_cast<float*>(e->priv + off_m);
-  e->exp_avg_sq = reinterpret_cast<float*>(e->priv + off_v);
-  e->d_segs = reinterpret_cast<amsp::Seg*>(e->priv + off_seg);
-  e->stats = reinterpret_cast<float*>(e->priv + off_stats);
-  e->err = reinterpret_cast<int*>(e->priv + off_err);
-  e->d_peer_flags = reinterpret_cast<uint32_t**>(e->priv + off_tab);
-  if (!segs.empty())
-    ck(cudaMemcpy(e->d_segs, segs.data(), segs.size() * sizeof(amsp::Seg),
-                  cudaMemcpyHostToDevice),
-       "copy segments");
-  ck(cudaMemset(e->priv + off_stats, 0, 2 * kAlign), "zero stats/err");
+  std::size_t off = 0;
+  auto carve = [&off](std::size_t bytes) {
+    const std::size_t at = off;
+    off += align_up(std::max<std::size_t>(bytes, 1));
+    return at;
+  };
+  const std::size_t o_master = carve(n * 4), o_m = carve(n * 4), o_v = carve(n * 4);
+  const std::size_t o_seg = carve(segs.size() * sizeof(amsp::Seg));
+  const std::size_t o_pseg = carve(psegs.size() * sizeof(amsp::Seg));
+  const std::size_t o_copy = carve(copy.size() * sizeof(amsp::CopySeg));
+  const std::size_t o_slot0 = carve(e->slot_elems * 2), o_slot1 = carve(e->slot_elems * 2);
+  const std::size_t o_stats = carve(kAlign), o_err = carve(kAlign), o_tab = carve(kAlign);
+  ck(cudaMalloc(&e->priv, off), "cudaMalloc optimizer state");
+  e->master = reinterpret_cast<float*>(e->priv + o_master);
+  e->exp_avg = reinterpret_cast<float*>(e->priv + o_m);
+  e->exp_avg_sq = reinterpret_cast<float*>(e->priv + o_v);
+  e->d_segs = reinterpret_cast<amsp::Seg*>(e->priv + o_seg);
+  e->d_psegs = reinterpret_cast<amsp::Seg*>(e->priv + o_pseg);
+  e->d_copy = reinterpret_cast<amsp::CopySeg*>(e->priv + o_copy);
+  e->slots[0] = reinterpret_cast<uint16_t*>(e->priv + o_slot0);
+  e->slots[1] = reinterpret_cast<uint16_t*>(e->priv + o_slot1);
+  e->stats = reinterpret_cast<float*>(e->priv + o_stats);
+  e->err = reinterpret_cast<int*>(e->priv + o_err);
+  e->d_peer_flags = reinterpret_cast<uint32_t**>(e->priv + o_tab);
+  auto upload = [](void* dst, const void* src, std::size_t bytes, const char* what) {
+    if (bytes) ck(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), what);
+  };
+  upload(e->d_segs, segs.data(), segs.size() * sizeof(amsp::Seg), "copy segments");
+  upload(e->d_psegs, psegs.data(), psegs.size() * sizeof(amsp::Seg), "copy P segments");
+  upload(e->d_copy, copy.data(), copy.size() * sizeof(amsp::CopySeg), "copy gather table");
+  ck(cudaMemset(e->priv + o_stats, 0, 2 * kAlign), "zero stats/err");
   e->publish_peer_flags();
-  e->device_bytes = e->shared_bytes + priv_bytes;
+  e->device_bytes = e->shared_bytes + off;
 
   int sms = 148;
   ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device), "sm count");
   e->sms = sms;
   e->retune(0, 0);
   *out = e.release();
+}
+
+void* buffer_ptr(amsp_engine_t* e, int which, std::size_t* elem, std::uint64_t* count) {
+  switch (which) {
+    case 0: *elem = 2; *count = e->phi; return e->grads_of(e->rank);
+    case 1: *elem = 2; *count = e->param_elems; return e->params_of(e->rank);
+    case 2: *elem = 4; *count = e->layout.owned; return e->master;
+    case 3: *elem = 4; *count = e->layout.owned; return e->exp_avg;
+    case 4: *elem = 4; *count = e->layout.owned; return e->exp_avg_sq;
+    case 5: *elem = 2; *count = e->slot_elems; return e->slots[0];
+    case 6: *elem = 2; *count = e->slot_elems; return e->slots[1];
+    default: throw Error("engine: unknown buffer id " + std::to_string(which));
+  }
 }
 
 }  // namespace
@@ -281,7 +422,7 @@ int amsp_engine_info(const amsp_engine_t* e, amsp_engine_info_t* info) {
     info->world = e->world;
     info->os_block = e->os_group.block;
     info->os_position = e->os_group.position;
-    info->os_group_size = static_cast<int>(e->os_group.members.size());
+    info->os_group_size = static_cast<int>(e->dst_members.size());
     info->replica_count = e->replicas;
     info->ntiles = e->ntiles;
     info->grid = e->grid;
@@ -292,6 +433,32 @@ int amsp_engine_info(const amsp_engine_t* e, amsp_engine_info_t* info) {
     info->exp_avg = e->exp_avg;
     info->exp_avg_sq = e->exp_avg_sq;
     info->device_bytes = e->device_bytes;
+    info->sp = e->sp;
+    info->p_position = e->p_group.position;
+    info->param_elems = e->param_elems;
+    info->n_units = static_cast<int>(e->units.size());
+    info->slot_elems = e->slot_elems;
+  });
+}
+
+int amsp_engine_unit(const amsp_engine_t* e, int unit, int* first_tensor, int* n_tensors,
+                     uint64_t* elems) {
+  return amsp::guarded([&] {
+    if (!e) throw Error("engine: null argument");
+    if (unit < 0 || unit >= static_cast<int>(e->units.size()))
+      throw Error("engine: gather unit out of range");
+    const GatherUnit& u = e->units[unit];
+    if (first_tensor) *first_tensor = u.first_tensor;
+    if (n_tensors) *n_tensors = u.n_tensors;
+    if (elems) *elems = u.elems;
+  });
+}
+
+int amsp_engine_gather(amsp_engine_t* e, int unit, int slot, void* stream) {
+  return amsp::guarded([&] {
+    if (!e) throw Error("engine: null argument");
+    e->use_device();
+    e->gather(unit, slot, e->pick(stream));
   });
 }
 
@@ -352,7 +519,9 @@ int amsp_engine_init_state(amsp_engine_t* e, void* stream) {
     if (!e) throw Error("engine: null argument");
     e->use_device();
     cudaStream_t s = e->pick(stream);
-    ck(amsp::launch_init_params(e->params_of(e->rank), e->phi, e->cfg.seed, s), "init params");
+    ck(amsp::launch_init_params(e->d_psegs, e->npseg, e->nptiles, e->params_of(e->rank),
+                                e->cfg.seed, s),
+       "init params");
     ck(amsp::launch_init_state(e->d_segs, e->nseg, e->ntiles, e->master, e->exp_avg,
                                e->exp_avg_sq, e->cfg.seed, std::max(e->grid, 1), s),
        "init state");
@@ -409,17 +578,6 @@ int amsp_engine_stats(amsp_engine_t* e, float* stats2) {
     e->check_err();
     ck(cudaMemcpy(stats2, e->stats, 2 * sizeof(float), cudaMemcpyDeviceToHost), "read stats");
   });
-}
-
-static void* buffer_ptr(amsp_engine_t* e, int which, std::size_t* elem, std::uint64_t* count) {
-  switch (which) {
-    case 0: *elem = 2; *count = e->phi; return e->grads_of(e->rank);
-    case 1: *elem = 2; *count = e->phi; return e->params_of(e->rank);
-    case 2: *elem = 4; *count = e->layout.owned; return e->master;
-    case 3: *elem = 4; *count = e->layout.owned; return e->exp_avg;
-    case 4: *elem = 4; *count = e->layout.owned; return e->exp_avg_sq;
-    default: throw Error("engine: unknown buffer id " + std::to_string(which));
-  }
 }
 
 int amsp_engine_read(amsp_engine_t* e, int which, uint64_t offset, uint64_t count,

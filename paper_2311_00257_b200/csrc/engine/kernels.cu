@@ -18,6 +18,7 @@
 // CTAs streaming 128-bit vectors with several independent loads in flight.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
@@ -57,6 +58,7 @@ __device__ __forceinline__ Seg find_seg(const Seg* segs, int nseg, int tile) {
   Seg s;
   s.flat = __ldg(&segs[lo].flat);
   s.os = __ldg(&segs[lo].os);
+  s.dst = __ldg(&segs[lo].dst);
   s.len = __ldg(&segs[lo].len);
   s.tile0 = __ldg(&segs[lo].tile0);
   return s;
@@ -85,7 +87,7 @@ __device__ void scalar_elems(const FusedArgs& a, const Seg& sg,
     a.exp_avg[o] = m;
     a.exp_avg_sq[o] = v;
     const uint16_t b = to_bf16(p);
-    for (int d = 0; d < a.ndst; ++d) a.dsts[d][f] = b;
+    for (int d = 0; d < a.ndst; ++d) a.dsts[d][sg.dst + e] = b;
     sq += g * g;
   }
 }
@@ -99,7 +101,7 @@ fused_step_kernel(const FusedArgs a) {
     const Seg sg = find_seg(a.segs, a.nseg, tile);
     const unsigned long long base =
         (static_cast<unsigned long long>(tile) - sg.tile0) * kTile;
-    const bool aligned = ((sg.flat | sg.os) & 7ull) == 0;
+    const bool aligned = ((sg.flat | sg.os | sg.dst) & 7ull) == 0;
 #pragma unroll 1
     for (int it = 0; it < kVecPerThread; it += U) {
       unsigned long long e[U];
@@ -157,7 +159,7 @@ fused_step_kernel(const FusedArgs a) {
           st_stream_v4(a.exp_avg_sq + o, v[u][0]);
           st_stream_v4(a.exp_avg_sq + o + 4, v[u][1]);
           const uint4 out = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-          for (int d = 0; d < a.ndst; ++d) st_v4(a.dsts[d] + f, out);
+          for (int d = 0; d < a.ndst; ++d) st_v4(a.dsts[d] + sg.dst + e[u], out);
         } else if (e[u] < sg.len) {
           scalar_elems<W>(a, sg, e[u], sq);
         }
@@ -214,19 +216,50 @@ __global__ void barrier_kernel(uint32_t* const* peer_flags, int world, int rank,
   __syncthreads();
 }
 
-__global__ void init_params_kernel(uint16_t* __restrict__ p, unsigned long long n,
-                                   uint64_t seed) {
-  const unsigned long long stride = 8ull * gridDim.x * blockDim.x;
-  for (unsigned long long i = 8ull * (blockIdx.x * blockDim.x + threadIdx.x); i < n;
-       i += stride) {
-    if (i + 8 <= n) {
-      uint32_t w[4];
+__global__ void init_params_kernel(const Seg* segs, int nseg, int ntiles,
+                                   uint16_t* __restrict__ p, uint64_t seed) {
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const Seg sg = find_seg(segs, nseg, tile);
+    const unsigned long long base =
+        (static_cast<unsigned long long>(tile) - sg.tile0) * kTile;
+    for (unsigned long long e = base + threadIdx.x; e < base + kTile && e < sg.len;
+         e += blockDim.x)
+      p[sg.dst + e] = to_bf16(master_init(seed, sg.flat + e));
+  }
+}
+
+// All-gather of one unit (a run of tensors) from the P shards of the P group
+// into a local gathered buffer: pure NVLink pulls, 128-bit when aligned.
+__global__ void __launch_bounds__(256) gather_kernel(const GatherArgs a) {
+  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    int lo = 0, hi = a.nseg - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(&a.segs[mid].tile0) <= static_cast<unsigned long long>(tile))
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const CopySeg& cs = a.segs[lo];
+    const unsigned long long dst = __ldg(&cs.dst), src = __ldg(&cs.src);
+    const unsigned long long len = __ldg(&cs.len), t0 = __ldg(&cs.tile0);
+    const uint16_t* from = a.src[__ldg(&cs.rank)];
+    const unsigned long long base = (static_cast<unsigned long long>(tile) - t0) * kTile;
+    if (((dst | src) & 7ull) == 0) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        w[k] = pack_bf16x2(master_init(seed, i + 2 * k), master_init(seed, i + 2 * k + 1));
-      st_v4(p + i, make_uint4(w[0], w[1], w[2], w[3]));
+      for (int u = 0; u < kVecPerThread; ++u) {
+        const unsigned long long e = base + (static_cast<unsigned long long>(u) * kBlock +
+                                             threadIdx.x) * 8ull;
+        if (e + 8 <= len) {
+          st_v4(a.dst + dst + e, ld_ro_v4(from + src + e));
+        } else {
+          for (unsigned long long k = e; k < len && k < e + 8; ++k) a.dst[dst + k] = from[src + k];
+        }
+      }
     } else {
-      for (unsigned long long k = i; k < n; ++k) p[k] = to_bf16(master_init(seed, k));
+      for (unsigned long long e = base + threadIdx.x; e < base + kTile && e < len;
+           e += blockDim.x)
+        a.dst[dst + e] = from[src + e];
     }
   }
 }
@@ -358,10 +391,17 @@ cudaError_t launch_barrier(uint32_t* const* peer_flags, int world, int rank,
   return cudaGetLastError();
 }
 
-cudaError_t launch_init_params(uint16_t* params, unsigned long long n, uint64_t seed,
-                               cudaStream_t stream) {
-  if (n == 0) return cudaSuccess;
-  init_params_kernel<<<sm_count() * 8, 256, 0, stream>>>(params, n, seed);
+cudaError_t launch_init_params(const Seg* psegs, int nseg, int ntiles, uint16_t* params,
+                               uint64_t seed, cudaStream_t stream) {
+  if (ntiles == 0) return cudaSuccess;
+  init_params_kernel<<<std::min(ntiles, sm_count() * 8), 256, 0, stream>>>(psegs, nseg, ntiles,
+                                                                           params, seed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const GatherArgs& a, cudaStream_t stream) {
+  if (a.ntiles == 0) return cudaSuccess;
+  gather_kernel<<<std::min(a.ntiles, sm_count() * 4), 256, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -20,7 +20,22 @@ struct AdamScalars {
 // [flat, flat+len) of the parameter vector, stored at os..os+len of the
 // shard; tile0 = index of the segment's first kTile-element tile.
 struct Seg {
-  unsigned long long flat, os, len, tile0;
+  unsigned long long flat, os, dst, len, tile0;
+};
+
+// One contiguous copy of the all-gather: len elements from P shard
+// `rank` (position in the P group) at src to the gathered buffer at dst.
+struct CopySeg {
+  unsigned long long dst, src, len, tile0;
+  int rank, pad;
+};
+
+struct GatherArgs {
+  const CopySeg* segs;  // this unit's copy segments
+  int nseg;
+  int ntiles;
+  const uint16_t* src[8];  // P shards of the P-group members, position order
+  uint16_t* dst;           // gathered unit buffer (local)
 };
 
 constexpr int kBlock = 256;
@@ -55,8 +70,10 @@ cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int varia
                               cudaStream_t stream);
 cudaError_t launch_barrier(uint32_t* const* peer_flags, int world, int rank,
                            uint32_t epoch, int* err, cudaStream_t stream);
-cudaError_t launch_init_params(uint16_t* params, unsigned long long n,
+// params[dst+k] = bf16(master_init(flat+k)) over a P-shard segment table.
+cudaError_t launch_init_params(const Seg* psegs, int nseg, int ntiles, uint16_t* params,
                                uint64_t seed, cudaStream_t stream);
+cudaError_t launch_gather(const GatherArgs& a, cudaStream_t stream);
 cudaError_t launch_init_state(const Seg* segs, int nseg, int ntiles, float* master,
                               float* m, float* v, uint64_t seed, int grid,
                               cudaStream_t stream);

@@ -18,7 +18,8 @@ from .shardplan import DeviceMesh, ModelSpec, ShardingPlan, llama_tensors
 
 LAYOUTS = {"greedy": 0, "contiguous": 1}
 BUFFERS = {"grads": (0, np.uint16), "params": (1, np.uint16), "master": (2, np.float32),
-           "exp_avg": (3, np.float32), "exp_avg_sq": (4, np.float32)}
+           "exp_avg": (3, np.float32), "exp_avg_sq": (4, np.float32),
+           "slot0": (5, np.uint16), "slot1": (6, np.uint16)}
 DEFAULT_SEED = 0x414D5350  # "AMSP"
 
 
@@ -34,7 +35,8 @@ class Engine:
     def __init__(self, tensors: Sequence[int] | ModelSpec, plan: ShardingPlan,
                  dp_mesh: DeviceMesh, rank: int = 0, device: int = 0,
                  layout: str = "greedy", lr: float = 1e-3, betas=(0.9, 0.95),
-                 eps: float = 1e-8, weight_decay: float = 0.1, seed: int = DEFAULT_SEED):
+                 eps: float = 1e-8, weight_decay: float = 0.1, seed: int = DEFAULT_SEED,
+                 skip_gathers: bool = False):
         if isinstance(tensors, ModelSpec):
             tensors = llama_tensors(tensors)
         self.tensor_sizes = [int(t) for t in tensors]
@@ -46,7 +48,7 @@ class Engine:
         arr = (C.c_uint64 * len(self.tensor_sizes))(*self.tensor_sizes)
         cfg = N.EngineConfig(C.cast(arr, C.POINTER(C.c_uint64)), len(self.tensor_sizes),
                              plan._c(), dp_mesh._c(), rank, device, LAYOUTS[layout], lr,
-                             betas[0], betas[1], eps, weight_decay, seed)
+                             betas[0], betas[1], eps, weight_decay, seed, int(skip_gathers))
         self._h = C.c_void_p()
         N.check(N.lib().amsp_engine_create(C.byref(cfg), C.byref(self._h)))
         self.info = self._info()
@@ -99,7 +101,8 @@ class Engine:
 
     def read(self, which: str, offset: int = 0, count: Optional[int] = None) -> np.ndarray:
         idx, dt = BUFFERS[which]
-        total = self.info.total_params if idx < 2 else self.info.owned
+        total = {0: self.info.total_params, 1: self.info.param_elems}.get(
+            idx, self.info.owned if idx < 5 else self.info.slot_elems)
         count = total - offset if count is None else count
         out = np.empty(count, dtype=dt)
         N.check(N.lib().amsp_engine_read(self._h, idx, offset, count,
@@ -117,6 +120,15 @@ class Engine:
         N.check(N.lib().amsp_engine_launch_count(self._h, C.byref(n)))
         return n.value
 
+    def unit(self, u: int):
+        """(first_tensor, n_tensors, elems) of all-gather unit u (s_p > 1)."""
+        f, n, el = C.c_int(), C.c_int(), C.c_uint64()
+        N.check(N.lib().amsp_engine_unit(self._h, u, C.byref(f), C.byref(n), C.byref(el)))
+        return f.value, n.value, el.value
+
+    def gather(self, unit: int, slot: int = 0, stream=None) -> None:
+        N.check(N.lib().amsp_engine_gather(self._h, unit, slot, _stream_ptr(stream)))
+
     def tune(self, variant: int = 0, grid: int = 0) -> None:
         N.check(N.lib().amsp_engine_tune(self._h, variant, grid))
         self.info = self._info()
@@ -132,8 +144,21 @@ class Engine:
 
     def segments(self):
         """(flat, os, len) triples of this rank's optimizer-state shard."""
-        return layout_segments(self.tensor_sizes, self.plan.sos(), self.info.os_position,
-                               self.layout)
+        return self.shard_layout()[0], self.info.owned
+
+    def shard_layout(self):
+        """([(flat, os, dst, len)], owned) of this rank's optimizer-state shard."""
+        segs, owned = pshard_layout(self.tensor_sizes, self.plan.sp(), self.info.p_position,
+                                    self.info.os_group_size, self._k_position(), self.layout)
+        return [(f, o, ln) for f, o, d, ln in segs], segs
+
+    def _k_position(self):
+        # index of this rank among its OS block's ranks with the same P position
+        dp, plan = self.dp_mesh, self.plan
+        _, _, members = mesh_group(dp, plan.os, self.rank)
+        mine = mesh_group(dp, plan.p, self.rank)[1]
+        same = [m for m in members if mesh_group(dp, plan.p, m)[1] == mine]
+        return same.index(self.rank)
 
     def close(self) -> None:
         if self._h:
@@ -181,6 +206,21 @@ def layout_segments(tensor_sizes: Sequence[int], shard_count: int, shard: int,
     N.check(N.lib().amsp_layout_segments(arr, n, shard_count, shard, LAYOUTS[layout], f, o,
                                          ln, k, C.byref(nseg), C.byref(owned)))
     return [(f[i], o[i], ln[i]) for i in range(nseg.value)], owned.value
+
+
+def pshard_layout(tensor_sizes: Sequence[int], sp: int, p_pos: int, k: int, os_pos: int,
+                  layout: str = "greedy"):
+    """([(flat, os, dst, len)], owned) — see amsp_pshard_layout."""
+    n = len(tensor_sizes)
+    arr = (C.c_uint64 * max(n, 1))(*tensor_sizes)
+    nseg, owned = C.c_int(), C.c_uint64()
+    N.check(N.lib().amsp_pshard_layout(arr, n, sp, p_pos, k, os_pos, LAYOUTS[layout], None,
+                                       None, None, None, 0, C.byref(nseg), C.byref(owned)))
+    m = max(nseg.value, 1)
+    f, o, d, ln = [(C.c_uint64 * m)() for _ in range(4)]
+    N.check(N.lib().amsp_pshard_layout(arr, n, sp, p_pos, k, os_pos, LAYOUTS[layout], f, o, d,
+                                       ln, m, C.byref(nseg), C.byref(owned)))
+    return [(f[i], o[i], d[i], ln[i]) for i in range(nseg.value)], owned.value
 
 
 def mesh_group(dp: DeviceMesh, mesh: DeviceMesh, rank: int):

@@ -18,7 +18,7 @@ import torch.distributed as dist  # noqa: E402
 
 from oracle import cpu as O  # noqa: E402
 from paper_2311_00257_b200 import shardplan as S  # noqa: E402
-from paper_2311_00257_b200.engine import DEFAULT_SEED, Engine  # noqa: E402
+from paper_2311_00257_b200.engine import DEFAULT_SEED, Engine, pshard_layout  # noqa: E402
 
 
 def main():
@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--os-mesh", default=None)
     ap.add_argument("--dp-mesh", default=None)
     ap.add_argument("--layout", default="greedy")
+    ap.add_argument("--p-mesh", default=None)
     ap.add_argument("--model", default="tiny")
     ap.add_argument("--steps", type=int, default=4)
     args = ap.parse_args()
@@ -37,7 +38,9 @@ def main():
     mesh = lambda s: M(*map(int, s.split("x")))  # noqa: E731
     dp = mesh(args.dp_mesh) if args.dp_mesh else M(world, 1)
     os_mesh = mesh(args.os_mesh) if args.os_mesh else dp
-    plan = S.ShardingPlan(M(1, 1), M(1, 1), os_mesh)
+    p_mesh = mesh(args.p_mesh) if args.p_mesh else M(1, 1)
+    g_mesh = p_mesh if p_mesh == os_mesh or args.p_mesh else M(1, 1)
+    plan = S.ShardingPlan(p_mesh, g_mesh, os_mesh)
     e = Engine(S.model(args.model), plan, dp, rank=rank, device=local, layout=args.layout)
     e.connect()
     e.init_state()
@@ -56,7 +59,20 @@ def main():
             print(f"RANK {rank} MISMATCH {name}: {int(np.sum(got != ref))}", flush=True)
             ok = False
     params = e.read("params")
-    full = O.trajectory_range(0, phi, DEFAULT_SEED, args.steps, world, O.hyper())[3]
+    full_all = O.trajectory_range(0, phi, DEFAULT_SEED, args.steps, world, O.hyper())[3]
+    psegs, pn = pshard_layout(e.tensor_sizes, plan.sp(), e.info.p_position, 1, 0, "contiguous")
+    full = np.empty(pn, np.uint16)
+    for f, _, d, ln in psegs:
+        full[d:d + ln] = full_all[f:f + ln]
+    if plan.sp() > 1:  # every all-gather unit reproduces the updated tensors
+        offs = np.cumsum([0] + e.tensor_sizes)
+        for u in range(e.info.n_units):
+            first, _, elems = e.unit(u)
+            e.gather(u, 0)
+            got = e.read("slot0", 0, elems)
+            if not np.array_equal(got, full_all[offs[first]:offs[first] + elems]):
+                print(f"RANK {rank} MISMATCH gather unit {u}", flush=True)
+                ok = False
     if not np.array_equal(params, full):
         print(f"RANK {rank} MISMATCH params: {int(np.sum(params != full))}", flush=True)
         ok = False

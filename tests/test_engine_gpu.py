@@ -29,6 +29,16 @@ def _expected_from_segments(segs, owned, want):
     return out
 
 
+def _expected_params(e, want_bf16):
+    """The rank's parameter buffer (its P shard; everything when s_p = 1)."""
+    from paper_2311_00257_b200.engine import pshard_layout
+    segs, n = pshard_layout(e.tensor_sizes, e.plan.sp(), e.info.p_position, 1, 0, "contiguous")
+    out = np.empty(n, np.uint16)
+    for f, _, d, ln in segs:
+        out[d:d + ln] = want_bf16[f:f + ln]
+    return out
+
+
 def _check_rank(e, want_full, steps):
     segs, owned = e.segments()
     exp = _expected_from_segments(segs, owned, want_full)
@@ -39,7 +49,8 @@ def _check_rank(e, want_full, steps):
         # the north-star tolerance, stated explicitly
         np.testing.assert_allclose(got, ref, rtol=1e-5, atol=0)
     params = e.read("params")
-    assert np.array_equal(params, want_full[3]), int(np.sum(params != want_full[3]))
+    want = _expected_params(e, want_full[3])
+    assert np.array_equal(params, want), int(np.sum(params != want))
 
 
 @pytest.mark.parametrize("layout", ["greedy", "contiguous"])
@@ -155,9 +166,46 @@ def test_invalid_plans_fail_loudly(cuda):
     model = S.model("tiny")
     with pytest.raises(N.InvalidConfig, match="s_g in"):
         Engine(model, S.ShardingPlan(M(1, 1), M(2, 1), M(4, 1)), M(4, 1))
-    with pytest.raises(N.InvalidConfig, match="s_p > 1"):
-        Engine(model, S.ShardingPlan(M(2, 1), M(2, 1), M(2, 1)), M(2, 1))
+    with pytest.raises(N.InvalidConfig, match="not divisible"):
+        Engine([10, 7], S.ShardingPlan(M(2, 1), M(2, 1), M(2, 1)), M(2, 1))
     e = Engine(model, _plan(M(2, 1)), M(2, 1))
     with pytest.raises(N.InvalidConfig, match="peers not imported"):
         e.step(1)
     e.close()
+
+
+@pytest.mark.parametrize("world,p,os_k,layout", [(2, 2, 2, "greedy"), (4, 4, 4, "greedy"),
+                                                 (4, 2, 4, "greedy"), (4, 2, 2, "greedy"),
+                                                 (4, 2, 4, "contiguous"), (8, 8, 8, "greedy")])
+def test_emulated_parameter_sharding_bit_exact(cuda, world, p, os_k, layout):
+    """s_p > 1 (ZeRO-3 / AMSP-13B-style): intra-tensor P shards, forward and
+    backward all-gathers inside the step, RS fused into the optimizer kernel;
+    P shards, OS shards and gathered units checked against the oracle."""
+    model = S.model("tiny")
+    plan = S.ShardingPlan(M(p, 1), M(p, 1) if os_k == p else M(os_k, 1), M(os_k, 1))
+    engines = [Engine(model, plan, M(world, 1), rank=r, layout=layout) for r in range(world)]
+    link_local(engines)
+    for e in engines:
+        e.init_state()
+    steps = 3
+    for t in range(1, steps + 1):
+        for e in engines:
+            e.synth_grads(t)
+        for e in engines:
+            e.step(t)
+    phi = engines[0].info.total_params
+    want = O.trajectory_range(0, phi, DEFAULT_SEED, steps, world, H)
+    for e in engines:
+        assert e.info.sp == p and e.info.param_elems == phi // p
+        _check_rank(e, want, steps)
+    # every rank's all-gather reproduces the full updated tensors of each unit
+    offsets = np.cumsum([0] + engines[0].tensor_sizes)
+    e = engines[-1]
+    for u in range(e.info.n_units):
+        first, n, elems = e.unit(u)
+        e.gather(u, u % 2)
+        got = e.read(f"slot{u % 2}", 0, elems)
+        lo = offsets[first]
+        assert np.array_equal(got, want[3][lo:lo + elems]), (u, int(np.sum(got != want[3][lo:lo + elems])))
+    for e in engines:
+        e.close()

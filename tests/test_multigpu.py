@@ -16,13 +16,16 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-CASES = [(2, "2x1", None, "greedy"), (2, "2x1", None, "contiguous"),
-         (4, "4x1", None, "greedy"), (4, "2x1", None, "greedy"),
-         (4, "2x2", "2x2", "greedy"), (4, "4x1", None, "contiguous")]
+CASES = [(2, "2x1", None, "greedy", None), (2, "2x1", None, "contiguous", None),
+         (2, "2x1", None, "greedy", "2x1"),                      # ZeRO-3
+         (4, "4x1", None, "greedy", None), (4, "2x1", None, "greedy", None),
+         (4, "2x2", "2x2", "greedy", None), (4, "4x1", None, "contiguous", None),
+         (4, "4x1", None, "greedy", "4x1"),                      # ZeRO-3
+         (4, "4x1", None, "greedy", "2x1")]                      # AMSP-13B-style
 
 
-@pytest.mark.parametrize("world,os_mesh,dp_mesh,layout", CASES)
-def test_torchrun_group(world, os_mesh, dp_mesh, layout):
+@pytest.mark.parametrize("world,os_mesh,dp_mesh,layout,p_mesh", CASES)
+def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh):
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
@@ -30,6 +33,8 @@ def test_torchrun_group(world, os_mesh, dp_mesh, layout):
            str(REPO / "tests" / "mp_worker.py"), "--os-mesh", os_mesh, "--layout", layout]
     if dp_mesh:
         cmd += ["--dp-mesh", dp_mesh]
+    if p_mesh:
+        cmd += ["--p-mesh", p_mesh]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=REPO,
                        env={**os.environ, "OMP_NUM_THREADS": "4"})
     out = r.stdout + r.stderr

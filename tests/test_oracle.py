@@ -166,3 +166,30 @@ def test_mesh_groups():
     assert sorted(map(sorted, seen.values())) == [[0, 1, 2, 3], [4, 5, 6, 7]]
     blk, pos, mem = mesh_group(S.DeviceMesh(4, 1), S.DeviceMesh(2, 1), 3)
     assert (blk, pos, mem) == (1, 1, [2, 3])
+
+
+@pytest.mark.parametrize("sp,k", [(2, 1), (2, 2), (4, 2), (8, 1), (4, 4)])
+@pytest.mark.parametrize("layout", ["greedy", "contiguous"])
+def test_pshard_layout_partitions(sp, k, layout):
+    from paper_2311_00257_b200.engine import pshard_layout
+    tensors = S.llama_tensors(S.model("tiny"))
+    phi = sum(tensors)
+    flat_spans = []
+    for p_pos in range(sp):
+        dst_spans = []
+        owned_total = 0
+        for os_pos in range(k):
+            segs, owned = pshard_layout(tensors, sp, p_pos, k, os_pos, layout)
+            owned_total += owned
+            assert sum(s[3] for s in segs) == owned
+            flat_spans += [(f, f + ln) for f, _, _, ln in segs]
+            dst_spans += [(d, d + ln) for _, _, d, ln in segs]
+        assert owned_total == phi // sp
+        dst_spans.sort()
+        assert dst_spans[0][0] == 0 and dst_spans[-1][1] == phi // sp
+        assert all(a[1] == b[0] for a, b in zip(dst_spans, dst_spans[1:]))
+    flat_spans.sort()
+    assert flat_spans[0][0] == 0 and flat_spans[-1][1] == phi
+    assert all(a[1] == b[0] for a, b in zip(flat_spans, flat_spans[1:]))
+    with pytest.raises(Exception, match="not divisible"):
+        pshard_layout([10, 7], 2, 0, 1, 0, layout)
