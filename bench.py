@@ -68,6 +68,8 @@ def plan_of(args, S, dp):
         return S.ShardingPlan(S.DeviceMesh(1, 1), S.DeviceMesh(1, 1), dp)
     if args.plan == "replica":
         return S.ShardingPlan()
+    if args.plan == "zero3":
+        return S.ShardingPlan(dp, dp, dp)
     parts = dict(kv.split("=") for kv in args.plan.split(","))
     return S.ShardingPlan(mesh_of(parts["p"], S), mesh_of(parts["g"], S), mesh_of(parts["os"], S))
 
@@ -139,21 +141,27 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def step_bytes(phi, owned, world, ndst):
-    """Algorithmic bytes per GPU of ONE step (all ranks' fused launches run
-    concurrently).
-    HBM of this GPU: its OS shard read+written (24 B/elem), every rank's
-    reads of this GPU's bf16 gradients (2 B x Phi x replicas... = 2 B for
-    each element some owner pulls from here) and every owner's bf16
-    parameter stores into this GPU (2 B x Phi).
-    NVLink per direction of this GPU:
-      in  = my pulls of (W-1) peers' grads for my elements
-            + the other OS-group owners' param pushes into me
-      out = peers' pulls of my grads + my param pushes to (ndst-1) peers."""
-    replicas = world // ndst
-    hbm = 24 * owned + 2 * phi * replicas + 2 * phi
-    nvl_in = 2 * owned * (world - 1) + 2 * (phi - owned)
-    nvl_out = 2 * (replicas * phi - owned) + 2 * owned * (ndst - 1)
+def step_bytes(phi, owned, world, k, sp=1, sos=None, gathers=2):
+    """Algorithmic bytes per GPU of ONE step (all ranks run concurrently;
+    DESIGN.md §4). k = ranks sharing this rank's P position in its OS group
+    (its parameter-store destinations), R = W/s_os replica groups.
+    Fused reduce+AdamW+gather:
+      HBM  = 24*owned (state r+w) + 2*Phi*R (owners' reads of this GPU's
+             grads) + 2*Phi/s_p (parameter stores landing in this P shard)
+      NVL in  = my pulls 2*owned*(W-1) + pushes into my P shard 2*(Phi/s_p-owned)
+      NVL out = peers' pulls 2*(R*Phi-owned) + my pushes 2*owned*(k-1)
+    s_p > 1 adds `gathers` all-gather passes (forward + backward):
+      HBM  = 2*Phi (gathered write) + 2*Phi (the P group reading this shard)
+      NVL  = 2*Phi*(s_p-1)/s_p per direction."""
+    sos = sos or k * sp
+    R = world // sos
+    hbm = 24 * owned + 2 * phi * R + 2 * phi // sp
+    nvl_in = 2 * owned * (world - 1) + 2 * (phi // sp - owned)
+    nvl_out = 2 * (R * phi - owned) + 2 * owned * (k - 1)
+    if sp > 1:
+        hbm += gathers * 4 * phi
+        nvl_in += gathers * 2 * phi * (sp - 1) // sp
+        nvl_out += gathers * 2 * phi * (sp - 1) // sp
     if world == 1:
         nvl_in = nvl_out = 0
     return hbm, max(nvl_in, nvl_out)
@@ -323,9 +331,15 @@ def run_ours(args):
     phi = info.total_params
     value = phi / (ms_per_step * 1e-3)
     pk, pk_src = peaks()
-    hbm_b, nvl_b = step_bytes(phi, info.owned, world, info.os_group_size)
-    hbm_ach = hbm_b / (kernel_ms * 1e-3) / 1e9
-    nvl_ach = nvl_b / (kernel_ms * 1e-3) / 1e9
+    hbm_b, nvl_b = step_bytes(phi, info.owned, world, info.os_group_size, info.sp, plan.sos())
+    # s_p = 1: the step is one fused launch (+2 tiny barriers) -> time the
+    # kernel. s_p > 1: the all-gather passes are part of the roofline bytes,
+    # so the whole step is the timed unit.
+    t_meas = kernel_ms if info.sp == 1 else ms_per_step
+    scope = ("fused_step_kernel (reduce + AdamW + gather)" if info.sp == 1 else
+             "whole step: 2 all-gather passes (gather_kernel) + fused reduce/AdamW + barriers")
+    hbm_ach = hbm_b / (t_meas * 1e-3) / 1e9
+    nvl_ach = nvl_b / (t_meas * 1e-3) / 1e9
     t_hbm = hbm_b / (pk["hbm_gbs"] * 1e9)
     t_nvl = nvl_b / (NVLINK_P2P_GBS * 1e9)
     bound = "hbm" if t_hbm >= t_nvl else "nvlink"
@@ -336,8 +350,9 @@ def run_ours(args):
         "unit": "GB/s",
         "frac": round((hbm_ach / pk["hbm_gbs"]) if bound == "hbm" else (nvl_ach / NVLINK_P2P_GBS), 4),
         "traffic": None,
-        "kernel": "fused_step_kernel (reduce + AdamW + gather)",
+        "kernel": scope,
         "kernel_ms": round(kernel_ms, 4),
+        "timed_ms": round(t_meas, 4),
         "algorithmic_bytes": {"hbm": hbm_b, "nvlink_per_direction": nvl_b},
         "hbm": {"achieved": round(hbm_ach, 1), "peak": pk["hbm_gbs"],
                 "frac": round(hbm_ach / pk["hbm_gbs"], 4), "peak_source": pk_src},

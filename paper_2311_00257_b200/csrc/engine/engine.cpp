@@ -270,7 +270,11 @@ void plan_units(amsp_engine* e, std::vector<amsp::CopySeg>& copy) {
     for (int i = 0; i < u.n_tensors; ++i) {
       const std::size_t ti = static_cast<std::size_t>(u.first_tensor + i);
       const std::uint64_t slice = e->pmap.slice_len[ti];
-      for (int q = 0; q < e->sp; ++q) {
+      // Source order rotated by this rank's P position, local slice last:
+      // at any moment the P group's ranks pull from distinct peers instead
+      // of all hammering the same rank's NVLink egress.
+      for (int j = 0; j < e->sp; ++j) {
+        const int q = (e->p_group.position + 1 + j) % e->sp;
         amsp::CopySeg c{};
         c.dst = e->pmap.tensor_offset[ti] - base + static_cast<std::uint64_t>(q) * slice;
         c.src = e->pmap.pshard_offset[ti];

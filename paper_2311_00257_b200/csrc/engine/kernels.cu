@@ -246,14 +246,22 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs a) {
     const uint16_t* from = a.src[__ldg(&cs.rank)];
     const unsigned long long base = (static_cast<unsigned long long>(tile) - t0) * kTile;
     if (((dst | src) & 7ull) == 0) {
+      // All loads of the tile in flight before the first store (the asm
+      // volatile accesses are never reordered by the compiler).
+      uint4 v[kVecPerThread];
+      unsigned long long e[kVecPerThread];
 #pragma unroll
       for (int u = 0; u < kVecPerThread; ++u) {
-        const unsigned long long e = base + (static_cast<unsigned long long>(u) * kBlock +
-                                             threadIdx.x) * 8ull;
-        if (e + 8 <= len) {
-          st_v4(a.dst + dst + e, ld_ro_v4(from + src + e));
+        e[u] = base + (static_cast<unsigned long long>(u) * kBlock + threadIdx.x) * 8ull;
+        if (e[u] + 8 <= len) v[u] = ld_ro_v4(from + src + e[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kVecPerThread; ++u) {
+        if (e[u] + 8 <= len) {
+          st_v4(a.dst + dst + e[u], v[u]);
         } else {
-          for (unsigned long long k = e; k < len && k < e + 8; ++k) a.dst[dst + k] = from[src + k];
+          for (unsigned long long k = e[u]; k < len && k < e[u] + 8; ++k)
+            a.dst[dst + k] = from[src + k];
         }
       }
     } else {
