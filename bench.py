@@ -325,8 +325,10 @@ def run_ours(args):
     # The fused kernel alone (barriers excluded), bracketed by CUDA events on
     # the engine stream inside the same timed region.
     k_total, k_n = eng.kernel_ms()
+    g_total, g_n = eng.gather_ms()
     eng.time_kernel(False)
     kernel_ms = max_over_ranks(k_total / max(k_n, 1))
+    gather_ms = max_over_ranks(g_total / g_n) if g_n else 0.0
 
     phi = info.total_params
     value = phi / (ms_per_step * 1e-3)
@@ -353,6 +355,9 @@ def run_ours(args):
         "kernel": scope,
         "kernel_ms": round(kernel_ms, 4),
         "timed_ms": round(t_meas, 4),
+        "step_breakdown_ms": {"all_gather_passes": round(gather_ms, 4),
+                              "fused_reduce_adamw_gather": round(kernel_ms, 4),
+                              "barriers_and_gaps": round(ms_per_step - gather_ms - kernel_ms, 4)},
         "algorithmic_bytes": {"hbm": hbm_b, "nvlink_per_direction": nvl_b},
         "hbm": {"achieved": round(hbm_ach, 1), "peak": pk["hbm_gbs"],
                 "frac": round(hbm_ach / pk["hbm_gbs"], 4), "peak_source": pk_src},

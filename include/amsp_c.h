@@ -300,11 +300,15 @@ int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t cou
  * 2 two vectors, 3 two vectors + >=3 CTAs/SM, 4 one vector + >=4 CTAs/SM;
  * grid 0 = SMs x resident CTAs (persistent). */
 int amsp_engine_tune(amsp_engine_t* e, int variant, int grid);
+/* All-gather kernel grid (0 = 4 CTAs per SM). */
+int amsp_engine_tune_gather(amsp_engine_t* e, int grid);
 /* Bracket every fused launch with CUDA events on the step's stream (enable
  * != 0), then read the summed kernel time of the launches since enabling
  * (synchronous; resets the count). */
 int amsp_engine_time_kernel(amsp_engine_t* e, int enable);
 int amsp_engine_kernel_ms(amsp_engine_t* e, double* total_ms, int* launches);
+/* Same for the all-gather phase of each step (s_p > 1). */
+int amsp_engine_gather_ms(amsp_engine_t* e, double* total_ms, int* steps);
 /* Number of kernels this engine launched so far. */
 int amsp_engine_launch_count(const amsp_engine_t* e, uint64_t* n);
 void amsp_engine_destroy(amsp_engine_t* e);

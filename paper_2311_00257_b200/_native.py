@@ -172,8 +172,10 @@ SIGNATURES = {
     "amsp_engine_write": (C.c_int, [vp, C.c_int, u64, u64, vp]),
     "amsp_engine_launch_count": (C.c_int, [vp, P(u64)]),
     "amsp_engine_tune": (C.c_int, [vp, C.c_int, C.c_int]),
+    "amsp_engine_tune_gather": (C.c_int, [vp, C.c_int]),
     "amsp_engine_time_kernel": (C.c_int, [vp, C.c_int]),
     "amsp_engine_kernel_ms": (C.c_int, [vp, P(C.c_double), P(C.c_int)]),
+    "amsp_engine_gather_ms": (C.c_int, [vp, P(C.c_double), P(C.c_int)]),
     "amsp_engine_destroy": (None, [vp]),
     "amsp_k_synth_grad": (C.c_int, [vp, u64, u64, u64, C.c_int, C.c_int, vp]),
     "amsp_k_adamw": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, u64, C.c_int, C.c_double,

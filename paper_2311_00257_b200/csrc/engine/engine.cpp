@@ -99,7 +99,7 @@ struct amsp_engine {
   int* err = nullptr;
   uint32_t** d_peer_flags = nullptr;
   int nseg = 0, ntiles = 0, npseg = 0, nptiles = 0;
-  int grid = 0, variant = 0, sms = 148;
+  int grid = 0, variant = 0, sms = 148, gather_grid = 0;
   std::uint64_t device_bytes = 0;
 
   cudaStream_t own_stream = nullptr;
@@ -109,9 +109,36 @@ struct amsp_engine {
   uint32_t epoch = 0;
   // Optional CUDA-event bracketing of every fused launch (bench roofline).
   bool time_kernel = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kernel_events;
-  std::size_t kernel_events_used = 0;
+  using EventPairs = std::vector<std::pair<cudaEvent_t, cudaEvent_t>>;
+  EventPairs kernel_events, gather_events;
+  std::size_t kernel_events_used = 0, gather_events_used = 0;
   std::uint64_t launches = 0;
+
+  // When timing is on, records the start event of the next pair and returns
+  // the end event to record after the timed work (else nullptr).
+  cudaEvent_t record_begin(EventPairs& pairs, std::size_t& used, cudaStream_t s) {
+    if (!time_kernel) return nullptr;
+    if (used == pairs.size()) {
+      cudaEvent_t x, y;
+      ck(cudaEventCreate(&x), "event");
+      ck(cudaEventCreate(&y), "event");
+      pairs.emplace_back(x, y);
+    }
+    auto& ev = pairs[used++];
+    ck(cudaEventRecord(ev.first, s), "event record");
+    return ev.second;
+  }
+
+  static double sum_ms(EventPairs& pairs, std::size_t used) {
+    double sum = 0.0;
+    for (std::size_t i = 0; i < used; ++i) {
+      ck(cudaEventSynchronize(pairs[i].second), "event sync");
+      float ms = 0.0f;
+      ck(cudaEventElapsedTime(&ms, pairs[i].first, pairs[i].second), "event elapsed");
+      sum += ms;
+    }
+    return sum;
+  }
 
   uint16_t* grads_of(int r) const {
     return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_grads);
@@ -178,6 +205,9 @@ struct amsp_engine {
     g.ntiles = u.ntiles;
     for (int q = 0; q < sp; ++q) g.src[q] = params_of(p_group.members[q]);
     g.dst = slots[slot & 1];
+    g.grid = gather_grid;
+    g.sp = sp;
+    g.rot = (p_group.position + 1) % sp;
     ck(amsp::launch_gather(g, s), "gather launch");
     ++launches;
   }
@@ -188,9 +218,11 @@ struct amsp_engine {
     if (sp > 1 && !cfg.skip_gathers) {
       // Forward then backward parameter all-gathers (T_p's two AG terms,
       // cost_model.cpp:46-49); RS is fused into the optimizer kernel below.
+      cudaEvent_t g_end = record_begin(gather_events, gather_events_used, s);
       const int n = static_cast<int>(units.size());
       for (int u = 0; u < n; ++u) gather(u, u, s);
       for (int u = n - 1; u >= 0; --u) gather(u, u, s);
+      if (g_end) ck(cudaEventRecord(g_end, s), "event record");
     }
     amsp::FusedArgs a{};
     a.segs = d_segs;
@@ -208,18 +240,8 @@ struct amsp_engine {
     a.fence_peers = (world > 1 && !local_linked) ? 1 : 0;
     ck(cudaMemsetAsync(stats, 0, 2 * sizeof(float), s), "reset stats");
     barrier(s);  // every rank's gradients are complete
-    cudaEvent_t t_end = nullptr;
-    if (time_kernel && ntiles > 0) {
-      if (kernel_events_used == kernel_events.size()) {
-        cudaEvent_t x, y;
-        ck(cudaEventCreate(&x), "event");
-        ck(cudaEventCreate(&y), "event");
-        kernel_events.emplace_back(x, y);
-      }
-      auto& ev = kernel_events[kernel_events_used++];
-      ck(cudaEventRecord(ev.first, s), "event record");
-      t_end = ev.second;
-    }
+    cudaEvent_t t_end =
+        ntiles > 0 ? record_begin(kernel_events, kernel_events_used, s) : nullptr;
     ck(amsp::launch_fused_step(a, world, grid, variant, s), "fused step launch");
     if (t_end) ck(cudaEventRecord(t_end, s), "event record");
     if (ntiles > 0) ++launches;
@@ -269,21 +291,21 @@ void plan_units(amsp_engine* e, std::vector<amsp::CopySeg>& copy) {
     const std::uint64_t base = e->pmap.tensor_offset[u.first_tensor];
     for (int i = 0; i < u.n_tensors; ++i) {
       const std::size_t ti = static_cast<std::size_t>(u.first_tensor + i);
-      const std::uint64_t slice = e->pmap.slice_len[ti];
-      // Source order rotated by this rank's P position, local slice last:
-      // at any moment the P group's ranks pull from distinct peers instead
-      // of all hammering the same rank's NVLink egress.
-      for (int j = 0; j < e->sp; ++j) {
-        const int q = (e->p_group.position + 1 + j) % e->sp;
-        amsp::CopySeg c{};
-        c.dst = e->pmap.tensor_offset[ti] - base + static_cast<std::uint64_t>(q) * slice;
-        c.src = e->pmap.pshard_offset[ti];
-        c.len = slice;
-        c.rank = q;
-        segs.push_back(c);
-      }
+      // One entry per tensor; the kernel interleaves the s_p sources tile by
+      // tile (kernels.h CopySeg), rotated by this rank's P position.
+      amsp::CopySeg c{};
+      c.dst = e->pmap.tensor_offset[ti] - base;
+      c.src = e->pmap.pshard_offset[ti];
+      c.len = e->pmap.slice_len[ti];
+      segs.push_back(c);
     }
-    u.ntiles = tile_prefix(segs);
+    long long tiles = 0;
+    for (auto& c : segs) {
+      c.tile0 = static_cast<unsigned long long>(tiles);
+      tiles += static_cast<long long>((c.len + amsp::kTile - 1) / amsp::kTile) * e->sp;
+    }
+    if (tiles > 0x7fffffffLL) throw Error("engine: gather unit too large");
+    u.ntiles = static_cast<int>(tiles);
     u.seg_begin = static_cast<int>(copy.size());
     u.nseg = static_cast<int>(segs.size());
     copy.insert(copy.end(), segs.begin(), segs.end());
@@ -613,6 +635,13 @@ int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t cou
   });
 }
 
+int amsp_engine_tune_gather(amsp_engine_t* e, int grid) {
+  return amsp::guarded([&] {
+    if (!e || grid < 0) throw Error("engine: bad argument");
+    e->gather_grid = grid;
+  });
+}
+
 int amsp_engine_tune(amsp_engine_t* e, int variant, int grid) {
   return amsp::guarded([&] {
     if (!e) throw Error("engine: null argument");
@@ -627,6 +656,7 @@ int amsp_engine_time_kernel(amsp_engine_t* e, int enable) {
     if (!e) throw Error("engine: null argument");
     e->time_kernel = enable != 0;
     e->kernel_events_used = 0;
+    e->gather_events_used = 0;
   });
 }
 
@@ -634,17 +664,19 @@ int amsp_engine_kernel_ms(amsp_engine_t* e, double* total_ms, int* launches) {
   return amsp::guarded([&] {
     if (!e || !total_ms) throw Error("engine: null argument");
     e->use_device();
-    double sum = 0.0;
-    for (std::size_t i = 0; i < e->kernel_events_used; ++i) {
-      ck(cudaEventSynchronize(e->kernel_events[i].second), "event sync");
-      float ms = 0.0f;
-      ck(cudaEventElapsedTime(&ms, e->kernel_events[i].first, e->kernel_events[i].second),
-         "event elapsed");
-      sum += ms;
-    }
-    *total_ms = sum;
+    *total_ms = amsp_engine::sum_ms(e->kernel_events, e->kernel_events_used);
     if (launches) *launches = static_cast<int>(e->kernel_events_used);
     e->kernel_events_used = 0;
+  });
+}
+
+int amsp_engine_gather_ms(amsp_engine_t* e, double* total_ms, int* steps) {
+  return amsp::guarded([&] {
+    if (!e || !total_ms) throw Error("engine: null argument");
+    e->use_device();
+    *total_ms = amsp_engine::sum_ms(e->gather_events, e->gather_events_used);
+    if (steps) *steps = static_cast<int>(e->gather_events_used);
+    e->gather_events_used = 0;
   });
 }
 
@@ -665,10 +697,11 @@ void amsp_engine_destroy(amsp_engine_t* e) {
   cudaFree(e->shared);
   cudaFree(e->priv);
   if (e->own_stream) cudaStreamDestroy(e->own_stream);
-  for (auto& ev : e->kernel_events) {
-    cudaEventDestroy(ev.first);
-    cudaEventDestroy(ev.second);
-  }
+  for (auto* pairs : {&e->kernel_events, &e->gather_events})
+    for (auto& ev : *pairs) {
+      cudaEventDestroy(ev.first);
+      cudaEventDestroy(ev.second);
+    }
   delete e;
 }
 

@@ -64,6 +64,51 @@ __device__ __forceinline__ Seg find_seg(const Seg* segs, int nseg, int tile) {
   return s;
 }
 
+// Segment lookup for persistent grid-stride loops: the table is staged in
+// shared memory once per CTA (when it fits) and, since a CTA visits tiles in
+// increasing order, the owning segment is found by advancing a cursor —
+// no dependent global-memory search chain in front of every tile's loads.
+template <class T, int CAP>
+struct SegCursor {
+  const T* table;
+  int n, cur;
+  bool staged;
+
+  __device__ void init(T* smem, const T* global, int nseg) {
+    n = nseg;
+    cur = 0;
+    staged = nseg <= CAP;
+    if (staged) {
+      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(global);
+      unsigned long long* dst = reinterpret_cast<unsigned long long*>(smem);
+      constexpr int kWords = sizeof(T) / 8;
+      for (int i = threadIdx.x; i < nseg * kWords; i += blockDim.x) dst[i] = src[i];
+      __syncthreads();
+      table = smem;
+    } else {
+      table = global;
+    }
+  }
+
+  __device__ const T& at(int tile) {
+    const unsigned long long t = static_cast<unsigned long long>(tile);
+    if (staged) {
+      while (cur + 1 < n && table[cur + 1].tile0 <= t) ++cur;
+    } else {
+      int lo = cur, hi = n - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (table[mid].tile0 <= t) lo = mid; else hi = mid - 1;
+      }
+      cur = lo;
+    }
+    return table[cur];
+  }
+};
+
+constexpr int kSegCap = 384;    // 15 KB of Seg in shared memory
+constexpr int kCopyCap = 256;   // 10 KB of CopySeg
+
 template <int W>
 __device__ __forceinline__ float reduce_scalar(const FusedArgs& a,
                                                unsigned long long idx) {
@@ -96,9 +141,12 @@ __device__ void scalar_elems(const FusedArgs& a, const Seg& sg,
 template <int W, int U, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB)
 fused_step_kernel(const FusedArgs a) {
+  __shared__ Seg s_segs[kSegCap];
+  SegCursor<Seg, kSegCap> cursor;
+  cursor.init(s_segs, a.segs, a.nseg);
   float sq = 0.0f;
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-    const Seg sg = find_seg(a.segs, a.nseg, tile);
+    const Seg sg = cursor.at(tile);
     const unsigned long long base =
         (static_cast<unsigned long long>(tile) - sg.tile0) * kTile;
     const bool aligned = ((sg.flat | sg.os | sg.dst) & 7ull) == 0;
@@ -231,20 +279,24 @@ __global__ void init_params_kernel(const Seg* segs, int nseg, int ntiles,
 // All-gather of one unit (a run of tensors) from the P shards of the P group
 // into a local gathered buffer: pure NVLink pulls, 128-bit when aligned.
 __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs a) {
+  __shared__ CopySeg s_segs[kCopyCap];
+  __shared__ const uint16_t* s_src[8];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s_src[q] = a.src[q];  // constant indices: no local copy
+  }
+  SegCursor<CopySeg, kCopyCap> cursor;
+  cursor.init(s_segs, a.segs, a.nseg);  // includes a __syncthreads when staged
+  __syncthreads();
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-    int lo = 0, hi = a.nseg - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (__ldg(&a.segs[mid].tile0) <= static_cast<unsigned long long>(tile))
-        lo = mid;
-      else
-        hi = mid - 1;
-    }
-    const CopySeg& cs = a.segs[lo];
-    const unsigned long long dst = __ldg(&cs.dst), src = __ldg(&cs.src);
-    const unsigned long long len = __ldg(&cs.len), t0 = __ldg(&cs.tile0);
-    const uint16_t* from = a.src[__ldg(&cs.rank)];
-    const unsigned long long base = (static_cast<unsigned long long>(tile) - t0) * kTile;
+    const CopySeg& cs = cursor.at(tile);
+    const unsigned long long v = static_cast<unsigned long long>(tile) - cs.tile0;
+    const unsigned long long chunk = v / a.sp;
+    const int q = static_cast<int>((v % a.sp + a.rot) % a.sp);
+    const unsigned long long len = cs.len, src = cs.src;
+    const unsigned long long dst = cs.dst + static_cast<unsigned long long>(q) * len;
+    const uint16_t* from = s_src[q];
+    const unsigned long long base = chunk * kTile;
     if (((dst | src) & 7ull) == 0) {
       // All loads of the tile in flight before the first store (the asm
       // volatile accesses are never reordered by the compiler).
@@ -409,7 +461,8 @@ cudaError_t launch_init_params(const Seg* psegs, int nseg, int ntiles, uint16_t*
 
 cudaError_t launch_gather(const GatherArgs& a, cudaStream_t stream) {
   if (a.ntiles == 0) return cudaSuccess;
-  gather_kernel<<<std::min(a.ntiles, sm_count() * 4), 256, 0, stream>>>(a);
+  const int grid = a.grid > 0 ? a.grid : sm_count() * 4;
+  gather_kernel<<<std::min(a.ntiles, grid), 256, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -23,19 +23,24 @@ struct Seg {
   unsigned long long flat, os, dst, len, tile0;
 };
 
-// One contiguous copy of the all-gather: len elements from P shard
-// `rank` (position in the P group) at src to the gathered buffer at dst.
+// One tensor of an all-gather unit: every P-group member q holds its slice
+// (len elements) at src of its P shard; slice q lands at dst + q*len of the
+// gathered buffer. Tiles interleave the sources: tile v of the tensor copies
+// chunk v / s_p from source (rot + v % s_p) % s_p, so at every instant a rank
+// pulls evenly from all peers (no NVLink egress hot spot when ranks drift).
 struct CopySeg {
   unsigned long long dst, src, len, tile0;
-  int rank, pad;
 };
 
 struct GatherArgs {
-  const CopySeg* segs;  // this unit's copy segments
+  const CopySeg* segs;  // this unit's tensors
   int nseg;
   int ntiles;
+  int sp;               // P-group size
+  int rot;              // source rotation (this rank's P position + 1)
   const uint16_t* src[8];  // P shards of the P-group members, position order
   uint16_t* dst;           // gathered unit buffer (local)
+  int grid;                // CTAs (0 = 4 per SM)
 };
 
 constexpr int kBlock = 256;

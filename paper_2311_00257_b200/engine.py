@@ -142,6 +142,12 @@ class Engine:
         N.check(N.lib().amsp_engine_kernel_ms(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    def gather_ms(self):
+        """(summed all-gather-phase ms, steps) since time_kernel(True)."""
+        ms, n = C.c_double(), C.c_int()
+        N.check(N.lib().amsp_engine_gather_ms(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
     def segments(self):
         """(flat, os, len) triples of this rank's optimizer-state shard."""
         return self.shard_layout()[0], self.info.owned

@@ -47,6 +47,29 @@ __global__ void add_kernel(const uint4* __restrict__ a, const uint4* __restrict_
   }
 }
 
+// Gather-shaped pull: `parts` sources read back to back (one contiguous slice
+// each), 2 x 16 B per thread per 8 KB tile, persistent grid-stride tiles.
+struct Srcs {
+  const uint4* p[8];
+};
+__global__ void gather_like(Srcs s, int parts, int rot, uint4* __restrict__ dst, size_t slice16) {
+  const size_t tiles_per = (slice16 + 511) / 512;  // 512 x 16 B = 8 KB tiles
+  const size_t ntiles = tiles_per * parts;
+  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int j = static_cast<int>(t / tiles_per);
+    const int q = (rot + j) % parts;
+    const size_t base = (t % tiles_per) * 512;
+    const uint4* src = s.p[q];
+    size_t i0 = base + threadIdx.x, i1 = base + 256 + threadIdx.x;
+    uint4 a, b;
+    const bool ok0 = i0 < slice16, ok1 = i1 < slice16;
+    if (ok0) a = src[i0];
+    if (ok1) b = src[i1];
+    if (ok0) dst[q * slice16 + i0] = a;
+    if (ok1) dst[q * slice16 + i1] = b;
+  }
+}
+
 int main(int argc, char** argv) {
   size_t bytes = argc > 1 ? strtoull(argv[1], nullptr, 10) : (size_t(1) << 31);
   int ng = 0;
@@ -123,6 +146,18 @@ int main(int argc, char** argv) {
     run("reduce2 (a + peer b)", gm, [&](int g, int grid) {
       add_kernel<<<grid, 256, 0, s0[g]>>>(a[g], b[(g + 1) % peers], c[g], n);
     }, 1.0 * bytes);
+    // All-gather shaped: every GPU pulls one slice from each peer (rotated
+    // start), slices of bytes/ng; data moved over NVLink = bytes*(ng-1)/ng.
+    run("gather-like rotated", gm, [&](int g, int grid) {
+      Srcs s{};
+      for (int q = 0; q < ng; ++q) s.p[q] = a[q] + (size_t)q * (n / ng);
+      gather_like<<<grid, 256, 0, s0[g]>>>(s, ng, g + 1, c[g], n / ng);
+    }, 1.0 * bytes * (ng - 1) / ng);
+    run("gather-like same order", gm, [&](int g, int grid) {
+      Srcs s{};
+      for (int q = 0; q < ng; ++q) s.p[q] = a[q] + (size_t)q * (n / ng);
+      gather_like<<<grid, 256, 0, s0[g]>>>(s, ng, 0, c[g], n / ng);
+    }, 1.0 * bytes * (ng - 1) / ng);
   }
   return 0;
 }
