@@ -313,6 +313,42 @@ int amsp_engine_gather_ms(amsp_engine_t* e, double* total_ms, int* steps);
 int amsp_engine_launch_count(const amsp_engine_t* e, uint64_t* n);
 void amsp_engine_destroy(amsp_engine_t* e);
 
+/* ------------------------------------------------------------ scheduler */
+/* Overlap scheduler (north-star item 4): replays the reference's one-step
+ * event graph (build_schedule, overlap_sim.cpp:442-457) on three CUDA
+ * streams of the engine's GPU. Compute events run a compute stand-in for
+ * their planned duration; AG / RS / AR-bucket events run the engine's NVLink
+ * gather / barrier + pull-reduce; after the graph: barrier, AdamW + bf16
+ * push to the OS-group owners, barrier. The engine's tensors must be the
+ * LLaMA layout [embed, L x K modules, final norm, lm_head] of `model`. */
+typedef struct amsp_sched amsp_sched_t;
+
+typedef struct {
+  amsp_model_t model;           /* M must be 1 */
+  amsp_cost_config_t cost;      /* bucket size U */
+  amsp_sim_config_t sim;        /* tier, recompute, streams, compute times */
+  int comm_ctas;                /* CTAs per communication kernel (0 = 128) */
+  int compute_ctas;             /* CTAs of the compute stand-in (0 = SMs) */
+  double time_scale;            /* multiplies compute durations (0 = 1) */
+  int optimizer_overlap;        /* 0: AdamW + push after the step barrier
+                                   (the paper's placement); 1: per module /
+                                   bucket inside backward (see sched.cpp) */
+} amsp_sched_config_t;
+
+typedef struct {
+  int n_events, n_compute, n_gather, n_reduce, n_buckets, n_barriers, stream_count;
+  double predicted_step_s;      /* simulate_step() of the same graph */
+  double predicted_compute_s;   /* compute-stream busy time */
+} amsp_sched_info_t;
+
+int amsp_sched_create(amsp_engine_t* e, const amsp_sched_config_t* cfg,
+                      const amsp_profile_t* profile, amsp_sched_t** out);
+int amsp_sched_info(const amsp_sched_t* s, amsp_sched_info_t* info);
+/* One step; with_comm = 0 runs the compute stand-ins only (the exposed-
+ * communication baseline). stream = the compute stream (NULL: engine's). */
+int amsp_sched_step(amsp_sched_t* s, int step, void* stream, int with_comm);
+void amsp_sched_destroy(amsp_sched_t* s);
+
 /* ------------------------------------------------------------ kernels */
 /* Raw launchers (device pointers + cudaStream_t passed as void*). */
 

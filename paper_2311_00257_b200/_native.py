@@ -114,6 +114,19 @@ class EngineInfo(C.Structure):
                 ("n_units", C.c_int), ("slot_elems", C.c_uint64)]
 
 
+class SchedConfig(C.Structure):
+    _fields_ = [("model", Model), ("cost", CostConfig), ("sim", SimConfig),
+                ("comm_ctas", C.c_int), ("compute_ctas", C.c_int), ("time_scale", C.c_double),
+                ("optimizer_overlap", C.c_int)]
+
+
+class SchedInfo(C.Structure):
+    _fields_ = [("n_events", C.c_int), ("n_compute", C.c_int), ("n_gather", C.c_int),
+                ("n_reduce", C.c_int), ("n_buckets", C.c_int), ("n_barriers", C.c_int),
+                ("stream_count", C.c_int), ("predicted_step_s", C.c_double),
+                ("predicted_compute_s", C.c_double)]
+
+
 P = C.POINTER
 vp = C.c_void_p
 u64 = C.c_uint64
@@ -177,6 +190,10 @@ SIGNATURES = {
     "amsp_engine_kernel_ms": (C.c_int, [vp, P(C.c_double), P(C.c_int)]),
     "amsp_engine_gather_ms": (C.c_int, [vp, P(C.c_double), P(C.c_int)]),
     "amsp_engine_destroy": (None, [vp]),
+    "amsp_sched_create": (C.c_int, [vp, P(SchedConfig), vp, P(vp)]),
+    "amsp_sched_info": (C.c_int, [vp, P(SchedInfo)]),
+    "amsp_sched_step": (C.c_int, [vp, C.c_int, vp, C.c_int]),
+    "amsp_sched_destroy": (None, [vp]),
     "amsp_k_synth_grad": (C.c_int, [vp, u64, u64, u64, C.c_int, C.c_int, vp]),
     "amsp_k_adamw": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, u64, C.c_int, C.c_double,
                                C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,

@@ -12,242 +12,12 @@
 //     grads  bf16 [Phi]      this rank's local gradient (backward output)
 //     params bf16 [Phi/s_p]  this rank's P shard (= all params when s_p = 1),
 //                            written by the OS owners of its elements
-//     flags  u32 [64]        cross-GPU barrier slots (slot r written by rank r)
+//     flags  u32 [8192 x 8]  cross-GPU barrier words ([id][r] written by rank r)
 //   private allocation:
 //     master, exp_avg, exp_avg_sq fp32 [owned]  the rank's OS shard
 //     segment tables, 2 gathered-unit slots (s_p > 1), stats, error flag
 // LLaMA-7B at s_p = 1: 27 GB shared + 81 GB / s_os private (fits 180 GB).
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cstring>
-#include <memory>
-#include <string>
-#include <vector>
-
-#include "amsp_c.h"
-#include "kernels.h"
-#include "layout.h"
-#include "../status.h"
-
-using shardplan::DeviceMesh;
-using shardplan::Error;
-
-namespace {
-
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess)
-    throw amsp::CudaFailure(std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
-}
-
-constexpr std::size_t kAlign = 256;
-std::size_t align_up(std::size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
-
-DeviceMesh to_mesh(amsp_mesh_t m) { return DeviceMesh{m.per_node, m.nodes}; }
-
-// Device segment table with tile prefix sums.
-template <class T>
-int tile_prefix(std::vector<T>& segs) {
-  long long tiles = 0;
-  for (auto& s : segs) {
-    s.tile0 = static_cast<unsigned long long>(tiles);
-    tiles += static_cast<long long>((s.len + amsp::kTile - 1) / amsp::kTile);
-  }
-  if (tiles > 0x7fffffffLL) throw Error("engine: shard too large");
-  return static_cast<int>(tiles);
-}
-
-// A run of consecutive tensors all-gathered by one launch.
-struct GatherUnit {
-  int first_tensor = 0, n_tensors = 0;
-  std::uint64_t elems = 0;
-  int seg_begin = 0, nseg = 0, ntiles = 0;
-};
-
-}  // namespace
-
-struct amsp_engine {
-  amsp_engine_config_t cfg{};
-  std::vector<std::uint64_t> tensor_sizes;
-  std::uint64_t phi = 0;
-  int world = 1, rank = 0, sp = 1;
-  amsp::ShardLayout layout;
-  amsp::PShardMap pmap;
-  amsp::MeshGroup os_group, p_group;
-  std::vector<int> dst_members;  // OS-block ranks holding my P position
-  int replicas = 1;
-
-  // Shared region and its offsets (identical on every rank).
-  char* shared = nullptr;
-  std::size_t shared_bytes = 0, off_grads = 0, off_params = 0, off_flags = 0;
-  std::uint64_t param_elems = 0;
-  void* peer_base[amsp::kMaxRanks] = {};
-  bool imported = false;
-  bool local_linked = false;  // single-GPU emulation: no barriers
-
-  float* master = nullptr;
-  float* exp_avg = nullptr;
-  float* exp_avg_sq = nullptr;
-  char* priv = nullptr;
-  amsp::Seg* d_segs = nullptr;
-  amsp::Seg* d_psegs = nullptr;
-  amsp::CopySeg* d_copy = nullptr;
-  uint16_t* slots[2] = {nullptr, nullptr};
-  std::uint64_t slot_elems = 0;
-  std::vector<GatherUnit> units;
-  float* stats = nullptr;
-  int* err = nullptr;
-  uint32_t** d_peer_flags = nullptr;
-  int nseg = 0, ntiles = 0, npseg = 0, nptiles = 0;
-  int grid = 0, variant = 0, sms = 148, gather_grid = 0;
-  std::uint64_t device_bytes = 0;
-
-  cudaStream_t own_stream = nullptr;
-  // Linked (single-GPU emulated) engines share rank 0's stream so that one
-  // rank's step is ordered after every rank's gradient production.
-  cudaStream_t shared_default = nullptr;
-  uint32_t epoch = 0;
-  // Optional CUDA-event bracketing of every fused launch (bench roofline).
-  bool time_kernel = false;
-  using EventPairs = std::vector<std::pair<cudaEvent_t, cudaEvent_t>>;
-  EventPairs kernel_events, gather_events;
-  std::size_t kernel_events_used = 0, gather_events_used = 0;
-  std::uint64_t launches = 0;
-
-  // When timing is on, records the start event of the next pair and returns
-  // the end event to record after the timed work (else nullptr).
-  cudaEvent_t record_begin(EventPairs& pairs, std::size_t& used, cudaStream_t s) {
-    if (!time_kernel) return nullptr;
-    if (used == pairs.size()) {
-      cudaEvent_t x, y;
-      ck(cudaEventCreate(&x), "event");
-      ck(cudaEventCreate(&y), "event");
-      pairs.emplace_back(x, y);
-    }
-    auto& ev = pairs[used++];
-    ck(cudaEventRecord(ev.first, s), "event record");
-    return ev.second;
-  }
-
-  static double sum_ms(EventPairs& pairs, std::size_t used) {
-    double sum = 0.0;
-    for (std::size_t i = 0; i < used; ++i) {
-      ck(cudaEventSynchronize(pairs[i].second), "event sync");
-      float ms = 0.0f;
-      ck(cudaEventElapsedTime(&ms, pairs[i].first, pairs[i].second), "event elapsed");
-      sum += ms;
-    }
-    return sum;
-  }
-
-  uint16_t* grads_of(int r) const {
-    return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_grads);
-  }
-  uint16_t* params_of(int r) const {
-    return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_params);
-  }
-  uint32_t* flags_of(int r) const {
-    return reinterpret_cast<uint32_t*>(static_cast<char*>(peer_base[r]) + off_flags);
-  }
-  cudaStream_t pick(void* s) const {
-    if (s) return static_cast<cudaStream_t>(s);
-    return shared_default ? shared_default : own_stream;
-  }
-  void use_device() const { ck(cudaSetDevice(cfg.device), "cudaSetDevice"); }
-
-  // Auto (v = 0) for one rank: one 8-element vector in flight per thread,
-  // <= 64 registers, 2 CTAs per SM — the best point of the r01 sweep on
-  // LLaMA-7B (tools/tune_fused.py, profiles/r01_tune_7b.jsonl).
-  void retune(int v, int forced_grid) {
-    variant = (v == 0 && world == 1) ? 4 : v;
-    const int per_sm = amsp::fused_blocks_per_sm(world, variant);
-    int g = sms * per_sm;
-    if (v == 0 && world == 1) g = 2 * sms;
-    grid = forced_grid > 0 ? forced_grid : g;
-    grid = std::max(1, std::min(ntiles, grid));
-  }
-
-  void publish_peer_flags() {
-    uint32_t* h[amsp::kMaxRanks] = {};
-    for (int r = 0; r < world; ++r) h[r] = flags_of(r);
-    ck(cudaMemcpy(d_peer_flags, h, sizeof(h), cudaMemcpyHostToDevice),
-       "copy peer flag table");
-  }
-
-  void barrier(cudaStream_t s) {
-    if (world == 1 || local_linked) return;
-    ++epoch;
-    ck(amsp::launch_barrier(d_peer_flags, world, rank, epoch, err, s), "barrier launch");
-    ++launches;
-  }
-
-  void check_err() {
-    int h = 0;
-    ck(cudaMemcpy(&h, err, sizeof(int), cudaMemcpyDeviceToHost), "read error flag");
-    if (h) throw amsp::CudaFailure("cross-GPU barrier timed out (a peer did not arrive)");
-  }
-
-  void require_peers() const {
-    if (world > 1 && !imported)
-      throw Error("engine: peers not imported (amsp_engine_import_handles)");
-  }
-
-  // AG of one gather unit into slot `slot` (s_p > 1).
-  void gather(int unit, int slot, cudaStream_t s) {
-    if (sp == 1) throw Error("engine: gather needs parameter sharding (s_p > 1)");
-    if (unit < 0 || unit >= static_cast<int>(units.size()))
-      throw Error("engine: gather unit out of range");
-    require_peers();
-    const GatherUnit& u = units[unit];
-    amsp::GatherArgs g{};
-    g.segs = d_copy + u.seg_begin;
-    g.nseg = u.nseg;
-    g.ntiles = u.ntiles;
-    for (int q = 0; q < sp; ++q) g.src[q] = params_of(p_group.members[q]);
-    g.dst = slots[slot & 1];
-    g.grid = gather_grid;
-    g.sp = sp;
-    g.rot = (p_group.position + 1) % sp;
-    ck(amsp::launch_gather(g, s), "gather launch");
-    ++launches;
-  }
-
-  void step(int t, cudaStream_t s) {
-    if (t < 1) throw Error("engine: step index must be >= 1");
-    require_peers();
-    if (sp > 1 && !cfg.skip_gathers) {
-      // Forward then backward parameter all-gathers (T_p's two AG terms,
-      // cost_model.cpp:46-49); RS is fused into the optimizer kernel below.
-      cudaEvent_t g_end = record_begin(gather_events, gather_events_used, s);
-      const int n = static_cast<int>(units.size());
-      for (int u = 0; u < n; ++u) gather(u, u, s);
-      for (int u = n - 1; u >= 0; --u) gather(u, u, s);
-      if (g_end) ck(cudaEventRecord(g_end, s), "event record");
-    }
-    amsp::FusedArgs a{};
-    a.segs = d_segs;
-    a.nseg = nseg;
-    a.ntiles = ntiles;
-    for (int r = 0; r < world; ++r) a.grads[r] = grads_of(r);
-    a.ndst = static_cast<int>(dst_members.size());
-    for (int d = 0; d < a.ndst; ++d) a.dsts[d] = params_of(dst_members[d]);
-    a.master = master;
-    a.exp_avg = exp_avg;
-    a.exp_avg_sq = exp_avg_sq;
-    a.s = amsp::make_adam_scalars(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
-                                  cfg.weight_decay, t, 1.0 / world);
-    a.stats = stats;
-    a.fence_peers = (world > 1 && !local_linked) ? 1 : 0;
-    ck(cudaMemsetAsync(stats, 0, 2 * sizeof(float), s), "reset stats");
-    barrier(s);  // every rank's gradients are complete
-    cudaEvent_t t_end =
-        ntiles > 0 ? record_begin(kernel_events, kernel_events_used, s) : nullptr;
-    ck(amsp::launch_fused_step(a, world, grid, variant, s), "fused step launch");
-    if (t_end) ck(cudaEventRecord(t_end, s), "event record");
-    if (ntiles > 0) ++launches;
-    barrier(s);  // every owner's parameter stores have landed
-  }
-};
+#include "engine_impl.h"
 
 namespace {
 
@@ -359,9 +129,9 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   e->off_grads = 0;
   e->off_params = align_up(e->phi * 2);
   e->off_flags = e->off_params + align_up(e->param_elems * 2);
-  e->shared_bytes = e->off_flags + align_up(64 * sizeof(uint32_t));
+  e->shared_bytes = e->off_flags + align_up(kFlagBytes);
   ck(cudaMalloc(&e->shared, e->shared_bytes), "cudaMalloc shared");
-  ck(cudaMemset(e->shared + e->off_flags, 0, 64 * sizeof(uint32_t)), "zero flags");
+  ck(cudaMemset(e->shared + e->off_flags, 0, kFlagBytes), "zero flags");
   for (int r = 0; r < e->world; ++r) e->peer_base[r] = e->shared;
 
   // Segment tables: the OS shard, and the whole P shard (for init).
@@ -703,6 +473,7 @@ void amsp_engine_destroy(amsp_engine_t* e) {
       cudaEventDestroy(ev.second);
     }
   delete e;
+  cudaGetLastError();  // teardown must not leave a sticky error for the next call
 }
 
 // ------------------------------------------------------------ raw kernels

@@ -231,18 +231,21 @@ fused_step_kernel(const FusedArgs a) {
   }
 }
 
-// Cross-GPU barrier over NVLink: thread r publishes this rank's epoch into
-// rank r's flag array (slot `rank`) and waits for rank r's epoch in its own
-// array. Bounded wait: after ~20 s it raises *err instead of hanging.
-__global__ void barrier_kernel(uint32_t* const* peer_flags, int world, int rank,
+// Cross-GPU barrier over NVLink. Barrier `id` owns kMaxRanks flag words in
+// every rank's flag array: thread r publishes this rank's epoch into rank
+// r's word [id][rank] and waits until its own word [id][r] reaches the
+// epoch. Distinct ids never interfere, so barriers issued on different
+// streams may complete in any order. Bounded wait: after ~20 s it raises
+// *err instead of hanging.
+__global__ void barrier_kernel(uint32_t* const* peer_flags, int world, int rank, int id,
                                uint32_t epoch, int* err) {
   const int t = threadIdx.x;
   __threadfence_system();
   if (t < world) {
-    uint32_t* slot = peer_flags[t] + rank;
+    uint32_t* slot = peer_flags[t] + id * kMaxRanks + rank;
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch)
                  : "memory");
-    const uint32_t* mine = peer_flags[rank] + t;
+    const uint32_t* mine = peer_flags[rank] + id * kMaxRanks + t;
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (true) {
@@ -387,6 +390,125 @@ __global__ void upcast_scale_kernel(const uint16_t* __restrict__ src, float* __r
     dst[i] = __fmul_rn(bf16_at(src[i]), scale);
 }
 
+// Reduce half of the split step: red[os] = (sum_r grads_r[flat]) * scale,
+// fixed rank order (bit-equal to the fused kernel's sum).
+template <int W>
+__global__ void __launch_bounds__(kBlock) reduce_kernel(const ReduceArgs a) {
+  __shared__ Seg s_segs[kSegCap];
+  SegCursor<Seg, kSegCap> cursor;
+  cursor.init(s_segs, a.segs, a.nseg);
+  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    const Seg sg = cursor.at(tile);
+    const unsigned long long base = (static_cast<unsigned long long>(tile) - sg.tile0) * kTile;
+    const bool aligned = ((sg.flat | sg.os) & 7ull) == 0;
+#pragma unroll 1
+    for (int it = 0; it < kVecPerThread; ++it) {
+      const unsigned long long e = base + (static_cast<unsigned long long>(it) * kBlock +
+                                           threadIdx.x) * 8ull;
+      if (e >= sg.len) continue;
+      if (aligned && e + 8 <= sg.len) {
+        uint4 g[W];
+#pragma unroll
+        for (int r = 0; r < W; ++r) g[r] = ld_ro_v4(a.grads[r] + sg.flat + e);
+        float out[8];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t* g0 = reinterpret_cast<const uint32_t*>(&g[0]);
+          float lo = bf16_lo(g0[w]), hi = bf16_hi(g0[w]);
+#pragma unroll
+          for (int r = 1; r < W; ++r) {
+            const uint32_t* gr = reinterpret_cast<const uint32_t*>(&g[r]);
+            lo = __fadd_rn(lo, bf16_lo(gr[w]));
+            hi = __fadd_rn(hi, bf16_hi(gr[w]));
+          }
+          out[2 * w] = __fmul_rn(lo, a.scale);
+          out[2 * w + 1] = __fmul_rn(hi, a.scale);
+        }
+        st_stream_v4(a.red + sg.os + e, make_float4(out[0], out[1], out[2], out[3]));
+        st_stream_v4(a.red + sg.os + e + 4, make_float4(out[4], out[5], out[6], out[7]));
+      } else {
+        const unsigned long long end = e + 8 < sg.len ? e + 8 : sg.len;
+        for (unsigned long long k = e; k < end; ++k) {
+          float g = bf16_at(a.grads[0][sg.flat + k]);
+#pragma unroll
+          for (int r = 1; r < W; ++r) g = __fadd_rn(g, bf16_at(a.grads[r][sg.flat + k]));
+          a.red[sg.os + k] = __fmul_rn(g, a.scale);
+        }
+      }
+    }
+  }
+}
+
+// AdamW + downcast + parameter push half of the split step.
+__global__ void __launch_bounds__(kBlock) adam_push_kernel(const AdamPushArgs a) {
+  __shared__ Seg s_segs[kSegCap];
+  SegCursor<Seg, kSegCap> cursor;
+  cursor.init(s_segs, a.segs, a.nseg);
+  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    const Seg sg = cursor.at(tile);
+    const unsigned long long base = (static_cast<unsigned long long>(tile) - sg.tile0) * kTile;
+    const bool aligned = ((sg.os | sg.dst) & 7ull) == 0;
+#pragma unroll 1
+    for (int it = 0; it < kVecPerThread; ++it) {
+      const unsigned long long e = base + (static_cast<unsigned long long>(it) * kBlock +
+                                           threadIdx.x) * 8ull;
+      if (e >= sg.len) continue;
+      const unsigned long long o = sg.os + e;
+      if (aligned && e + 8 <= sg.len) {
+        float4 g[2] = {ld_state_v4(a.red + o), ld_state_v4(a.red + o + 4)};
+        float4 p[2] = {ld_state_v4(a.master + o), ld_state_v4(a.master + o + 4)};
+        float4 m[2] = {ld_state_v4(a.exp_avg + o), ld_state_v4(a.exp_avg + o + 4)};
+        float4 v[2] = {ld_state_v4(a.exp_avg_sq + o), ld_state_v4(a.exp_avg_sq + o + 4)};
+        float* gf = reinterpret_cast<float*>(g);
+        float* pf = reinterpret_cast<float*>(p);
+        float* mf = reinterpret_cast<float*>(m);
+        float* vf = reinterpret_cast<float*>(v);
+        uint32_t packed[4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) adamw(a.s, gf[j], pf[j], mf[j], vf[j]);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) packed[w] = pack_bf16x2(pf[2 * w], pf[2 * w + 1]);
+        st_stream_v4(a.master + o, p[0]);
+        st_stream_v4(a.master + o + 4, p[1]);
+        st_stream_v4(a.exp_avg + o, m[0]);
+        st_stream_v4(a.exp_avg + o + 4, m[1]);
+        st_stream_v4(a.exp_avg_sq + o, v[0]);
+        st_stream_v4(a.exp_avg_sq + o + 4, v[1]);
+        const uint4 out = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        for (int d = 0; d < a.ndst; ++d) st_v4(a.dsts[d] + sg.dst + e, out);
+      } else {
+        const unsigned long long end = e + 8 < sg.len ? e + 8 : sg.len;
+        for (unsigned long long k = e; k < end; ++k) {
+          float p = a.master[sg.os + k], m = a.exp_avg[sg.os + k], v = a.exp_avg_sq[sg.os + k];
+          adamw(a.s, a.red[sg.os + k], p, m, v);
+          a.master[sg.os + k] = p;
+          a.exp_avg[sg.os + k] = m;
+          a.exp_avg_sq[sg.os + k] = v;
+          const uint16_t b = to_bf16(p);
+          for (int d = 0; d < a.ndst; ++d) a.dsts[d][sg.dst + k] = b;
+        }
+      }
+    }
+  }
+  if (a.fence_peers) __threadfence_system();
+}
+
+// Compute stand-in for the overlap schedule: every CTA keeps its warps
+// issuing dependent FMAs for `ns` nanoseconds (timed per CTA, so CTAs that
+// wait for SM slots held by communication kernels finish later — the
+// stand-in has a fixed amount of per-CTA work, like a GEMM tile loop).
+__global__ void spin_kernel(unsigned long long ns, float* sink) {
+  unsigned long long t0, now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  float x = threadIdx.x * 1e-3f, y = 1.0f;
+  do {
+#pragma unroll
+    for (int i = 0; i < 64; ++i) x = fmaf(x, 0.999f, y);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+  } while (now - t0 < ns);
+  if (x == 123.456f) sink[threadIdx.x] = x;  // keep the loop alive
+}
+
 int sm_count() {
   static int n = [] {
     int dev = 0, c = 148;
@@ -445,9 +567,38 @@ cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int varia
   return cudaGetLastError();
 }
 
-cudaError_t launch_barrier(uint32_t* const* peer_flags, int world, int rank,
+cudaError_t launch_barrier(uint32_t* const* peer_flags, int world, int rank, int id,
                            uint32_t epoch, int* err, cudaStream_t stream) {
-  barrier_kernel<<<1, 32, 0, stream>>>(peer_flags, world, rank, epoch, err);
+  barrier_kernel<<<1, 32, 0, stream>>>(peer_flags, world, rank, id, epoch, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(const ReduceArgs& a, int world, int grid, cudaStream_t stream) {
+  if (a.ntiles == 0) return cudaSuccess;
+  grid = std::max(1, std::min(a.ntiles, grid));
+  switch (world) {
+    case 1: reduce_kernel<1><<<grid, kBlock, 0, stream>>>(a); break;
+    case 2: reduce_kernel<2><<<grid, kBlock, 0, stream>>>(a); break;
+    case 3: reduce_kernel<3><<<grid, kBlock, 0, stream>>>(a); break;
+    case 4: reduce_kernel<4><<<grid, kBlock, 0, stream>>>(a); break;
+    case 5: reduce_kernel<5><<<grid, kBlock, 0, stream>>>(a); break;
+    case 6: reduce_kernel<6><<<grid, kBlock, 0, stream>>>(a); break;
+    case 7: reduce_kernel<7><<<grid, kBlock, 0, stream>>>(a); break;
+    case 8: reduce_kernel<8><<<grid, kBlock, 0, stream>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adam_push(const AdamPushArgs& a, int grid, cudaStream_t stream) {
+  if (a.ntiles == 0) return cudaSuccess;
+  adam_push_kernel<<<std::max(1, std::min(a.ntiles, grid)), kBlock, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spin(int ctas, unsigned long long ns, cudaStream_t stream) {
+  if (ns == 0 || ctas <= 0) return cudaSuccess;
+  spin_kernel<<<ctas, 128, 0, stream>>>(ns, nullptr);
   return cudaGetLastError();
 }
 

@@ -73,8 +73,39 @@ int fused_blocks_per_sm(int world, int variant);
 
 cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int variant,
                               cudaStream_t stream);
-cudaError_t launch_barrier(uint32_t* const* peer_flags, int world, int rank,
+// Barrier `id` (0 .. kBarrierIds-1): flag words [id*kMaxRanks, +world).
+constexpr int kBarrierIds = 8192;
+cudaError_t launch_barrier(uint32_t* const* peer_flags, int world, int rank, int id,
                            uint32_t epoch, int* err, cudaStream_t stream);
+
+// Split form of the fused step, used by the overlap scheduler: the reduce
+// runs per gradient bucket / module during backward into an fp32 shard
+// buffer; AdamW + parameter push runs once after the step's barrier.
+struct ReduceArgs {
+  const Seg* segs;   // os = offset in the fp32 reduced-gradient shard
+  int nseg;
+  int ntiles;
+  const uint16_t* grads[kMaxRanks];
+  float* red;
+  float scale;
+};
+struct AdamPushArgs {
+  const Seg* segs;
+  int nseg;
+  int ntiles;
+  const float* red;
+  uint16_t* dsts[kMaxRanks];
+  int ndst;
+  float* master;
+  float* exp_avg;
+  float* exp_avg_sq;
+  AdamScalars s;
+  int fence_peers;
+};
+cudaError_t launch_reduce(const ReduceArgs& a, int world, int grid, cudaStream_t stream);
+cudaError_t launch_adam_push(const AdamPushArgs& a, int grid, cudaStream_t stream);
+// Compute stand-in: `ctas` CTAs, each busy for `ns` nanoseconds of FMA work.
+cudaError_t launch_spin(int ctas, unsigned long long ns, cudaStream_t stream);
 // params[dst+k] = bf16(master_init(flat+k)) over a P-shard segment table.
 cudaError_t launch_init_params(const Seg* psegs, int nseg, int ntiles, uint16_t* params,
                                uint64_t seed, cudaStream_t stream);

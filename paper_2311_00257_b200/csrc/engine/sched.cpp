@@ -1,0 +1,537 @@
+// Overlap scheduler: executes the reference's one-step event graph
+// (shardplan::build_schedule, overlap_sim.cpp:122-457 — Fig 7(a)(b)(c) and
+// the Table V tiers) on real CUDA streams of one B200, with the AMSP data
+// plane doing the communication (north-star item 4).
+//
+//   stream 0 (caller's)  compute events -> compute stand-in kernels whose
+//                        durations are the graph's (FLOPs / peak x eff, or
+//                        a measured per-module table)
+//   stream 1             AllGather (l, i)     -> NVLink gather of tensor (l,i)
+//                        ReduceScatter (l, i) -> cross-GPU barrier + pull-
+//                                                reduce of tensor (l,i)
+//   stream 2             AllReduceBucket b    -> barrier + pull-reduce of
+//                                                bucket b's owned elements
+//                        BroadcastShard       -> marker (the push is below)
+//   after the graph      barrier -> update of whatever is left -> barrier
+//
+// Cross-stream dependencies are cudaEvents exactly as in Event::depends_on;
+// events on one stream keep graph order. Gradient buckets are the graph's
+// own cuts: the backward-ordered gradient byte stream (head first, then
+// layers L-1..0, modules K-1..0) cut every s_p * U bytes (overlap_sim.cpp:
+// 285-312), mapped onto the flat parameter vector.
+//
+// Optimizer placement (`optimizer_overlap`):
+//   0 — the paper's barrier semantics (overlap_sim.cpp:166-174, PAPER.md:
+//       299-312): reduces land in an fp32 shard during backward; AdamW +
+//       bf16 push to the OS-group owners run once after the step's barrier.
+//   1 — the optimizer moves into the backward pass: s_p > 1 runs the fused
+//       reduce + AdamW + push per module right after its reduce-scatter
+//       barrier (every rank has passed that module's gradient, so no rank
+//       reads its parameters again this step); s_p = 1 runs AdamW + push per
+//       bucket after a second barrier that certifies every rank finished the
+//       bucket's grad-input (the last reader of those replicated params).
+// Either way the arithmetic is bit-equal to the fused kernel and the oracle.
+#include "engine_impl.h"
+#include "../convert.h"
+
+namespace {
+
+enum class Work { Compute, Gather, Reduce, ReduceAdam, Marker };
+
+struct EventWork {
+  Work kind = Work::Marker;
+  int stream = 0;
+  int tensor = -1;
+  int barrier = -1;
+  int seg_begin = 0, nseg = 0, ntiles = 0;
+  unsigned long long ns = 0;
+  bool record = false;
+  // s_p = 1 with optimizer overlap: AdamW + push of this bucket after the
+  // local grad-input event `after_event` and barrier `barrier2`.
+  bool adam_after = false;
+  int after_event = -1;
+  int barrier2 = -1;
+};
+
+struct Table {
+  int begin = 0, nseg = 0, ntiles = 0;
+};
+
+constexpr int kFirstSchedBarrier = 16;  // ids 0..15 stay with the engine
+
+}  // namespace
+
+struct amsp_sched {
+  amsp_engine* e = nullptr;
+  shardplan::EventGraph graph;
+  double predicted_step = 0.0, predicted_compute = 0.0;
+  int comm_ctas = 128, compute_ctas = 148;
+  double time_scale = 1.0;
+  bool optimizer_overlap = true;
+  std::vector<EventWork> work;
+  int n_barriers = 0, end_a = 0, end_b = 0, n_buckets = 0, n_gather = 0, n_reduce = 0,
+      n_compute = 0;
+  Table resid, pending;  // end of step: fused update / AdamW-from-reduced update
+  amsp::Seg* d_rsegs = nullptr;
+  amsp::CopySeg* d_tcopy = nullptr;
+  float* red = nullptr;
+  cudaStream_t comm[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> events;
+  cudaEvent_t start_ev = nullptr, join_ev[2] = {nullptr, nullptr};
+  uint32_t epoch = 0;
+  amsp::AdamScalars scalars{};
+
+  ~amsp_sched() {
+    if (e) cudaSetDevice(e->cfg.device);
+    cudaDeviceSynchronize();
+    for (auto ev : events)
+      if (ev) cudaEventDestroy(ev);
+    if (start_ev) cudaEventDestroy(start_ev);
+    for (auto ev : join_ev)
+      if (ev) cudaEventDestroy(ev);
+    for (auto s : comm)
+      if (s) cudaStreamDestroy(s);
+    cudaFree(d_rsegs);
+    cudaFree(d_tcopy);
+    cudaFree(red);
+    cudaGetLastError();  // teardown must not leave a sticky error for the next call
+  }
+
+  cudaStream_t stream_of(int s, cudaStream_t main) const {
+    return s == 0 ? main : comm[s == 1 ? 0 : 1];
+  }
+
+  void barrier(int id, cudaStream_t s) {
+    if (e->world == 1 || e->local_linked) return;
+    ck(amsp::launch_barrier(e->d_peer_flags, e->world, e->rank, id, epoch, e->err, s),
+       "sched barrier");
+    ++e->launches;
+  }
+
+  void reduce(const Table& t, int grid, cudaStream_t s) {
+    if (t.ntiles == 0) return;
+    amsp::ReduceArgs a{};
+    a.segs = d_rsegs + t.begin;
+    a.nseg = t.nseg;
+    a.ntiles = t.ntiles;
+    for (int r = 0; r < e->world; ++r) a.grads[r] = e->grads_of(r);
+    a.red = red;
+    a.scale = static_cast<float>(1.0 / e->world);
+    ck(amsp::launch_reduce(a, e->world, grid, s), "sched reduce");
+    ++e->launches;
+  }
+
+  void adam_push(const Table& t, int grid, cudaStream_t s) {
+    if (t.ntiles == 0) return;
+    amsp::AdamPushArgs a{};
+    a.segs = d_rsegs + t.begin;
+    a.nseg = t.nseg;
+    a.ntiles = t.ntiles;
+    a.red = red;
+    a.ndst = static_cast<int>(e->dst_members.size());
+    for (int d = 0; d < a.ndst; ++d) a.dsts[d] = e->params_of(e->dst_members[d]);
+    a.master = e->master;
+    a.exp_avg = e->exp_avg;
+    a.exp_avg_sq = e->exp_avg_sq;
+    a.s = scalars;
+    a.fence_peers = (e->world > 1 && !e->local_linked) ? 1 : 0;
+    ck(amsp::launch_adam_push(a, grid, s), "adam push");
+    ++e->launches;
+  }
+
+  void fused(const Table& t, int grid, cudaStream_t s) {
+    if (t.ntiles == 0) return;
+    amsp::FusedArgs a{};
+    a.segs = d_rsegs + t.begin;
+    a.nseg = t.nseg;
+    a.ntiles = t.ntiles;
+    for (int r = 0; r < e->world; ++r) a.grads[r] = e->grads_of(r);
+    a.ndst = static_cast<int>(e->dst_members.size());
+    for (int d = 0; d < a.ndst; ++d) a.dsts[d] = e->params_of(e->dst_members[d]);
+    a.master = e->master;
+    a.exp_avg = e->exp_avg;
+    a.exp_avg_sq = e->exp_avg_sq;
+    a.s = scalars;
+    a.stats = nullptr;
+    a.fence_peers = (e->world > 1 && !e->local_linked) ? 1 : 0;
+    ck(amsp::launch_fused_step(a, e->world, grid, 0, s), "sched fused");
+    ++e->launches;
+  }
+
+  void gather_tensor(int t, cudaStream_t s) {
+    amsp::GatherArgs g{};
+    g.segs = d_tcopy + t;
+    g.nseg = 1;
+    const unsigned long long len = e->pmap.slice_len[t];
+    g.ntiles = static_cast<int>((len + amsp::kTile - 1) / amsp::kTile) * e->sp;
+    g.sp = e->sp;
+    g.rot = (e->p_group.position + 1) % e->sp;
+    for (int q = 0; q < e->sp; ++q) g.src[q] = e->params_of(e->p_group.members[q]);
+    g.dst = e->slots[t & 1];
+    g.grid = comm_ctas;
+    ck(amsp::launch_gather(g, s), "sched gather");
+    ++e->launches;
+  }
+
+  void run(int step, cudaStream_t main, bool with_comm) {
+    if (step < 1) throw Error("sched: step index must be >= 1");
+    e->require_peers();
+    ++epoch;
+    scalars = amsp::make_adam_scalars(e->cfg.lr, e->cfg.beta1, e->cfg.beta2, e->cfg.eps,
+                                      e->cfg.weight_decay, step, 1.0 / e->world);
+    ck(cudaEventRecord(start_ev, main), "event record");
+    for (auto s : comm) ck(cudaStreamWaitEvent(s, start_ev, 0), "stream wait");
+    const auto& evs = graph.events;
+    for (std::size_t i = 0; i < evs.size(); ++i) {
+      const EventWork& w = work[i];
+      cudaStream_t st = stream_of(w.stream, main);
+      for (int d : evs[i].depends_on)
+        if (work[d].stream != w.stream && work[d].record)
+          ck(cudaStreamWaitEvent(st, events[d], 0), "stream wait");
+      const Table t{w.seg_begin, w.nseg, w.ntiles};
+      switch (w.kind) {
+        case Work::Compute:
+          ck(amsp::launch_spin(compute_ctas, w.ns, st), "compute stand-in");
+          ++e->launches;
+          break;
+        case Work::Gather:
+          if (with_comm) gather_tensor(w.tensor, st);
+          break;
+        case Work::Reduce:
+          if (with_comm) {
+            barrier(w.barrier, st);
+            reduce(t, comm_ctas, st);
+            if (w.adam_after) {
+              ck(cudaStreamWaitEvent(st, events[w.after_event], 0), "stream wait");
+              barrier(w.barrier2, st);
+              adam_push(t, comm_ctas, st);
+            }
+          }
+          break;
+        case Work::ReduceAdam:
+          if (with_comm) {
+            barrier(w.barrier, st);
+            fused(t, comm_ctas, st);
+          }
+          break;
+        case Work::Marker:
+          break;
+      }
+      if (w.record) ck(cudaEventRecord(events[i], st), "event record");
+    }
+    for (int k = 0; k < 2; ++k) {
+      ck(cudaEventRecord(join_ev[k], comm[k]), "event record");
+      ck(cudaStreamWaitEvent(main, join_ev[k], 0), "stream wait");
+    }
+    if (!with_comm) return;
+    // Barrier semantics (overlap_sim.cpp:166-174): every gradient is reduced
+    // on every rank before the remaining owners update and push.
+    const int full_grid = e->sms * amsp::fused_blocks_per_sm(e->world, 0);
+    barrier(end_a, main);
+    fused(resid, full_grid, main);
+    adam_push(pending, e->sms * 2, main);
+    barrier(end_b, main);
+  }
+};
+
+namespace {
+
+using FlatRange = std::pair<std::uint64_t, std::uint64_t>;  // [begin, end)
+
+// Owned pieces of the flat ranges: (flat, os, dst, len) with a fresh tile
+// prefix, appended to `out`.
+Table owned_pieces(const amsp::ShardLayout& L, const std::vector<FlatRange>& ranges,
+                   std::vector<amsp::Seg>& out) {
+  Table t;
+  t.begin = static_cast<int>(out.size());
+  for (const auto& [a, b] : ranges) {
+    // segments are ascending in flat order (pshard_layout builds them so)
+    auto it = std::upper_bound(L.segs.begin(), L.segs.end(), a,
+                               [](std::uint64_t x, const amsp::Segment& s) { return x < s.flat; });
+    if (it != L.segs.begin()) --it;
+    for (; it != L.segs.end() && it->flat < b; ++it) {
+      const std::uint64_t lo = std::max(a, it->flat), hi = std::min(b, it->flat + it->len);
+      if (lo >= hi) continue;
+      const std::uint64_t off = lo - it->flat;
+      out.push_back({lo, it->os + off, it->dst + off, hi - lo, 0});
+    }
+  }
+  long long tiles = 0;
+  for (std::size_t i = static_cast<std::size_t>(t.begin); i < out.size(); ++i) {
+    out[i].tile0 = static_cast<unsigned long long>(tiles);
+    tiles += static_cast<long long>((out[i].len + amsp::kTile - 1) / amsp::kTile);
+  }
+  t.nseg = static_cast<int>(out.size()) - t.begin;
+  t.ntiles = static_cast<int>(tiles);
+  return t;
+}
+
+void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* profile) {
+  amsp_engine* e = s->e;
+  using namespace amsp::conv;
+  const shardplan::ModelSpec model = model_in(&cfg->model);
+  model.check();
+  const int L = model.layer_count, K = model.modules_per_layer;
+  if (model.micro_batch_count != 1)
+    throw Error("sched: the executor runs one micro-batch per step (M = 1)");
+  // Tensor list = [embed] + L x K modules + [final norm, lm_head].
+  const std::size_t n = e->tensor_sizes.size();
+  if (n != static_cast<std::size_t>(L) * K + 3)
+    throw Error("sched: engine tensors must be embed + L*K modules + norm + head");
+  for (int l = 0; l < L; ++l)
+    for (int i = 0; i < K; ++i)
+      if (e->tensor_sizes[1 + l * K + i] != model.module_params[i])
+        throw Error("sched: engine tensor sizes do not match the model's layer template");
+  if (e->phi != model.total_params)
+    throw Error("sched: engine Phi differs from the model's total_params");
+  auto tensor_of = [K](int l, int i) { return 1 + l * K + i; };
+  auto range_of = [e](int t) {
+    const std::uint64_t a = e->pmap.tensor_offset[t];
+    return FlatRange{a, a + e->tensor_sizes[t]};
+  };
+  s->optimizer_overlap = cfg->optimizer_overlap != 0;
+
+  shardplan::ClusterSpec cl;
+  const DeviceMesh dp = to_mesh(e->cfg.dp_mesh);
+  cl.gpus_per_node = dp.per_node;
+  cl.node_count = dp.nodes;
+  cl.gpu_memory_capacity = std::uint64_t{1} << 50;
+  cl.dp_mesh = dp;
+  cl.topology = {dp.nodes, 1, 1.0};
+  const shardplan::ShardingPlan plan = plan_in(&e->cfg.plan);
+  const shardplan::CostConfig cost = cost_in(&cfg->cost);
+  const shardplan::SimConfig sim = sim_in(&cfg->sim, K);
+  s->graph = shardplan::build_schedule(model, cl, plan, profile->p, cost, sim);
+  const shardplan::Timeline tl = shardplan::simulate_step(s->graph);
+  s->predicted_step = tl.step_time;
+  s->predicted_compute = tl.busy.empty() ? 0.0 : tl.busy[0];
+
+  // Gradient buckets as flat ranges (backward order: head = lm_head, final
+  // norm, embed; then layers / modules descending), plus, per bucket, the
+  // modules (tensors) it touches.
+  std::vector<std::pair<int, FlatRange>> stream_ranges = {
+      {static_cast<int>(n) - 1, range_of(static_cast<int>(n) - 1)},
+      {static_cast<int>(n) - 2, range_of(static_cast<int>(n) - 2)},
+      {0, range_of(0)}};
+  for (int l = L - 1; l >= 0; --l)
+    for (int i = K - 1; i >= 0; --i) stream_ranges.push_back({tensor_of(l, i), range_of(tensor_of(l, i))});
+  const std::uint64_t cut =
+      cost.bucket_size * static_cast<std::uint64_t>(plan.sp()) / model.bytes_per_grad;
+  std::vector<std::vector<FlatRange>> buckets(1);
+  std::vector<std::vector<int>> bucket_tensors(1);
+  std::uint64_t filled = 0;
+  for (auto [t, r] : stream_ranges) {
+    auto [a, b] = r;
+    while (a < b) {
+      const std::uint64_t take = std::min(b - a, cut - filled);
+      buckets.back().push_back({a, a + take});
+      bucket_tensors.back().push_back(t);
+      a += take;
+      filled += take;
+      if (filled == cut) {
+        buckets.emplace_back();
+        bucket_tensors.emplace_back();
+        filled = 0;
+      }
+    }
+  }
+  if (buckets.back().empty()) {
+    buckets.pop_back();
+    bucket_tensors.pop_back();
+  }
+
+  const auto& evs = s->graph.events;
+  // Last grad-input event of each tensor (head tensors: the head's gi).
+  std::vector<int> gi_event(n, -1);
+  for (std::size_t i = 0; i < evs.size(); ++i) {
+    if (evs[i].kind != shardplan::EventKind::BwdGradInput) continue;
+    if (evs[i].layer < 0) {
+      gi_event[0] = gi_event[n - 2] = gi_event[n - 1] = static_cast<int>(i);
+    } else {
+      gi_event[tensor_of(evs[i].layer, evs[i].module)] = static_cast<int>(i);
+    }
+  }
+
+  std::vector<amsp::Seg> rsegs;
+  std::vector<char> covered(n, 0);  // reduced by some event
+  std::vector<char> updated(n, 0);  // optimizer already applied by some event
+  int next_barrier = kFirstSchedBarrier;
+  s->work.resize(evs.size());
+  int ar_seen = 0;
+  for (std::size_t i = 0; i < evs.size(); ++i) {
+    const shardplan::Event& ev = evs[i];
+    EventWork& w = s->work[i];
+    w.stream = ev.stream;
+    switch (ev.kind) {
+      case shardplan::EventKind::FwdCompute:
+      case shardplan::EventKind::BwdGradInput:
+      case shardplan::EventKind::BwdGradWeight:
+      case shardplan::EventKind::RecomputeFwd:
+        w.kind = Work::Compute;
+        w.ns = static_cast<unsigned long long>(ev.duration * cfg->time_scale * 1e9);
+        ++s->n_compute;
+        break;
+      case shardplan::EventKind::AllGather:
+        w.kind = Work::Gather;
+        w.tensor = tensor_of(ev.layer, ev.module);
+        ++s->n_gather;
+        break;
+      case shardplan::EventKind::ReduceScatter: {
+        w.tensor = tensor_of(ev.layer, ev.module);
+        covered[w.tensor] = 1;
+        const Table t = owned_pieces(e->layout, {range_of(w.tensor)}, rsegs);
+        w.seg_begin = t.begin;
+        w.nseg = t.nseg;
+        w.ntiles = t.ntiles;
+        w.barrier = next_barrier++;
+        if (s->optimizer_overlap) {
+          w.kind = Work::ReduceAdam;
+          updated[w.tensor] = 1;
+        } else {
+          w.kind = Work::Reduce;
+        }
+        ++s->n_reduce;
+        break;
+      }
+      case shardplan::EventKind::AllReduceBucket: {
+        ++ar_seen;
+        if (plan.sp() > 1) {
+          // The module reduce-scatters already summed over every DP rank.
+          w.kind = Work::Marker;
+          break;
+        }
+        if (ev.module >= static_cast<int>(buckets.size()))
+          throw Error("sched: bucket index beyond the gradient stream");
+        w.kind = Work::Reduce;
+        const Table t = owned_pieces(e->layout, buckets[ev.module], rsegs);
+        w.seg_begin = t.begin;
+        w.nseg = t.nseg;
+        w.ntiles = t.ntiles;
+        w.barrier = next_barrier++;
+        if (s->optimizer_overlap) {
+          int last = -1;
+          for (int tt : bucket_tensors[ev.module]) last = std::max(last, gi_event[tt]);
+          if (last >= 0) {
+            w.adam_after = true;
+            w.after_event = last;
+            w.barrier2 = next_barrier++;
+            s->work[last].record = true;
+          }
+        }
+        ++s->n_reduce;
+        break;
+      }
+      case shardplan::EventKind::BroadcastShard:
+        w.kind = Work::Marker;
+        break;
+    }
+  }
+  s->n_buckets = ar_seen;
+  if (plan.sp() == 1 && ar_seen > 0) {
+    if (ar_seen != static_cast<int>(buckets.size()))
+      throw Error("sched: graph has " + std::to_string(ar_seen) + " buckets, executor cut " +
+                  std::to_string(buckets.size()));
+    std::fill(covered.begin(), covered.end(), 1);
+    if (s->optimizer_overlap) {
+      for (std::size_t b = 0; b < buckets.size(); ++b) {
+        bool all_have_gi = true;
+        for (int tt : bucket_tensors[b]) all_have_gi &= gi_event[tt] >= 0;
+        if (!all_have_gi) throw Error("sched: bucket without grad-input events");
+      }
+      std::fill(updated.begin(), updated.end(), 1);
+    }
+  }
+  // After the graph: tensors nobody reduced get the fused update; reduced but
+  // not yet updated ones get AdamW from the fp32 reduced gradients.
+  std::vector<FlatRange> rest, pend;
+  for (std::size_t t = 0; t < n; ++t) {
+    if (!covered[t]) rest.push_back(range_of(static_cast<int>(t)));
+    else if (!updated[t]) pend.push_back(range_of(static_cast<int>(t)));
+  }
+  s->resid = owned_pieces(e->layout, rest, rsegs);
+  s->pending = owned_pieces(e->layout, pend, rsegs);
+  s->end_a = next_barrier++;
+  s->end_b = next_barrier++;
+  s->n_barriers = next_barrier - kFirstSchedBarrier;
+  if (next_barrier > amsp::kBarrierIds) throw Error("sched: too many barriers per step");
+
+  // An event is recorded when a later event on another stream waits on it.
+  for (std::size_t i = 0; i < evs.size(); ++i)
+    for (int d : evs[i].depends_on)
+      if (s->work[d].stream != s->work[i].stream) s->work[d].record = true;
+
+  // Device tables and buffers.
+  e->use_device();
+  if (!rsegs.empty()) {
+    ck(cudaMalloc(&s->d_rsegs, rsegs.size() * sizeof(amsp::Seg)), "cudaMalloc sched segs");
+    ck(cudaMemcpy(s->d_rsegs, rsegs.data(), rsegs.size() * sizeof(amsp::Seg),
+                  cudaMemcpyHostToDevice),
+       "copy sched segs");
+  }
+  if (e->sp > 1) {
+    std::vector<amsp::CopySeg> tc(n);
+    for (std::size_t t = 0; t < n; ++t)
+      tc[t] = {0, e->pmap.pshard_offset[t], e->pmap.slice_len[t], 0};
+    ck(cudaMalloc(&s->d_tcopy, n * sizeof(amsp::CopySeg)), "cudaMalloc tensor copies");
+    ck(cudaMemcpy(s->d_tcopy, tc.data(), n * sizeof(amsp::CopySeg), cudaMemcpyHostToDevice),
+       "copy tensor copies");
+  }
+  const bool needs_red = s->pending.ntiles > 0 || (plan.sp() == 1 && ar_seen > 0);
+  if (needs_red)
+    ck(cudaMalloc(&s->red, std::max<std::size_t>(e->layout.owned, 1) * sizeof(float)),
+       "cudaMalloc reduced grads");
+  s->events.resize(evs.size(), nullptr);
+  for (std::size_t i = 0; i < evs.size(); ++i)
+    if (s->work[i].record)
+      ck(cudaEventCreateWithFlags(&s->events[i], cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&s->start_ev, cudaEventDisableTiming), "event");
+  for (auto& ev : s->join_ev) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+  for (auto& st : s->comm) ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  s->comm_ctas = cfg->comm_ctas > 0 ? cfg->comm_ctas : 128;
+  s->compute_ctas = cfg->compute_ctas > 0 ? cfg->compute_ctas : e->sms;
+  s->time_scale = cfg->time_scale > 0 ? cfg->time_scale : 1.0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int amsp_sched_create(amsp_engine_t* e, const amsp_sched_config_t* cfg,
+                      const amsp_profile_t* profile, amsp_sched_t** out) {
+  return amsp::guarded([&] {
+    if (!e || !cfg || !profile || !out) throw Error("sched: null argument");
+    auto s = std::make_unique<amsp_sched>();
+    s->e = e;
+    amsp_sched_config_t c = *cfg;
+    if (c.time_scale <= 0) c.time_scale = 1.0;
+    build(s.get(), &c, profile);
+    *out = s.release();
+  });
+}
+
+int amsp_sched_info(const amsp_sched_t* s, amsp_sched_info_t* info) {
+  return amsp::guarded([&] {
+    if (!s || !info) throw Error("sched: null argument");
+    info->n_events = static_cast<int>(s->graph.events.size());
+    info->n_compute = s->n_compute;
+    info->n_gather = s->n_gather;
+    info->n_reduce = s->n_reduce;
+    info->n_buckets = s->n_buckets;
+    info->n_barriers = s->n_barriers;
+    info->stream_count = s->graph.stream_count;
+    info->predicted_step_s = s->predicted_step;
+    info->predicted_compute_s = s->predicted_compute;
+  });
+}
+
+int amsp_sched_step(amsp_sched_t* s, int step, void* stream, int with_comm) {
+  return amsp::guarded([&] {
+    if (!s) throw Error("sched: null argument");
+    s->e->use_device();
+    s->run(step, s->e->pick(stream), with_comm != 0);
+  });
+}
+
+void amsp_sched_destroy(amsp_sched_t* s) { delete s; }
+
+}  // extern "C"

@@ -178,6 +178,66 @@ class Engine:
             pass
 
 
+class Scheduler:
+    """Overlap scheduler over an Engine (amsp_sched_*): replays the reference
+    event graph for `model` / the engine's plan on 3 CUDA streams."""
+
+    def __init__(self, engine: Engine, model: ModelSpec, profile, cost=None, sim=None,
+                 comm_ctas: int = 0, compute_ctas: int = 0, time_scale: float = 1.0,
+                 optimizer_overlap: bool = True):
+        from .shardplan import CostConfig, SimConfig
+        cost = cost or CostConfig()
+        sim = sim or SimConfig()
+        m, self._keep = model._c()
+        k = model.modules_per_layer
+        tabs = []
+
+        def arr(v):
+            if v is None:
+                return None
+            a = (C.c_double * k)(*v)
+            tabs.append(a)
+            return C.cast(a, C.POINTER(C.c_double))
+
+        sc = N.SimConfig(SimConfig.TIERS.index(sim.overlap_tier), int(sim.recompute),
+                         sim.comm_streams, 1 if sim.fwd_times is not None else 0,
+                         sim.peak_flops_per_gpu, sim.compute_efficiency, arr(sim.fwd_times),
+                         arr(sim.bwd_grad_weight_times), arr(sim.bwd_grad_input_times),
+                         sim.head_fwd_time, sim.head_bwd_time)
+        cfg = N.SchedConfig(m, cost._c(), sc, comm_ctas, compute_ctas, time_scale,
+                            int(optimizer_overlap))
+        self.engine = engine
+        self._h = C.c_void_p()
+        N.check(N.lib().amsp_sched_create(engine._h, C.byref(cfg), profile._h, C.byref(self._h)))
+        self.info = N.SchedInfo()
+        N.check(N.lib().amsp_sched_info(self._h, C.byref(self.info)))
+
+    def step(self, step: int, stream=None, with_comm: bool = True) -> None:
+        N.check(N.lib().amsp_sched_step(self._h, step, _stream_ptr(stream), int(with_comm)))
+
+    def close(self) -> None:
+        if self._h:
+            N.lib().amsp_sched_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def b200_profile(world_max: int = 8):
+    """Synthetic alpha-beta profile at the measured B200 NVLink rates
+    (680 GB/s per direction for a plain P2P copy, 5 us latency) for every
+    single-node mesh up to world_max GPUs — the planner's input when no
+    measured CSV is supplied."""
+    from .shardplan import BandwidthProfile
+    meshes = [DeviceMesh(a, b) for a in range(1, world_max + 1) for b in (1, 2, 4, 8)]
+    return BandwidthProfile.synthetic((5e-6, 680e9), (10e-6, 50e9), meshes,
+                                      [1 << k for k in range(10, 36)])
+
+
 def exchange_handles(handle: bytes, world: int, group=None) -> list:
     """All-gather every rank's 64-byte cudaIpc handle, in rank order."""
     import torch.distributed as dist

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--dp-mesh", default=None)
     ap.add_argument("--layout", default="greedy")
     ap.add_argument("--p-mesh", default=None)
+    ap.add_argument("--sched", action="store_true")
     ap.add_argument("--model", default="tiny")
     ap.add_argument("--steps", type=int, default=4)
     args = ap.parse_args()
@@ -41,12 +42,27 @@ def main():
     p_mesh = mesh(args.p_mesh) if args.p_mesh else M(1, 1)
     g_mesh = p_mesh if p_mesh == os_mesh or args.p_mesh else M(1, 1)
     plan = S.ShardingPlan(p_mesh, g_mesh, os_mesh)
-    e = Engine(S.model(args.model), plan, dp, rank=rank, device=local, layout=args.layout)
+    e = Engine(S.model(args.model), plan, dp, rank=rank, device=local, layout=args.layout,
+               skip_gathers=args.sched)
     e.connect()
     e.init_state()
+    sched = None
+    if args.sched:  # overlap scheduler: real cross-GPU barriers per bucket / module
+        from paper_2311_00257_b200.engine import Scheduler, b200_profile
+        sched = Scheduler(e, S.model(args.model), b200_profile(),
+                          S.CostConfig(bucket_size=1 << 20),
+                          S.SimConfig(overlap_tier="ag_rs_ar_bc", peak_flops_per_gpu=1e16))
     for t in range(1, args.steps + 1):
         e.synth_grads(t)
-        e.step(t)
+        if sched:
+            dist.barrier()  # every rank's grads of step t exist before pulls
+            sched.step(t)
+            torch.cuda.synchronize()
+            dist.barrier()
+        else:
+            e.step(t)
+    if sched:
+        sched.close()
     torch.cuda.synchronize()
     phi = e.info.total_params
     segs, owned = e.segments()

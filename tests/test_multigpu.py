@@ -21,11 +21,16 @@ CASES = [(2, "2x1", None, "greedy", None), (2, "2x1", None, "contiguous", None),
          (4, "4x1", None, "greedy", None), (4, "2x1", None, "greedy", None),
          (4, "2x2", "2x2", "greedy", None), (4, "4x1", None, "contiguous", None),
          (4, "4x1", None, "greedy", "4x1"),                      # ZeRO-3
-         (4, "4x1", None, "greedy", "2x1")]                      # AMSP-13B-style
+         (4, "4x1", None, "greedy", "2x1"),                      # AMSP-13B-style
+         (2, "2x1", None, "greedy", "sched"), (4, "4x1", None, "greedy", "sched"),
+         (4, "4x1", None, "greedy", "4x1+sched"), (4, "2x1", None, "greedy", "sched")]
 
 
 @pytest.mark.parametrize("world,os_mesh,dp_mesh,layout,p_mesh", CASES)
 def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh):
+    sched = p_mesh is not None and "sched" in p_mesh
+    if sched:
+        p_mesh = p_mesh.split("+")[0] if "+" in p_mesh else None
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
@@ -35,6 +40,8 @@ def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh):
         cmd += ["--dp-mesh", dp_mesh]
     if p_mesh:
         cmd += ["--p-mesh", p_mesh]
+    if sched:
+        cmd += ["--sched"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=REPO,
                        env={**os.environ, "OMP_NUM_THREADS": "4"})
     out = r.stdout + r.stderr
