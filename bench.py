@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--layout", default="greedy", choices=["greedy", "contiguous"])
     ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (0 auto)")
     ap.add_argument("--grid", type=int, default=0, help="fused-kernel grid (0 auto)")
-    ap.add_argument("--overlap", action="store_true",
+    ap.add_argument("--overlap", action=argparse.BooleanOptionalAction, default=True,
                     help="also time the overlapped step (scheduler + compute stand-ins)")
     ap.add_argument("--tier", default="ag_rs_ar_bc", help="overlap tier for --overlap")
     ap.add_argument("--seq-len", type=int, default=4096)
