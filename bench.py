@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference", "library"])
     ap.add_argument("--model", default="llama-7b")
     ap.add_argument("--plan", default="zero1",
                     help="zero1 (P/G replica, OS over dp) | replica | 'p=AxB,g=AxB,os=AxB'")
@@ -262,6 +262,80 @@ def run_reference(args):
         "cpu_baseline_detail": cpu,
     }
     print(json.dumps(line), flush=True)
+
+
+def run_library(args):
+    """Library baseline of the same step (not the product): torch's fused
+    AdamW (torch.optim.AdamW(fused=True)) on the fp32 master shard after an
+    upcast, with NCCL reduce-scatter (fp32, the precision the oracle needs)
+    and all-gather of bf16 params for W > 1 — what a ZeRO-1 framework on
+    stock PyTorch + NCCL does. Prints one JSON line (impl library-baseline)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_00257_b200 import _native as N
+    from paper_2311_00257_b200 import shardplan as S
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    phi = S.model(args.model).total_params
+    shard = -(-phi // world)
+    padded = shard * world
+    grads = torch.empty(padded, dtype=torch.bfloat16, device=dev)
+    N.check(N.lib().amsp_k_synth_grad(grads.data_ptr(), 0, phi, 0x414D5350, 1, rank, None))
+    grads[phi:].zero_()
+    params = torch.zeros(padded, dtype=torch.bfloat16, device=dev)
+    master = torch.nn.Parameter(torch.full((shard,), 0.01, dtype=torch.float32, device=dev))
+    opt = torch.optim.AdamW([master], lr=1e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1,
+                            fused=True)
+    g32_full = torch.empty(padded, dtype=torch.float32, device=dev) if world > 1 else None
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if world > 1:
+            g32_full.copy_(grads)                      # bf16 -> fp32 upcast
+            g = torch.empty(shard, dtype=torch.float32, device=dev)
+            dist.reduce_scatter_tensor(g, g32_full, op=dist.ReduceOp.SUM)
+            g.mul_(1.0 / world)
+            master.grad = g
+        else:
+            master.grad = grads[:shard].float()
+        opt.step()
+        mine = params[rank * shard:(rank + 1) * shard]
+        mine.copy_(master.detach())                    # fp32 -> bf16 downcast
+        if world > 1:
+            dist.all_gather_into_tensor(params, mine.clone())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.steps):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms)
+    if rank == 0:
+        print(json.dumps({
+            "impl": "library-baseline", "metric": METRIC, "value": phi / (ms * 1e-3),
+            "unit": "params/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+            "config": {"workload": f"{args.model} model states, ZeRO-1 over {world}",
+                       "path": "upcast + NCCL reduce_scatter(fp32) + torch fused AdamW + "
+                               "downcast + NCCL all_gather(bf16)" if world > 1 else
+                               "upcast + torch fused AdamW + downcast"}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def run_ours(args):
@@ -501,7 +575,9 @@ def run_ours(args):
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.impl == "library":
+        run_library(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
