@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--micro-batch", type=int, default=1)
     ap.add_argument("--compute-eff", type=float, default=0.6)
     ap.add_argument("--comm-ctas", type=int, default=0)
+    ap.add_argument("--trace-dir", default=None,
+                    help="write measured + predicted TEF traces of one overlapped step here")
+    ap.add_argument("--compute", default="standin", choices=["standin", "gemm"],
+                    help="overlapped step compute: timed stand-ins or real cuBLAS GEMMs")
     ap.add_argument("--optimizer-overlap", type=int, default=1,
                     help="1: AdamW+push per bucket/module inside backward; 0: after the barrier")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -481,7 +485,8 @@ def run_ours(args):
                           compute_efficiency=args.compute_eff)
         sched = Scheduler(eng, mspec, b200_profile(), S.CostConfig(), sim,
                           comm_ctas=args.comm_ctas,
-                          optimizer_overlap=bool(args.optimizer_overlap))
+                          optimizer_overlap=bool(args.optimizer_overlap),
+                          compute=args.compute)
 
         def timed(with_comm, k):
             nonlocal step
@@ -501,6 +506,21 @@ def run_ours(args):
         t_b = timed(True, args.steps)
         t_c = timed(False, args.steps)
         si = sched.info
+        if args.trace_dir and rank == 0:
+            # One extra traced step (outside the timed region): measured and
+            # predicted Chrome traces with the reference's schema.
+            sched.enable_trace(True)
+            step += 1
+            sched.step(step, stream, True)
+            text, _ = sched.trace()
+            Path(args.trace_dir).mkdir(parents=True, exist_ok=True)
+            tag = f"{args.model}_w{world}_{str(plan).replace(',', '_').replace('=', '')}"
+            (Path(args.trace_dir) / f"measured_{tag}.json").write_text(text)
+            (Path(args.trace_dir) / f"predicted_{tag}.json").write_text(sched.predicted_trace())
+        elif args.trace_dir:
+            sched.enable_trace(True)
+            step += 1
+            sched.step(step, stream, True)
         overlap = {"tier": args.tier, "tokens_per_microbatch": args.micro_batch * args.seq_len,
                    "optimizer": "in backward (per bucket/module)" if args.optimizer_overlap
                                 else "after the step barrier (paper)",
@@ -511,7 +531,11 @@ def run_ours(args):
                    "predicted_compute_ms": round(si.predicted_compute_s * 1e3, 3),
                    "events": si.n_events, "buckets": si.n_buckets, "gathers": si.n_gather,
                    "reduces": si.n_reduce, "barriers": si.n_barriers,
-                   "compute_model": f"6*Phi*B*S at {peak_tf} TF/s x {args.compute_eff}",
+                   "compute_model": (f"timed stand-ins: 6*Phi*B*S at {peak_tf} TF/s x "
+                                     f"{args.compute_eff}" if args.compute == "standin" else
+                                     "cuBLAS bf16 GEMMs of every linear module (fwd, dgrad, "
+                                     "wgrad into the gradient buffer), norms as stand-ins, "
+                                     "no attention"),
                    "profile": "synthetic B200 NVLink alpha-beta (680 GB/s, 5 us)"}
         sched.close()
 

@@ -333,6 +333,12 @@ typedef struct {
   int optimizer_overlap;        /* 0: AdamW + push after the step barrier
                                    (the paper's placement); 1: per module /
                                    bucket inside backward (see sched.cpp) */
+  int compute_mode;             /* 0: timed stand-ins of the graph's
+                                   durations; 1: cuBLAS bf16 GEMMs of each
+                                   linear module's true shape (fwd / dgrad /
+                                   wgrad into the real gradient buffer),
+                                   reading the gathered weights */
+  int tokens;                   /* GEMM rows T (0 = micro_batch * seq_len) */
 } amsp_sched_config_t;
 
 typedef struct {
@@ -347,6 +353,14 @@ int amsp_sched_info(const amsp_sched_t* s, amsp_sched_info_t* info);
 /* One step; with_comm = 0 runs the compute stand-ins only (the exposed-
  * communication baseline). stream = the compute stream (NULL: engine's). */
 int amsp_sched_step(amsp_sched_t* s, int step, void* stream, int with_comm);
+/* Measured trace: with tracing on, every graph event of a step
+ * is bracketed by CUDA events; amsp_sched_trace renders the last traced step
+ * with the reference's render_trace (overlap_sim.cpp:560-577), so measured
+ * and predicted (amsp_sched_predicted_trace) traces share one TEF schema
+ * and event names. *step_ms = measured span of the graph. */
+int amsp_sched_enable_trace(amsp_sched_t* s, int on);
+int amsp_sched_trace(amsp_sched_t* s, char* buf, size_t cap, size_t* needed, double* step_ms);
+int amsp_sched_predicted_trace(const amsp_sched_t* s, char* buf, size_t cap, size_t* needed);
 void amsp_sched_destroy(amsp_sched_t* s);
 
 /* ------------------------------------------------------------ kernels */

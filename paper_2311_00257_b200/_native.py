@@ -117,7 +117,7 @@ class EngineInfo(C.Structure):
 class SchedConfig(C.Structure):
     _fields_ = [("model", Model), ("cost", CostConfig), ("sim", SimConfig),
                 ("comm_ctas", C.c_int), ("compute_ctas", C.c_int), ("time_scale", C.c_double),
-                ("optimizer_overlap", C.c_int)]
+                ("optimizer_overlap", C.c_int), ("compute_mode", C.c_int), ("tokens", C.c_int)]
 
 
 class SchedInfo(C.Structure):
@@ -193,6 +193,9 @@ SIGNATURES = {
     "amsp_sched_create": (C.c_int, [vp, P(SchedConfig), vp, P(vp)]),
     "amsp_sched_info": (C.c_int, [vp, P(SchedInfo)]),
     "amsp_sched_step": (C.c_int, [vp, C.c_int, vp, C.c_int]),
+    "amsp_sched_enable_trace": (C.c_int, [vp, C.c_int]),
+    "amsp_sched_trace": (C.c_int, [vp, C.c_char_p, C.c_size_t, P(C.c_size_t), P(C.c_double)]),
+    "amsp_sched_predicted_trace": (C.c_int, [vp, C.c_char_p, C.c_size_t, P(C.c_size_t)]),
     "amsp_sched_destroy": (None, [vp]),
     "amsp_k_synth_grad": (C.c_int, [vp, u64, u64, u64, C.c_int, C.c_int, vp]),
     "amsp_k_adamw": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, u64, C.c_int, C.c_double,

@@ -31,6 +31,7 @@
 //       bucket after a second barrier that certifies every rank finished the
 //       bucket's grad-input (the last reader of those replicated params).
 // Either way the arithmetic is bit-equal to the fused kernel and the oracle.
+#include "blas.h"
 #include "engine_impl.h"
 #include "../convert.h"
 
@@ -38,10 +39,16 @@ namespace {
 
 enum class Work { Compute, Gather, Reduce, ReduceAdam, Marker };
 
+// Real-compute mode: a compute event of a linear module (or the LM head) is
+// a cuBLAS bf16 GEMM of its true shape over T tokens.
+enum class Gemm { None, Fwd, DGrad, WGrad };
+
 struct EventWork {
   Work kind = Work::Marker;
   int stream = 0;
   int tensor = -1;
+  Gemm gemm = Gemm::None;
+  int g_in = 0, g_out = 0;
   int barrier = -1;
   int seg_begin = 0, nseg = 0, ntiles = 0;
   unsigned long long ns = 0;
@@ -51,6 +58,9 @@ struct EventWork {
   bool adam_after = false;
   int after_event = -1;
   int barrier2 = -1;
+  // Single rank (no AllReduce buckets in the graph): fused update of the
+  // bucket completed by this grad-input event, on the AR/BC stream.
+  int post_begin = 0, post_nseg = 0, post_ntiles = 0;
 };
 
 struct Table {
@@ -75,17 +85,117 @@ struct amsp_sched {
   amsp::Seg* d_rsegs = nullptr;
   amsp::CopySeg* d_tcopy = nullptr;
   float* red = nullptr;
+  // Real-compute mode buffers: activations / output-grads / outputs of
+  // T x max-dim bf16, a 3-layer ring of gathered module weights (s_p > 1)
+  // and a head-weight scratch (the head is never gathered by the graph).
+  bool gemm_mode = false;
+  int tokens = 0, layers_k = 1;
+  uint16_t* act = nullptr;
+  uint16_t* dout = nullptr;
+  uint16_t* yout = nullptr;
+  uint16_t* ring = nullptr;
+  uint16_t* head_w = nullptr;
+  std::uint64_t ring_slot = 0;
+
+  uint16_t* gather_dst(int t) const {
+    if (!gemm_mode) return e->slots[t & 1];
+    const int l = (t - 1) / layers_k, i = (t - 1) % layers_k;
+    return ring + static_cast<std::uint64_t>((l % 3) * layers_k + i) * ring_slot;
+  }
+
+  const uint16_t* weight_of(int t) const {
+    if (t < 0) return head_w ? head_w : e->params_of(e->rank) + e->pmap.tensor_offset.back();
+    if (e->sp > 1) return gather_dst(t);
+    return e->params_of(e->rank) + e->pmap.tensor_offset[t];
+  }
+
+  void compute(const EventWork& w, cudaStream_t st) {
+    if (w.gemm == Gemm::None) {
+      ck(amsp::launch_spin(compute_ctas, w.ns, st), "compute stand-in");
+      ++e->launches;
+      return;
+    }
+    amsp::Blas& blas = amsp::Blas::instance();
+    const int t = w.tensor;  // -1: LM head
+    const uint16_t* wt = weight_of(t);
+    switch (w.gemm) {
+      case Gemm::Fwd:
+        blas.linear_fwd(st, act, wt, yout, tokens, w.g_in, w.g_out);
+        break;
+      case Gemm::DGrad:
+        blas.linear_dgrad(st, dout, wt, yout, tokens, w.g_in, w.g_out);
+        break;
+      case Gemm::WGrad: {
+        const std::size_t ti = t < 0 ? e->tensor_sizes.size() - 1 : static_cast<std::size_t>(t);
+        blas.linear_wgrad(st, dout, act, e->grads_of(e->rank) + e->pmap.tensor_offset[ti],
+                          tokens, w.g_in, w.g_out);
+        break;
+      }
+      case Gemm::None:
+        break;
+    }
+    ++e->launches;
+  }
   cudaStream_t comm[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> events;
   cudaEvent_t start_ev = nullptr, join_ev[2] = {nullptr, nullptr};
   uint32_t epoch = 0;
   amsp::AdamScalars scalars{};
+  // Measured trace: timing events around every graph event of the last step.
+  bool tracing = false;
+  cudaEvent_t trace_origin = nullptr;
+  std::vector<cudaEvent_t> t_begin, t_end;
+
+  void enable_trace(bool on) {
+    tracing = on;
+    if (!on || !t_begin.empty()) return;
+    ck(cudaEventCreate(&trace_origin), "event");
+    t_begin.resize(graph.events.size());
+    t_end.resize(graph.events.size());
+    for (auto& ev : t_begin) ck(cudaEventCreate(&ev), "event");
+    for (auto& ev : t_end) ck(cudaEventCreate(&ev), "event");
+  }
+
+  // The last traced step as a shardplan::Timeline, rendered by the same
+  // render_trace as the simulator (identical TEF schema and names).
+  std::string measured_trace(double* step_ms) {
+    if (t_begin.empty()) throw Error("sched: tracing was never enabled");
+    shardplan::Timeline tl;
+    tl.events = graph.events;
+    tl.streams.resize(graph.stream_count);
+    for (std::size_t i = 0; i < graph.events.size(); ++i) {
+      ck(cudaEventSynchronize(t_end[i]), "event sync");
+      float a = 0.0f, b = 0.0f;
+      ck(cudaEventElapsedTime(&a, trace_origin, t_begin[i]), "event elapsed");
+      ck(cudaEventElapsedTime(&b, trace_origin, t_end[i]), "event elapsed");
+      tl.streams[graph.events[i].stream].push_back(
+          {static_cast<int>(i), a * 1e-3, std::max(a, b) * 1e-3});
+    }
+    tl.busy.assign(graph.stream_count, 0.0);
+    for (int k = 0; k < graph.stream_count; ++k) {
+      auto& v = tl.streams[k];
+      std::stable_sort(v.begin(), v.end(), [](const shardplan::ScheduledEvent& x,
+                                              const shardplan::ScheduledEvent& y) {
+        return x.start < y.start;
+      });
+      for (const auto& se : v) {
+        tl.busy[k] += se.end - se.start;
+        tl.step_time = std::max(tl.step_time, se.end);
+      }
+    }
+    tl.idle.resize(graph.stream_count);
+    for (int k = 0; k < graph.stream_count; ++k) tl.idle[k] = tl.step_time - tl.busy[k];
+    if (step_ms) *step_ms = tl.step_time * 1e3;
+    return shardplan::render_trace(tl);
+  }
 
   ~amsp_sched() {
     if (e) cudaSetDevice(e->cfg.device);
     cudaDeviceSynchronize();
-    for (auto ev : events)
-      if (ev) cudaEventDestroy(ev);
+    for (auto* v : {&events, &t_begin, &t_end})
+      for (auto ev : *v)
+        if (ev) cudaEventDestroy(ev);
+    if (trace_origin) cudaEventDestroy(trace_origin);
     if (start_ev) cudaEventDestroy(start_ev);
     for (auto ev : join_ev)
       if (ev) cudaEventDestroy(ev);
@@ -94,6 +204,9 @@ struct amsp_sched {
     cudaFree(d_rsegs);
     cudaFree(d_tcopy);
     cudaFree(red);
+    for (void* p : {static_cast<void*>(act), static_cast<void*>(dout), static_cast<void*>(yout),
+                    static_cast<void*>(ring), static_cast<void*>(head_w)})
+      cudaFree(p);
     cudaGetLastError();  // teardown must not leave a sticky error for the next call
   }
 
@@ -167,7 +280,7 @@ struct amsp_sched {
     g.sp = e->sp;
     g.rot = (e->p_group.position + 1) % e->sp;
     for (int q = 0; q < e->sp; ++q) g.src[q] = e->params_of(e->p_group.members[q]);
-    g.dst = e->slots[t & 1];
+    g.dst = gather_dst(t);
     g.grid = comm_ctas;
     ck(amsp::launch_gather(g, s), "sched gather");
     ++e->launches;
@@ -180,6 +293,7 @@ struct amsp_sched {
     scalars = amsp::make_adam_scalars(e->cfg.lr, e->cfg.beta1, e->cfg.beta2, e->cfg.eps,
                                       e->cfg.weight_decay, step, 1.0 / e->world);
     ck(cudaEventRecord(start_ev, main), "event record");
+    if (tracing) ck(cudaEventRecord(trace_origin, main), "event record");
     for (auto s : comm) ck(cudaStreamWaitEvent(s, start_ev, 0), "stream wait");
     const auto& evs = graph.events;
     for (std::size_t i = 0; i < evs.size(); ++i) {
@@ -188,11 +302,11 @@ struct amsp_sched {
       for (int d : evs[i].depends_on)
         if (work[d].stream != w.stream && work[d].record)
           ck(cudaStreamWaitEvent(st, events[d], 0), "stream wait");
+      if (tracing) ck(cudaEventRecord(t_begin[i], st), "event record");
       const Table t{w.seg_begin, w.nseg, w.ntiles};
       switch (w.kind) {
         case Work::Compute:
-          ck(amsp::launch_spin(compute_ctas, w.ns, st), "compute stand-in");
-          ++e->launches;
+          compute(w, st);
           break;
         case Work::Gather:
           if (with_comm) gather_tensor(w.tensor, st);
@@ -217,7 +331,12 @@ struct amsp_sched {
         case Work::Marker:
           break;
       }
+      if (tracing) ck(cudaEventRecord(t_end[i], st), "event record");
       if (w.record) ck(cudaEventRecord(events[i], st), "event record");
+      if (with_comm && w.post_ntiles > 0) {
+        ck(cudaStreamWaitEvent(comm[1], events[i], 0), "stream wait");
+        fused(Table{w.post_begin, w.post_nseg, w.post_ntiles}, comm_ctas, comm[1]);
+      }
     }
     for (int k = 0; k < 2; ++k) {
       ck(cudaEventRecord(join_ev[k], comm[k]), "event record");
@@ -352,6 +471,9 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     }
   }
 
+  s->gemm_mode = cfg->compute_mode == 1;
+  s->layers_k = K;
+  std::uint64_t max_out = 0;
   std::vector<amsp::Seg> rsegs;
   std::vector<char> covered(n, 0);  // reduced by some event
   std::vector<char> updated(n, 0);  // optimizer already applied by some event
@@ -366,11 +488,25 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
       case shardplan::EventKind::FwdCompute:
       case shardplan::EventKind::BwdGradInput:
       case shardplan::EventKind::BwdGradWeight:
-      case shardplan::EventKind::RecomputeFwd:
+      case shardplan::EventKind::RecomputeFwd: {
         w.kind = Work::Compute;
         w.ns = static_cast<unsigned long long>(ev.duration * cfg->time_scale * 1e9);
         ++s->n_compute;
+        if (!s->gemm_mode) break;
+        const int t = ev.layer < 0 ? -1 : tensor_of(ev.layer, ev.module);
+        const std::uint64_t size = e->tensor_sizes[t < 0 ? n - 1 : static_cast<std::size_t>(t)];
+        const std::uint64_t H = static_cast<std::uint64_t>(model.hidden);
+        if (size > H && size % H == 0) {  // linear module (norms stay timed stand-ins)
+          w.tensor = t;
+          w.g_in = model.hidden;
+          w.g_out = static_cast<int>(size / H);
+          w.gemm = ev.kind == shardplan::EventKind::BwdGradInput    ? Gemm::DGrad
+                   : ev.kind == shardplan::EventKind::BwdGradWeight ? Gemm::WGrad
+                                                                    : Gemm::Fwd;
+          max_out = std::max<std::uint64_t>(max_out, size / H);
+        }
         break;
+      }
       case shardplan::EventKind::AllGather:
         w.kind = Work::Gather;
         w.tensor = tensor_of(ev.layer, ev.module);
@@ -441,6 +577,34 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
       std::fill(updated.begin(), updated.end(), 1);
     }
   }
+  // A single rank has nothing to reduce: with optimizer overlap its fused
+  // update runs bucket by bucket behind the backward pass (the graph's own
+  // bucket cuts), each after the grad-input that last reads those params.
+  if (plan.sp() == 1 && ar_seen == 0 && s->optimizer_overlap && e->world == 1) {
+    for (std::size_t b = 0; b < buckets.size(); ++b) {
+      int last = -1;
+      for (int tt : bucket_tensors[b]) last = std::max(last, gi_event[tt]);
+      if (last < 0) continue;
+      EventWork& w = s->work[last];
+      if (w.post_ntiles > 0) {
+        // Several buckets closed by one event: extend its table.
+        const Table t = owned_pieces(e->layout, buckets[b], rsegs);
+        if (t.begin != w.post_begin + w.post_nseg)
+          throw Error("sched: non-contiguous post tables");
+        for (int q = t.begin; q < t.begin + t.nseg; ++q)
+          rsegs[q].tile0 += static_cast<unsigned long long>(w.post_ntiles);
+        w.post_nseg += t.nseg;
+        w.post_ntiles += t.ntiles;
+      } else {
+        const Table t = owned_pieces(e->layout, buckets[b], rsegs);
+        w.post_begin = t.begin;
+        w.post_nseg = t.nseg;
+        w.post_ntiles = t.ntiles;
+      }
+      w.record = true;
+      for (int tt : bucket_tensors[b]) covered[tt] = updated[tt] = 1;
+    }
+  }
   // After the graph: tensors nobody reduced get the fused update; reduced but
   // not yet updated ones get AdamW from the fp32 reduced gradients.
   std::vector<FlatRange> rest, pend;
@@ -487,6 +651,32 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
   ck(cudaEventCreateWithFlags(&s->start_ev, cudaEventDisableTiming), "event");
   for (auto& ev : s->join_ev) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
   for (auto& st : s->comm) ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  if (s->gemm_mode) {
+    amsp::Blas::instance();  // fail now, not mid-step, when cuBLAS is missing
+    s->tokens = cfg->tokens > 0 ? cfg->tokens : model.micro_batch * model.seq_len;
+    const std::uint64_t T = static_cast<std::uint64_t>(s->tokens);
+    const std::uint64_t H = static_cast<std::uint64_t>(model.hidden);
+    const std::uint64_t wide = std::max(max_out, H);
+    auto alloc = [](uint16_t** p, std::uint64_t elems, const char* what) {
+      ck(cudaMalloc(p, std::max<std::uint64_t>(elems, 8) * 2), what);
+    };
+    alloc(&s->act, T * H, "cudaMalloc activations");
+    alloc(&s->dout, T * wide, "cudaMalloc output grads");
+    alloc(&s->yout, T * wide, "cudaMalloc outputs");
+    // Small, finite synthetic activations (counter-based, like the grads).
+    ck(amsp::launch_synth_grad(s->act, 0, T * H, 0x5EED, 1, 0, nullptr), "fill activations");
+    ck(amsp::launch_synth_grad(s->dout, 0, T * wide, 0x5EED, 2, 0, nullptr), "fill out-grads");
+    if (e->sp > 1) {
+      std::uint64_t biggest = 0;
+      for (int i = 0; i < K; ++i) biggest = std::max(biggest, model.module_params[i]);
+      s->ring_slot = (biggest + 7) / 8 * 8;
+      alloc(&s->ring, s->ring_slot * 3 * K, "cudaMalloc gathered-weight ring");
+      alloc(&s->head_w, e->tensor_sizes[n - 1], "cudaMalloc head weight");
+      ck(amsp::launch_synth_grad(s->head_w, 0, e->tensor_sizes[n - 1], 0x5EED, 3, 0, nullptr),
+         "fill head weight");
+    }
+    ck(cudaDeviceSynchronize(), "gemm buffers");
+  }
   s->comm_ctas = cfg->comm_ctas > 0 ? cfg->comm_ctas : 128;
   s->compute_ctas = cfg->compute_ctas > 0 ? cfg->compute_ctas : e->sms;
   s->time_scale = cfg->time_scale > 0 ? cfg->time_scale : 1.0;
@@ -529,6 +719,41 @@ int amsp_sched_step(amsp_sched_t* s, int step, void* stream, int with_comm) {
     if (!s) throw Error("sched: null argument");
     s->e->use_device();
     s->run(step, s->e->pick(stream), with_comm != 0);
+  });
+}
+
+int amsp_sched_enable_trace(amsp_sched_t* s, int on) {
+  return amsp::guarded([&] {
+    if (!s) throw Error("sched: null argument");
+    s->e->use_device();
+    s->enable_trace(on != 0);
+  });
+}
+
+int amsp_sched_trace(amsp_sched_t* s, char* buf, size_t cap, size_t* needed, double* step_ms) {
+  return amsp::guarded([&] {
+    if (!s) throw Error("sched: null argument");
+    s->e->use_device();
+    const std::string text = s->measured_trace(step_ms);
+    if (needed) *needed = text.size();
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, text.size());
+      std::memcpy(buf, text.data(), n);
+      buf[n] = '\0';
+    }
+  });
+}
+
+int amsp_sched_predicted_trace(const amsp_sched_t* s, char* buf, size_t cap, size_t* needed) {
+  return amsp::guarded([&] {
+    if (!s) throw Error("sched: null argument");
+    const std::string text = shardplan::render_trace(shardplan::simulate_step(s->graph));
+    if (needed) *needed = text.size();
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, text.size());
+      std::memcpy(buf, text.data(), n);
+      buf[n] = '\0';
+    }
   });
 }
 

@@ -184,7 +184,7 @@ class Scheduler:
 
     def __init__(self, engine: Engine, model: ModelSpec, profile, cost=None, sim=None,
                  comm_ctas: int = 0, compute_ctas: int = 0, time_scale: float = 1.0,
-                 optimizer_overlap: bool = True):
+                 optimizer_overlap: bool = True, compute: str = "standin", tokens: int = 0):
         from .shardplan import CostConfig, SimConfig
         cost = cost or CostConfig()
         sim = sim or SimConfig()
@@ -205,7 +205,7 @@ class Scheduler:
                          arr(sim.bwd_grad_weight_times), arr(sim.bwd_grad_input_times),
                          sim.head_fwd_time, sim.head_bwd_time)
         cfg = N.SchedConfig(m, cost._c(), sc, comm_ctas, compute_ctas, time_scale,
-                            int(optimizer_overlap))
+                            int(optimizer_overlap), {"standin": 0, "gemm": 1}[compute], tokens)
         self.engine = engine
         self._h = C.c_void_p()
         N.check(N.lib().amsp_sched_create(engine._h, C.byref(cfg), profile._h, C.byref(self._h)))
@@ -214,6 +214,24 @@ class Scheduler:
 
     def step(self, step: int, stream=None, with_comm: bool = True) -> None:
         N.check(N.lib().amsp_sched_step(self._h, step, _stream_ptr(stream), int(with_comm)))
+
+    def enable_trace(self, on: bool = True) -> None:
+        N.check(N.lib().amsp_sched_enable_trace(self._h, int(on)))
+
+    def trace(self):
+        """(measured TEF JSON of the last traced step, its span in ms)."""
+        need, ms = C.c_size_t(), C.c_double()
+        N.check(N.lib().amsp_sched_trace(self._h, None, 0, C.byref(need), C.byref(ms)))
+        buf = C.create_string_buffer(need.value + 1)
+        N.check(N.lib().amsp_sched_trace(self._h, buf, need.value + 1, None, None))
+        return buf.value.decode(), ms.value
+
+    def predicted_trace(self) -> str:
+        need = C.c_size_t()
+        N.check(N.lib().amsp_sched_predicted_trace(self._h, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value + 1)
+        N.check(N.lib().amsp_sched_predicted_trace(self._h, buf, need.value + 1, None))
+        return buf.value.decode()
 
     def close(self) -> None:
         if self._h:

@@ -212,6 +212,52 @@ def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap):
     want = O.trajectory_range(0, engines[0].info.total_params, DEFAULT_SEED, steps, world, H)
     for e in engines:
         _check_rank(e, want, steps)
+    # measured trace: same TEF schema / event names as the simulator's
+    import json
+    scheds[0].enable_trace(True)
+    for e in engines:
+        e.synth_grads(steps + 1)
+    for sc in scheds:
+        sc.step(steps + 1)
+    measured, span_ms = scheds[0].trace()
+    predicted = json.loads(scheds[0].predicted_trace())
+    measured = json.loads(measured)
+    assert len(measured) == len(predicted) == info.n_events
+    assert sorted(x["name"] for x in measured) == sorted(x["name"] for x in predicted)
+    assert span_ms > 0
+    for sc in scheds:
+        sc.close()
+    for e in engines:
+        e.close()
+
+
+@pytest.mark.parametrize("world,p", [(1, 1), (2, 1), (2, 2)])
+def test_scheduler_real_gemm_compute(cuda, world, p):
+    """compute='gemm': linear modules run cuBLAS GEMMs of their true shapes,
+    grad-weight writes the real gradient buffer the reductions read. The
+    replicated / gathered parameters must stay finite and identical on every
+    rank that holds them."""
+    from paper_2311_00257_b200.engine import Scheduler, b200_profile
+    model = S.model("tiny", seq_len=256)
+    plan = S.ShardingPlan(M(p, 1), M(p, 1), M(world, 1))
+    engines = [Engine(model, plan, M(world, 1), rank=r) for r in range(world)]
+    if world > 1:
+        link_local(engines)
+    scheds = [Scheduler(e, model, b200_profile(), S.CostConfig(bucket_size=1 << 20),
+                        S.SimConfig(peak_flops_per_gpu=1e15), compute="gemm")
+              for e in engines]
+    for e in engines:
+        e.init_state()
+    for t in (1, 2):
+        for sc in scheds:
+            sc.step(t)
+    params = [e.read("params").view(np.int16).astype(np.uint16) for e in engines]
+    for prm in params:
+        f = (prm.astype(np.uint32) << 16).view(np.float32)
+        assert np.all(np.isfinite(f))
+    if p == 1:
+        for prm in params[1:]:
+            assert np.array_equal(prm, params[0])
     for sc in scheds:
         sc.close()
     for e in engines:
