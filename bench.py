@@ -61,10 +61,15 @@ def parse():
     ap.add_argument("--comm-ctas", type=int, default=0)
     ap.add_argument("--trace-dir", default=None,
                     help="write measured + predicted TEF traces of one overlapped step here")
-    ap.add_argument("--compute", default="standin", choices=["standin", "gemm"],
+    ap.add_argument("--compute", default="both", choices=["standin", "gemm", "both"],
                     help="overlapped step compute: timed stand-ins or real cuBLAS GEMMs")
-    ap.add_argument("--optimizer-overlap", type=int, default=1,
-                    help="1: AdamW+push per bucket/module inside backward; 0: after the barrier")
+    ap.add_argument("--gemm-sm-margin", type=int, default=0,
+                    help="SMs withheld from cuBLAS GEMMs for comm kernels (--compute gemm)")
+    ap.add_argument("--optimizer-overlap", type=int, default=-1,
+                    help="1: AdamW+push per bucket/module inside backward; 0: after the "
+                         "barrier; -1: auto")
+    ap.add_argument("--gather", default="dma", choices=["dma", "sm"],
+                    help="overlapped all-gathers on copy engines (dma) or an SM kernel")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -473,20 +478,28 @@ def run_ours(args):
                  "all_gather_equiv_gbs": round(2 * phi * (world - 1) / world / (kernel_ms * 1e-3) / 1e9, 1),
                  "vs_nvlink_gbs": NVLINK_NOMINAL_GBS}
 
-    # Overlapped step: the reference event graph replayed by the scheduler
-    # with compute stand-ins of 6*Phi*B*S FLOPs at the measured sustained
-    # bf16 peak x efficiency; exposed comm = t(with comm) - t(compute only).
-    overlap = None
-    if args.overlap:
+    # Overlapped step: the reference event graph replayed by the scheduler on
+    # 3 streams; measured with real cuBLAS GEMM compute (the realistic case)
+    # and with the reference's timed stand-ins (6*Phi*B*S FLOPs at the
+    # measured sustained bf16 peak x efficiency).
+    def measure_overlap(compute):
+        nonlocal step
         from paper_2311_00257_b200.engine import Scheduler, b200_profile
         mspec = S.model(args.model, micro_batch=args.micro_batch, seq_len=args.seq_len)
         peak_tf = pk.get("bf16_tflops_sustained", 1400.0)
         sim = S.SimConfig(overlap_tier=args.tier, peak_flops_per_gpu=peak_tf * 1e12,
                           compute_efficiency=args.compute_eff)
-        sched = Scheduler(eng, mspec, b200_profile(), S.CostConfig(), sim,
-                          comm_ctas=args.comm_ctas,
-                          optimizer_overlap=bool(args.optimizer_overlap),
-                          compute=args.compute)
+        # Defaults from the r01 sweeps (profiles/r01_tune_overlap_*.jsonl):
+        # with real GEMMs the HBM-bound optimizer competes with compute for
+        # SMs, so it stays after the barrier unless P is sharded; all-gathers
+        # run on the copy engines (no SMs taken from compute).
+        opt = args.optimizer_overlap
+        if opt < 0:
+            opt = 1 if (compute == "standin" or plan.sp() > 1) else 0
+        ctas = args.comm_ctas or (64 if (compute == "gemm" and plan.sp() > 1) else 128)
+        sched = Scheduler(eng, mspec, b200_profile(), S.CostConfig(), sim, comm_ctas=ctas,
+                          optimizer_overlap=bool(opt), compute=compute,
+                          gemm_sm_margin=args.gemm_sm_margin, gather=args.gather)
 
         def timed(with_comm, k):
             nonlocal step
@@ -505,39 +518,55 @@ def run_ours(args):
         timed(True, args.warmup)
         t_b = timed(True, args.steps)
         t_c = timed(False, args.steps)
+        t_o = timed("optimizer", args.steps)
         si = sched.info
-        if args.trace_dir and rank == 0:
-            # One extra traced step (outside the timed region): measured and
+        if args.trace_dir:
+            # One extra traced step (outside the timed regions): measured and
             # predicted Chrome traces with the reference's schema.
             sched.enable_trace(True)
             step += 1
             sched.step(step, stream, True)
-            text, _ = sched.trace()
-            Path(args.trace_dir).mkdir(parents=True, exist_ok=True)
-            tag = f"{args.model}_w{world}_{str(plan).replace(',', '_').replace('=', '')}"
-            (Path(args.trace_dir) / f"measured_{tag}.json").write_text(text)
-            (Path(args.trace_dir) / f"predicted_{tag}.json").write_text(sched.predicted_trace())
-        elif args.trace_dir:
-            sched.enable_trace(True)
-            step += 1
-            sched.step(step, stream, True)
-        overlap = {"tier": args.tier, "tokens_per_microbatch": args.micro_batch * args.seq_len,
-                   "optimizer": "in backward (per bucket/module)" if args.optimizer_overlap
-                                else "after the step barrier (paper)",
-                   "step_ms": round(t_b, 3), "compute_only_ms": round(t_c, 3),
-                   "exposed_comm_ms": round(t_b - t_c, 3),
-                   "exposed_frac": round((t_b - t_c) / t_b, 4),
-                   "predicted_step_ms": round(si.predicted_step_s * 1e3, 3),
-                   "predicted_compute_ms": round(si.predicted_compute_s * 1e3, 3),
-                   "events": si.n_events, "buckets": si.n_buckets, "gathers": si.n_gather,
-                   "reduces": si.n_reduce, "barriers": si.n_barriers,
-                   "compute_model": (f"timed stand-ins: 6*Phi*B*S at {peak_tf} TF/s x "
-                                     f"{args.compute_eff}" if args.compute == "standin" else
-                                     "cuBLAS bf16 GEMMs of every linear module (fwd, dgrad, "
-                                     "wgrad into the gradient buffer), norms as stand-ins, "
-                                     "no attention"),
-                   "profile": "synthetic B200 NVLink alpha-beta (680 GB/s, 5 us)"}
+            if rank == 0:
+                text, _ = sched.trace()
+                Path(args.trace_dir).mkdir(parents=True, exist_ok=True)
+                tag = (f"{args.model}_w{world}_{str(plan).replace(',', '_').replace('=', '')}"
+                       f"_{compute}")
+                (Path(args.trace_dir) / f"measured_{tag}.json").write_text(text)
+                (Path(args.trace_dir) / f"predicted_{tag}.json").write_text(
+                    sched.predicted_trace())
         sched.close()
+        return {"compute": compute, "tier": args.tier,
+                "tokens_per_microbatch": args.micro_batch * args.seq_len,
+                "optimizer": "in backward (per bucket/module)" if opt
+                             else "after the step barrier (paper)",
+                "gather": "copy engines" if args.gather == "dma" else "SM kernel",
+                "comm_ctas": ctas,
+                "step_ms": round(t_b, 3), "compute_only_ms": round(t_c, 3),
+                "compute_plus_optimizer_ms": round(t_o, 3),
+                "exposed_comm_ms": round(t_b - t_o, 3),
+                "exposed_comm_frac": round((t_b - t_o) / t_b, 4),
+                "exposed_frac": round((t_b - t_c) / t_b, 4),
+                "predicted_step_ms": round(si.predicted_step_s * 1e3, 3),
+                "predicted_compute_ms": round(si.predicted_compute_s * 1e3, 3),
+                "events": si.n_events, "buckets": si.n_buckets, "gathers": si.n_gather,
+                "reduces": si.n_reduce, "barriers": si.n_barriers,
+                "compute_model": (f"timed stand-ins: 6*Phi*B*S at {peak_tf} TF/s x "
+                                  f"{args.compute_eff}" if compute == "standin" else
+                                  "cuBLAS bf16 GEMMs of every linear module (fwd, dgrad, "
+                                  "wgrad into the gradient buffer), norms as stand-ins, "
+                                  "no attention"),
+                "profile": "synthetic B200 NVLink alpha-beta (680 GB/s, 5 us)"}
+
+    overlap = None
+    if args.overlap:
+        modes = ["gemm", "standin"] if args.compute == "both" else [args.compute]
+        results = [measure_overlap(c) for c in modes]
+        overlap = results[0]
+        if len(results) > 1:
+            overlap = dict(results[0], standin=results[1])
+        overlap["exposed_definitions"] = (
+            "exposed_comm = step - (compute + local optimizer, no NVLink); exposed_frac = "
+            "(step - compute only) / step, i.e. communication AND optimizer time not hidden")
 
     # End-to-end through the host-buffer C-ABI call.
     e2e = None

@@ -339,6 +339,12 @@ typedef struct {
                                    wgrad into the real gradient buffer),
                                    reading the gathered weights */
   int tokens;                   /* GEMM rows T (0 = micro_batch * seq_len) */
+  int gemm_sm_margin;           /* SMs withheld from GEMMs for the concurrent
+                                   communication / optimizer kernels (cuBLAS
+                                   SM-count target = SMs - margin) */
+  int gather_mode;              /* all-gathers: 0 = SM kernel (NVLink pulls,
+                                   tile-interleaved sources); 1 = copy
+                                   engines (peer cudaMemcpyAsync, no SMs) */
 } amsp_sched_config_t;
 
 typedef struct {
@@ -350,9 +356,11 @@ typedef struct {
 int amsp_sched_create(amsp_engine_t* e, const amsp_sched_config_t* cfg,
                       const amsp_profile_t* profile, amsp_sched_t** out);
 int amsp_sched_info(const amsp_sched_t* s, amsp_sched_info_t* info);
-/* One step; with_comm = 0 runs the compute stand-ins only (the exposed-
- * communication baseline). stream = the compute stream (NULL: engine's). */
-int amsp_sched_step(amsp_sched_t* s, int step, void* stream, int with_comm);
+/* One step. mode 1 = the full step; 0 = compute only; 2 = compute + the
+ * optimizer's local HBM work without any NVLink traffic (a timing proxy for
+ * the exposed-communication baseline, not a valid update). stream = the
+ * compute stream (NULL: engine's). */
+int amsp_sched_step(amsp_sched_t* s, int step, void* stream, int mode);
 /* Measured trace: with tracing on, every graph event of a step
  * is bracketed by CUDA events; amsp_sched_trace renders the last traced step
  * with the reference's render_trace (overlap_sim.cpp:560-577), so measured

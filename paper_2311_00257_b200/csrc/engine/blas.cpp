@@ -33,6 +33,8 @@ Blas::Blas() {
   if (!lib_) return;
   create_ = reinterpret_cast<decltype(create_)>(dlsym(lib_, "cublasCreate_v2"));
   set_stream_ = reinterpret_cast<decltype(set_stream_)>(dlsym(lib_, "cublasSetStream_v2"));
+  set_sm_target_ =
+      reinterpret_cast<decltype(set_sm_target_)>(dlsym(lib_, "cublasSetSmCountTarget"));
   auto gemm = reinterpret_cast<decltype(gemm_ex_)>(dlsym(lib_, "cublasGemmEx"));
   if (!create_ || !set_stream_ || !gemm) return;
   if (create_(&handle_) != 0) return;
@@ -46,6 +48,11 @@ void Blas::gemm(cudaStream_t s, bool ta, bool tb, int m, int n, int k, const voi
   const int st = gemm_ex_(handle_, ta ? kOpT : kOpN, tb ? kOpT : kOpN, m, n, k, &one, a, kBf16,
                           lda, b, kBf16, ldb, &zero, c, kBf16, ldc, kCompute32F, kAlgoDefault);
   if (st != 0) throw shardplan::Error("cublasGemmEx failed with status " + std::to_string(st));
+}
+
+void Blas::set_sm_target(int sms) {
+  if (!set_sm_target_) return;  // older cuBLAS: ignore the hint
+  if (set_sm_target_(handle_, sms) != 0) throw shardplan::Error("cublasSetSmCountTarget failed");
 }
 
 // Column-major views: a row-major [r, c] matrix is a col-major [c, r] one.

@@ -21,6 +21,9 @@ class Blas {
   // dw[out,in] = dy[T,out]^T * x[T,in]
   void linear_wgrad(cudaStream_t s, const void* dy, const void* x, void* dw, int T, int in,
                     int out);
+  // Limit the SMs GEMM kernels are sized for (0 = all): leaves SMs free for
+  // concurrently running communication / optimizer kernels.
+  void set_sm_target(int sms);
 
  private:
   Blas();
@@ -30,6 +33,7 @@ class Blas {
   void* handle_ = nullptr;
   int (*create_)(void**) = nullptr;
   int (*set_stream_)(void*, cudaStream_t) = nullptr;
+  int (*set_sm_target_)(void*, int) = nullptr;
   int (*gemm_ex_)(void*, int, int, int, int, int, const void*, const void*, int, int,
                   const void*, int, int, const void*, void*, int, int, int, int) = nullptr;
 };

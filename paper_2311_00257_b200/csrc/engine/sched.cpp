@@ -89,7 +89,8 @@ struct amsp_sched {
   // T x max-dim bf16, a 3-layer ring of gathered module weights (s_p > 1)
   // and a head-weight scratch (the head is never gathered by the graph).
   bool gemm_mode = false;
-  int tokens = 0, layers_k = 1;
+  bool gather_dma = false;  // all-gathers on the copy engines
+  int tokens = 0, layers_k = 1, gemm_sm_target = 0;
   uint16_t* act = nullptr;
   uint16_t* dout = nullptr;
   uint16_t* yout = nullptr;
@@ -116,6 +117,7 @@ struct amsp_sched {
       return;
     }
     amsp::Blas& blas = amsp::Blas::instance();
+    blas.set_sm_target(gemm_sm_target);
     const int t = w.tensor;  // -1: LM head
     const uint16_t* wt = weight_of(t);
     switch (w.gemm) {
@@ -272,6 +274,20 @@ struct amsp_sched {
   }
 
   void gather_tensor(int t, cudaStream_t s) {
+    if (gather_dma) {
+      // Copy-engine all-gather: one peer-to-local DMA per P-group member
+      // (rotated start, like the SM kernel) — no SMs taken from compute.
+      const std::uint64_t len = e->pmap.slice_len[t], src = e->pmap.pshard_offset[t];
+      uint16_t* dst = gather_dst(t);
+      for (int j = 0; j < e->sp; ++j) {
+        const int q = (e->p_group.position + 1 + j) % e->sp;
+        ck(cudaMemcpyAsync(dst + static_cast<std::uint64_t>(q) * len,
+                           e->params_of(e->p_group.members[q]) + src, len * 2,
+                           cudaMemcpyDeviceToDevice, s),
+           "gather DMA");
+      }
+      return;
+    }
     amsp::GatherArgs g{};
     g.segs = d_tcopy + t;
     g.nseg = 1;
@@ -286,7 +302,8 @@ struct amsp_sched {
     ++e->launches;
   }
 
-  void run(int step, cudaStream_t main, bool with_comm) {
+  void run(int step, cudaStream_t main, int mode) {
+    const bool with_comm = mode == 1, local_optimizer = mode == 2;
     if (step < 1) throw Error("sched: step index must be >= 1");
     e->require_peers();
     ++epoch;
@@ -341,6 +358,26 @@ struct amsp_sched {
     for (int k = 0; k < 2; ++k) {
       ck(cudaEventRecord(join_ev[k], comm[k]), "event record");
       ck(cudaStreamWaitEvent(main, join_ev[k], 0), "stream wait");
+    }
+    if (local_optimizer) {
+      // Baseline "compute + optimizer, no communication": the fused update
+      // of this rank's shard from its OWN gradients only, written to its own
+      // parameters — the optimizer's HBM work without any NVLink traffic
+      // (a timing proxy; the values are not the step's).
+      amsp::FusedArgs a{};
+      a.segs = e->d_segs;
+      a.nseg = e->nseg;
+      a.ntiles = e->ntiles;
+      a.grads[0] = e->grads_of(e->rank);
+      a.ndst = 1;
+      a.dsts[0] = e->params_of(e->rank);
+      a.master = e->master;
+      a.exp_avg = e->exp_avg;
+      a.exp_avg_sq = e->exp_avg_sq;
+      a.s = scalars;
+      ck(amsp::launch_fused_step(a, 1, e->sms * 2, 4, main), "local optimizer");
+      ++e->launches;
+      return;
     }
     if (!with_comm) return;
     // Barrier semantics (overlap_sim.cpp:166-174): every gradient is reduced
@@ -472,6 +509,7 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
   }
 
   s->gemm_mode = cfg->compute_mode == 1;
+  s->gather_dma = cfg->gather_mode == 1;
   s->layers_k = K;
   std::uint64_t max_out = 0;
   std::vector<amsp::Seg> rsegs;
@@ -650,7 +688,14 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
       ck(cudaEventCreateWithFlags(&s->events[i], cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s->start_ev, cudaEventDisableTiming), "event");
   for (auto& ev : s->join_ev) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
-  for (auto& st : s->comm) ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  // Communication streams get the highest priority so their CTAs are placed
+  // first whenever SMs free up between compute CTAs.
+  int lo_prio = 0, hi_prio = 0;
+  ck(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio), "stream priorities");
+  for (auto& st : s->comm)
+    ck(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi_prio), "stream");
+  if (s->gemm_mode && cfg->gemm_sm_margin > 0)
+    s->gemm_sm_target = std::max(1, e->sms - cfg->gemm_sm_margin);
   if (s->gemm_mode) {
     amsp::Blas::instance();  // fail now, not mid-step, when cuBLAS is missing
     s->tokens = cfg->tokens > 0 ? cfg->tokens : model.micro_batch * model.seq_len;
@@ -714,11 +759,12 @@ int amsp_sched_info(const amsp_sched_t* s, amsp_sched_info_t* info) {
   });
 }
 
-int amsp_sched_step(amsp_sched_t* s, int step, void* stream, int with_comm) {
+int amsp_sched_step(amsp_sched_t* s, int step, void* stream, int mode) {
   return amsp::guarded([&] {
     if (!s) throw Error("sched: null argument");
     s->e->use_device();
-    s->run(step, s->e->pick(stream), with_comm != 0);
+    if (mode < 0 || mode > 2) throw Error("sched: mode must be 0, 1 or 2");
+    s->run(step, s->e->pick(stream), mode);
   });
 }
 

@@ -184,7 +184,8 @@ class Scheduler:
 
     def __init__(self, engine: Engine, model: ModelSpec, profile, cost=None, sim=None,
                  comm_ctas: int = 0, compute_ctas: int = 0, time_scale: float = 1.0,
-                 optimizer_overlap: bool = True, compute: str = "standin", tokens: int = 0):
+                 optimizer_overlap: bool = True, compute: str = "standin", tokens: int = 0,
+                 gemm_sm_margin: int = 0, gather: str = "sm"):
         from .shardplan import CostConfig, SimConfig
         cost = cost or CostConfig()
         sim = sim or SimConfig()
@@ -205,15 +206,19 @@ class Scheduler:
                          arr(sim.bwd_grad_weight_times), arr(sim.bwd_grad_input_times),
                          sim.head_fwd_time, sim.head_bwd_time)
         cfg = N.SchedConfig(m, cost._c(), sc, comm_ctas, compute_ctas, time_scale,
-                            int(optimizer_overlap), {"standin": 0, "gemm": 1}[compute], tokens)
+                            int(optimizer_overlap), {"standin": 0, "gemm": 1}[compute], tokens,
+                            gemm_sm_margin, {"sm": 0, "dma": 1}[gather])
         self.engine = engine
         self._h = C.c_void_p()
         N.check(N.lib().amsp_sched_create(engine._h, C.byref(cfg), profile._h, C.byref(self._h)))
         self.info = N.SchedInfo()
         N.check(N.lib().amsp_sched_info(self._h, C.byref(self.info)))
 
-    def step(self, step: int, stream=None, with_comm: bool = True) -> None:
-        N.check(N.lib().amsp_sched_step(self._h, step, _stream_ptr(stream), int(with_comm)))
+    def step(self, step: int, stream=None, with_comm=True) -> None:
+        """with_comm: True = full step, False = compute only, "optimizer" =
+        compute + local optimizer work without communication (timing)."""
+        mode = 2 if with_comm == "optimizer" else int(bool(with_comm))
+        N.check(N.lib().amsp_sched_step(self._h, step, _stream_ptr(stream), mode))
 
     def enable_trace(self, on: bool = True) -> None:
         N.check(N.lib().amsp_sched_enable_trace(self._h, int(on)))
