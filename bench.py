@@ -198,7 +198,7 @@ def cpu_baseline(phi_total, world, steps_budget_s=12.0, sample=None):
     grads = [O.grads(0, n, DEFAULT_SEED, 1, r) for r in range(world)]
     master = np.array([0.0], np.float32)
     master = np.empty(n, np.float32)
-    O.lib()  # load
+    O.use_all_threads()
     master[:] = 0.01
     m = np.zeros(n, np.float32)
     v = np.zeros(n, np.float32)
@@ -216,7 +216,7 @@ def cpu_baseline(phi_total, world, steps_budget_s=12.0, sample=None):
         if time.perf_counter() - t_start > steps_budget_s or len(times) >= 5:
             break
     best = min(times)
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    cores = O.use_all_threads()
     return {"value": n / best, "unit": "params/s", "cores": cores, "kind": "port",
             "sample": f"{n} consecutive params of the {phi_total}-param flat model, {world} "
                       f"rank gradients reduced + AdamW + bf16 into {world} param copies; "
@@ -240,6 +240,7 @@ def run_reference(args):
     from paper_2311_00257_b200.engine import DEFAULT_SEED
     n = 32 << 20
     h = O.hyper()
+    O.use_all_threads()
     grads = [O.grads(0, n, DEFAULT_SEED, 1, r) for r in range(world)]
     master = np.full(n, 0.01, np.float32)
     m = np.zeros(n, np.float32)
@@ -252,7 +253,7 @@ def run_reference(args):
         O.step(grads, [(0, 0, n)], master, m, v, params, O.scalars(t, world, h))
     dt = (time.perf_counter() - t0) / args.steps
     value = n / dt
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    cores = O.use_all_threads()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "params/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

@@ -42,6 +42,22 @@
 
 #include "amsp_oracle.h"
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* The CPU baseline uses every host thread regardless of OMP_NUM_THREADS
+ * (torchrun exports 1); returns the thread count now in effect. */
+int amsp_o_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
+}
+
 uint64_t amsp_o_splitmix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

@@ -20,6 +20,7 @@ typedef struct {
   double lr, beta1, beta2, eps, weight_decay;
 } amsp_o_hyper;
 
+int amsp_o_set_threads(int n);
 uint64_t amsp_o_splitmix64(uint64_t x);
 uint16_t amsp_o_f32_to_bf16(float f);
 float amsp_o_bf16_to_f32(uint16_t h);

@@ -33,6 +33,8 @@ def lib() -> C.CDLL:
         u64p = C.POINTER(C.c_uint64)
         fp = C.POINTER(C.c_float)
         u16p = C.POINTER(C.c_uint16)
+        L.amsp_o_set_threads.restype = C.c_int
+        L.amsp_o_set_threads.argtypes = [C.c_int]
         L.amsp_o_grad_bf16.restype = C.c_uint16
         L.amsp_o_grad_bf16.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64]
         L.amsp_o_master_init.restype = C.c_float
@@ -51,6 +53,13 @@ def lib() -> C.CDLL:
                                   fp, C.POINTER(u16p), C.c_int, C.POINTER(Scalars)]
         _lib = L
     return _lib
+
+
+def use_all_threads() -> int:
+    """Run the CPU step on every host thread (torchrun exports
+    OMP_NUM_THREADS=1); returns the thread count in effect."""
+    import os
+    return lib().amsp_o_set_threads(os.cpu_count() or 1)
 
 
 def _p(a, t):
