@@ -350,14 +350,21 @@ int amsp_engine_step_host(amsp_engine_t* e, int step, const void* host_grads,
     if (!e || !host_grads) throw Error("engine: null argument");
     e->use_device();
     cudaStream_t s = e->pick(stream);
-    const std::size_t total = e->phi * 2, chunk = std::size_t{1} << 30;
-    char* dst = reinterpret_cast<char*>(e->grads_of(e->rank));
-    const char* src = static_cast<const char*>(host_grads);
-    for (std::size_t off = 0; off < total; off += chunk)
-      ck(cudaMemcpyAsync(dst + off, src + off, std::min(chunk, total - off),
-                         cudaMemcpyHostToDevice, s),
-         "H2D gradients");
-    e->step(step, s);
+    if (step < 1) throw Error("engine: step index must be >= 1");
+    if (e->world == 1) {
+      e->step_host_pipelined(step, host_grads, s);
+    } else {
+      // Multi-rank: every rank's full gradient must be resident before any
+      // owner pulls, so upload first, then the barrier-bracketed step.
+      const std::size_t total = e->phi * 2, chunk = std::size_t{1} << 30;
+      char* dst = reinterpret_cast<char*>(e->grads_of(e->rank));
+      const char* src = static_cast<const char*>(host_grads);
+      for (std::size_t off = 0; off < total; off += chunk)
+        ck(cudaMemcpyAsync(dst + off, src + off, std::min(chunk, total - off),
+                           cudaMemcpyHostToDevice, s),
+           "H2D gradients");
+      e->step(step, s);
+    }
     if (host_stats)
       ck(cudaMemcpyAsync(host_stats, e->stats, 2 * sizeof(float), cudaMemcpyDeviceToHost, s),
          "D2H stats");
@@ -466,6 +473,9 @@ void amsp_engine_destroy(amsp_engine_t* e) {
       cudaIpcCloseMemHandle(e->peer_base[r]);
   cudaFree(e->shared);
   cudaFree(e->priv);
+  cudaFree(e->d_chunk_segs);
+  for (auto ev : e->chunk_events) cudaEventDestroy(ev);
+  if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
   if (e->own_stream) cudaStreamDestroy(e->own_stream);
   for (auto* pairs : {&e->kernel_events, &e->gather_events})
     for (auto& ev : *pairs) {

@@ -178,6 +178,74 @@ struct amsp_engine {
     if (h) throw amsp::CudaFailure("cross-GPU barrier timed out (a peer did not arrive)");
   }
 
+  // Host-buffer step of a single rank, pipelined: the gradient upload is cut
+  // into chunks on a copy stream and the fused update of chunk c runs as
+  // soon as chunk c has landed, so the PCIe copy hides the HBM-bound update.
+  static constexpr std::uint64_t kHostChunk = std::uint64_t{1} << 28;  // elements (512 MB)
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> chunk_events;
+  std::vector<int> chunk_begin, chunk_nseg, chunk_ntiles;
+  amsp::Seg* d_chunk_segs = nullptr;
+
+  void build_chunks() {
+    std::vector<amsp::Seg> segs;
+    for (std::uint64_t lo = 0; lo < phi; lo += kHostChunk) {
+      const std::uint64_t hi = std::min(phi, lo + kHostChunk);
+      chunk_begin.push_back(static_cast<int>(segs.size()));
+      long long tiles = 0;
+      for (const auto& s : layout.segs) {
+        const std::uint64_t a = std::max(lo, s.flat), b = std::min(hi, s.flat + s.len);
+        if (a >= b) continue;
+        const std::uint64_t off = a - s.flat;
+        segs.push_back({a, s.os + off, s.dst + off, b - a, static_cast<unsigned long long>(tiles)});
+        tiles += static_cast<long long>((b - a + amsp::kTile - 1) / amsp::kTile);
+      }
+      chunk_nseg.push_back(static_cast<int>(segs.size()) - chunk_begin.back());
+      chunk_ntiles.push_back(static_cast<int>(tiles));
+    }
+    ck(cudaMalloc(&d_chunk_segs, std::max<std::size_t>(segs.size(), 1) * sizeof(amsp::Seg)),
+       "cudaMalloc chunk segs");
+    ck(cudaMemcpy(d_chunk_segs, segs.data(), segs.size() * sizeof(amsp::Seg),
+                  cudaMemcpyHostToDevice),
+       "copy chunk segs");
+    ck(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "copy stream");
+    chunk_events.resize(chunk_begin.size());
+    for (auto& ev : chunk_events)
+      ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+  }
+
+  void step_host_pipelined(int t, const void* host, cudaStream_t s) {
+    if (chunk_begin.empty()) build_chunks();
+    const char* src = static_cast<const char*>(host);
+    char* dst = reinterpret_cast<char*>(grads_of(rank));
+    ck(cudaMemsetAsync(stats, 0, 2 * sizeof(float), s), "reset stats");
+    // The copies must not overwrite gradients the previous work still reads.
+    ck(cudaEventRecord(chunk_events[0], s), "event record");
+    ck(cudaStreamWaitEvent(copy_stream, chunk_events[0], 0), "stream wait");
+    amsp::FusedArgs a{};
+    a.grads[0] = grads_of(rank);
+    a.ndst = 1;
+    a.dsts[0] = params_of(rank);
+    a.master = master;
+    a.exp_avg = exp_avg;
+    a.exp_avg_sq = exp_avg_sq;
+    a.s = amsp::make_adam_scalars(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, t, 1.0);
+    a.stats = stats;
+    for (std::size_t c = 0; c < chunk_begin.size(); ++c) {
+      const std::uint64_t lo = c * kHostChunk, n = std::min(kHostChunk, phi - lo);
+      ck(cudaMemcpyAsync(dst + lo * 2, src + lo * 2, n * 2, cudaMemcpyHostToDevice, copy_stream),
+         "H2D gradients");
+      ck(cudaEventRecord(chunk_events[c], copy_stream), "event record");
+      ck(cudaStreamWaitEvent(s, chunk_events[c], 0), "stream wait");
+      a.segs = d_chunk_segs + chunk_begin[c];
+      a.nseg = chunk_nseg[c];
+      a.ntiles = chunk_ntiles[c];
+      ck(amsp::launch_fused_step(a, 1, std::max(1, std::min(a.ntiles, grid)), variant, s),
+         "fused step launch");
+      ++launches;
+    }
+  }
+
   void require_peers() const {
     if (world > 1 && !imported)
       throw Error("engine: peers not imported (amsp_engine_import_handles)");

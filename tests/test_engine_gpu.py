@@ -138,6 +138,29 @@ def test_host_buffer_step_matches_device_path(cuda):
     e.close()
 
 
+def test_host_step_pipelined_across_chunks(cuda):
+    """Single-rank host-buffer step uploads in 256M-element chunks on a copy
+    stream and updates each chunk behind it: check elements on both sides of
+    the chunk boundary and at the ragged tail."""
+    import torch
+    tensors = [200_000_000, 100_000_008, 64]
+    phi = sum(tensors)
+    e = Engine(tensors, _plan(M(1, 1)), M(1, 1))
+    e.init_state()
+    host = torch.empty(phi, dtype=torch.int16, pin_memory=True)
+    for t in (1, 2):
+        host.numpy().view(np.uint16)[:] = O.grads(0, phi, DEFAULT_SEED, t, 0)
+        e.step_host(t, host.data_ptr())
+    b = 1 << 28
+    idx = np.unique(np.concatenate([np.arange(0, phi, 104729), np.arange(b - 40, b + 40),
+                                    np.arange(phi - 80, phi)])).astype(np.uint64)
+    want = O.trajectory(idx, DEFAULT_SEED, 2, 1, H)
+    assert np.array_equal(e.read("master")[idx], want[0])
+    assert np.array_equal(e.read("exp_avg_sq")[idx], want[2])
+    assert np.array_equal(e.read("params")[idx], want[3])
+    e.close()
+
+
 def test_llama1b_sampled_after_3_steps(cuda):
     """Full-size layout (1B params, 8-way greedy OS shards emulated would need
     8x the memory; use the single-rank replica) checked on a strided sample
