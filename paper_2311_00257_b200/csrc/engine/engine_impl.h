@@ -144,14 +144,26 @@ struct amsp_engine {
   }
   void use_device() const { ck(cudaSetDevice(cfg.device), "cudaSetDevice"); }
 
-  // Auto (v = 0) for one rank: one 8-element vector in flight per thread,
-  // <= 64 registers, 2 CTAs per SM — the best point of the r01 sweep on
-  // LLaMA-7B (tools/tune_fused.py, profiles/r01_tune_7b.jsonl).
+  // Auto (v = 0) for one rank: the TMA bulk-copy pipeline (variant 5, 3-stage
+  // ring, 1 CTA per SM: 29.9 ms = 96.8% of measured copy bandwidth on
+  // LLaMA-7B, profiles/r01_tune_tma.jsonl) when every segment is 8-element
+  // aligned, else the LDG kernel with one vector in flight, <= 64 registers,
+  // 2 CTAs per SM (profiles/r01_tune_7b.jsonl).
+  bool segments_aligned() const {
+    for (const auto& s : layout.segs)
+      if ((s.flat | s.os | s.dst | s.len) & 7u) return false;
+    return true;
+  }
+
   void retune(int v, int forced_grid) {
-    variant = (v == 0 && world == 1) ? 4 : v;
-    const int per_sm = amsp::fused_blocks_per_sm(world, variant);
-    int g = sms * per_sm;
-    if (v == 0 && world == 1) g = 2 * sms;
+    int g = 0;
+    if (v == 0 && world == 1) {
+      variant = segments_aligned() ? 5 : 4;
+      g = variant == 5 ? sms : 2 * sms;
+    } else {
+      variant = v;
+      g = sms * amsp::fused_blocks_per_sm(world, variant);
+    }
     grid = forced_grid > 0 ? forced_grid : g;
     grid = std::max(1, std::min(ntiles, grid));
   }

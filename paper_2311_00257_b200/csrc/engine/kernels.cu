@@ -509,6 +509,173 @@ __global__ void spin_kernel(unsigned long long ns, float* sink) {
   if (x == 123.456f) sink[threadIdx.x] = x;  // keep the loop alive
 }
 
+// ---------------------------------------------------------------------------
+// TMA-pipelined fused step for a single rank (W = 1; variant 5).
+//
+// Warp 8 is a producer: one lane walks the CTA's tiles and, per tile, issues
+// four bulk async copies (cp.async.bulk, the TMA engine's 1-D path) of the
+// bf16 gradients and fp32 master / m / v into a kStages-deep shared-memory
+// ring, signalling completion through an mbarrier transaction count. Warps
+// 0-7 consume: each thread reads its 8 elements from shared memory, applies
+// AdamW and streams master / m / v / bf16 params straight to global memory.
+// Memory-level parallelism now comes from the ring (kStages x 28 KB in
+// flight per CTA) instead of registers, which is what limits the LDG
+// version at 16 warps / SM (ncu: long-scoreboard stalls).
+// Ring depth is a template parameter: 3 stages (84 KB, 2 CTAs / SM) or 6
+// stages (168 KB, 1 CTA / SM).
+constexpr int kTmaConsumers = 256;
+constexpr int kTmaTile = kTmaConsumers * 8;  // elements per stage (2048)
+constexpr int kTmaStageBytes = kTmaTile * (2 + 4 + 4 + 4);
+constexpr int tma_smem(int stages) { return stages * kTmaStageBytes + 1024; }
+
+struct TmaStageMeta {
+  unsigned long long os, dst, len;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+template <int kTmaStages>
+__global__ void __launch_bounds__(kTmaConsumers + 32, kTmaStages <= 3 ? 2 : 1)
+fused_step_tma_kernel(const FusedArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint16_t* s_g = reinterpret_cast<uint16_t*>(smem);
+  float* s_p = reinterpret_cast<float*>(smem + kTmaStages * kTmaTile * 2);
+  float* s_m = s_p + kTmaStages * kTmaTile;
+  float* s_v = s_m + kTmaStages * kTmaTile;
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_v + kTmaStages * kTmaTile);
+  uint64_t* empty = full + kTmaStages;
+  TmaStageMeta* meta = reinterpret_cast<TmaStageMeta*>(empty + kTmaStages);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // Tiles of this CTA: blockIdx.x, +gridDim.x, ... over the segment table
+  // re-cut into kTmaTile-element tiles (tile0 of a Seg counts kTile = 4096
+  // tiles, so every kTile tile holds two TMA tiles).
+  const int ntiles = a.ntiles * 2;
+  if (warp == kTmaConsumers / 32) {  // producer warp
+    if (lane == 0) {
+      SegCursor<Seg, 1> cur;  // global-table binary search (one thread)
+      cur.table = a.segs;
+      cur.n = a.nseg;
+      cur.cur = 0;
+      cur.staged = false;
+      int k = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int s = k % kTmaStages;
+        if (k >= kTmaStages) mbar_wait(&empty[s], ((k / kTmaStages) - 1) & 1);
+        const Seg& sg = cur.at(t / 2);
+        const unsigned long long base =
+            (static_cast<unsigned long long>(t / 2) - sg.tile0) * kTile + (t & 1) * kTmaTile;
+        unsigned long long len = 0;
+        if (base < sg.len) len = sg.len - base < kTmaTile ? sg.len - base : kTmaTile;
+        meta[s] = {sg.os + base, sg.dst + base, len};
+        const uint32_t bytes = static_cast<uint32_t>(len * 14);
+        mbar_expect_tx(&full[s], bytes);
+        if (len) {
+          bulk_g2s(s_g + s * kTmaTile, a.grads[0] + sg.flat + base, len * 2, &full[s]);
+          bulk_g2s(s_p + s * kTmaTile, a.master + sg.os + base, len * 4, &full[s]);
+          bulk_g2s(s_m + s * kTmaTile, a.exp_avg + sg.os + base, len * 4, &full[s]);
+          bulk_g2s(s_v + s * kTmaTile, a.exp_avg_sq + sg.os + base, len * 4, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  float sq = 0.0f;
+  int k = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int s = k % kTmaStages;
+    mbar_wait(&full[s], (k / kTmaStages) & 1);
+    const TmaStageMeta md = meta[s];
+    const unsigned long long e = static_cast<unsigned long long>(threadIdx.x) * 8;
+    if (e < md.len) {  // segment lengths are multiples of 8 on this path
+      const uint4 graw = *reinterpret_cast<const uint4*>(s_g + s * kTmaTile + e);
+      float4 p[2], m[2], v[2];
+      p[0] = *reinterpret_cast<const float4*>(s_p + s * kTmaTile + e);
+      p[1] = *reinterpret_cast<const float4*>(s_p + s * kTmaTile + e + 4);
+      m[0] = *reinterpret_cast<const float4*>(s_m + s * kTmaTile + e);
+      m[1] = *reinterpret_cast<const float4*>(s_m + s * kTmaTile + e + 4);
+      v[0] = *reinterpret_cast<const float4*>(s_v + s * kTmaTile + e);
+      v[1] = *reinterpret_cast<const float4*>(s_v + s * kTmaTile + e + 4);
+      float* pf = reinterpret_cast<float*>(p);
+      float* mf = reinterpret_cast<float*>(m);
+      float* vf = reinterpret_cast<float*>(v);
+      const uint32_t* gw = reinterpret_cast<const uint32_t*>(&graw);
+      uint32_t packed[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float glo = __fmul_rn(bf16_lo(gw[w]), a.s.grad_scale);
+        const float ghi = __fmul_rn(bf16_hi(gw[w]), a.s.grad_scale);
+        sq += glo * glo + ghi * ghi;
+        adamw(a.s, glo, pf[2 * w], mf[2 * w], vf[2 * w]);
+        adamw(a.s, ghi, pf[2 * w + 1], mf[2 * w + 1], vf[2 * w + 1]);
+        packed[w] = pack_bf16x2(pf[2 * w], pf[2 * w + 1]);
+      }
+      const unsigned long long o = md.os + e;
+      st_stream_v4(a.master + o, p[0]);
+      st_stream_v4(a.master + o + 4, p[1]);
+      st_stream_v4(a.exp_avg + o, m[0]);
+      st_stream_v4(a.exp_avg + o + 4, m[1]);
+      st_stream_v4(a.exp_avg_sq + o, v[0]);
+      st_stream_v4(a.exp_avg_sq + o + 4, v[1]);
+      st_v4(a.dsts[0] + md.dst + e, make_uint4(packed[0], packed[1], packed[2], packed[3]));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (a.stats != nullptr) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if (lane == 0) atomicAdd(a.stats, sq);
+  }
+}
+
 int sm_count() {
   static int n = [] {
     int dev = 0, c = 148;
@@ -551,7 +718,35 @@ FusedFn select_fused(int world, int variant) {
 
 }  // namespace
 
+// Variants 5 / 6: the TMA pipeline with a 3- / 6-stage ring.
+template <int kStages>
+cudaError_t tma_prepare() {
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      fused_step_tma_kernel<kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      tma_smem(kStages));
+  return attr;
+}
+
+template <int kStages>
+int tma_blocks_per_sm() {
+  int blocks = 0;
+  if (tma_prepare<kStages>() == cudaSuccess)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fused_step_tma_kernel<kStages>,
+                                                  kTmaConsumers + 32, tma_smem(kStages));
+  return blocks > 0 ? blocks : 1;
+}
+
+template <int kStages>
+cudaError_t tma_launch(const FusedArgs& a, int grid, cudaStream_t stream) {
+  const cudaError_t attr = tma_prepare<kStages>();
+  if (attr != cudaSuccess) return attr;
+  fused_step_tma_kernel<kStages><<<grid, kTmaConsumers + 32, tma_smem(kStages), stream>>>(a);
+  return cudaGetLastError();
+}
+
 int fused_blocks_per_sm(int world, int variant) {
+  if (variant == 5) return tma_blocks_per_sm<3>();
+  if (variant == 6) return tma_blocks_per_sm<6>();
   FusedFn f = select_fused(world, variant);
   int blocks = 0;
   if (f) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f, kBlock, 0);
@@ -561,6 +756,10 @@ int fused_blocks_per_sm(int world, int variant) {
 cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int variant,
                               cudaStream_t stream) {
   if (a.ntiles == 0) return cudaSuccess;
+  if (variant == 5 || variant == 6) {  // TMA pipeline: single rank, 8-aligned segments
+    if (world != 1) return cudaErrorInvalidValue;
+    return variant == 5 ? tma_launch<3>(a, grid, stream) : tma_launch<6>(a, grid, stream);
+  }
   FusedFn f = select_fused(world, variant);
   if (!f) return cudaErrorInvalidValue;
   f<<<grid, kBlock, 0, stream>>>(a);

@@ -53,10 +53,14 @@ def _check_rank(e, want_full, steps):
     assert np.array_equal(params, want), int(np.sum(params != want))
 
 
-@pytest.mark.parametrize("layout", ["greedy", "contiguous"])
-def test_single_gpu_tiny_10_steps_bit_exact(cuda, layout):
+@pytest.mark.parametrize("layout,variant", [("greedy", 0), ("contiguous", 0), ("greedy", 5),
+                                            ("greedy", 1), ("greedy", 2), ("greedy", 3)])
+def test_single_gpu_tiny_10_steps_bit_exact(cuda, layout, variant):
+    """variant 5 = the TMA bulk-copy pipeline (cp.async.bulk + mbarrier)."""
     model = S.model("tiny")
     e = Engine(model, _plan(M(1, 1)), M(1, 1), layout=layout)
+    if variant:
+        e.tune(variant)
     e.init_state()
     steps = 10
     for t in range(1, steps + 1):

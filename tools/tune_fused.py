@@ -23,8 +23,8 @@ def main():
     ap.add_argument("--model", default="llama-7b")
     ap.add_argument("--world", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--variants", default="0,1,2,3,4")
-    ap.add_argument("--grids", default="0,148,296,592,1184,2368,-1")
+    ap.add_argument("--variants", default="5,6")
+    ap.add_argument("--grids", default="148,296")
     args = ap.parse_args()
     M = S.DeviceMesh
     model = S.model(args.model)
