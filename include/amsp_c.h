@@ -300,7 +300,8 @@ int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t cou
  * 2 two vectors, 3 two vectors + >=3 CTAs/SM, 4 one vector + >=4 CTAs/SM;
  * grid 0 = SMs x resident CTAs (persistent). */
 int amsp_engine_tune(amsp_engine_t* e, int variant, int grid);
-/* All-gather kernel grid (0 = 4 CTAs per SM). */
+/* All-gather kernel grid (0 = 4 CTAs per SM; -1 = copy engines instead of
+ * an SM kernel). */
 int amsp_engine_tune_gather(amsp_engine_t* e, int grid);
 /* Bracket every fused launch with CUDA events on the step's stream (enable
  * != 0), then read the summed kernel time of the launches since enabling

@@ -414,7 +414,7 @@ int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t cou
 
 int amsp_engine_tune_gather(amsp_engine_t* e, int grid) {
   return amsp::guarded([&] {
-    if (!e || grid < 0) throw Error("engine: bad argument");
+    if (!e || grid < -1) throw Error("engine: bad argument");
     e->gather_grid = grid;
   });
 }

@@ -270,6 +270,24 @@ struct amsp_engine {
       throw Error("engine: gather unit out of range");
     require_peers();
     const GatherUnit& u = units[unit];
+    if (gather_grid < 0) {
+      // Copy-engine all-gather: per tensor of the unit, one peer-to-local
+      // DMA per P-group member (rotated start), no SMs involved.
+      uint16_t* dst = slots[slot & 1];
+      const std::uint64_t base = pmap.tensor_offset[u.first_tensor];
+      for (int i = 0; i < u.n_tensors; ++i) {
+        const std::size_t t = static_cast<std::size_t>(u.first_tensor + i);
+        const std::uint64_t len = pmap.slice_len[t];
+        for (int j = 0; j < sp; ++j) {
+          const int q = (p_group.position + 1 + j) % sp;
+          ck(cudaMemcpyAsync(dst + (pmap.tensor_offset[t] - base) + q * len,
+                             params_of(p_group.members[q]) + pmap.pshard_offset[t], len * 2,
+                             cudaMemcpyDeviceToDevice, s),
+             "gather DMA");
+        }
+      }
+      return;
+    }
     amsp::GatherArgs g{};
     g.segs = d_copy + u.seg_begin;
     g.nseg = u.nseg;

@@ -24,7 +24,7 @@ from paper_2311_00257_b200.engine import Engine  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="llama-13b")
-    ap.add_argument("--grids", default="0,148,296,592,1184")
+    ap.add_argument("--grids", default="0,-1,296,-1,0")
     ap.add_argument("--passes", type=int, default=4)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
