@@ -431,7 +431,8 @@ def run_ours(args):
     # kernel. s_p > 1: the all-gather passes are part of the roofline bytes,
     # so the whole step is the timed unit.
     t_meas = kernel_ms if info.sp == 1 else ms_per_step
-    scope = ("fused_step_kernel (reduce + AdamW + gather)" if info.sp == 1 else
+    kname = "fused_step_tma_kernel" if info.variant in (5, 6) else "fused_step_kernel"
+    scope = (f"{kname} (reduce + AdamW + gather), variant {info.variant}" if info.sp == 1 else
              "whole step: 2 all-gather passes (gather_kernel) + fused reduce/AdamW + barriers")
     hbm_ach = hbm_b / (t_meas * 1e-3) / 1e9
     nvl_ach = nvl_b / (t_meas * 1e-3) / 1e9

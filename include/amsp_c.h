@@ -251,6 +251,7 @@ typedef struct {
   uint64_t param_elems;         /* elements of `params` (Phi / s_p) */
   int n_units;                  /* all-gather units (s_p > 1) */
   uint64_t slot_elems;          /* gathered-unit slot capacity */
+  int variant;                  /* fused-kernel variant in use (see amsp_engine_tune) */
 } amsp_engine_info_t;
 
 #define AMSP_IPC_HANDLE_BYTES 64
@@ -297,7 +298,9 @@ int amsp_engine_read(amsp_engine_t* e, int which, uint64_t offset, uint64_t coun
 int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t count,
                       const void* host_src);
 /* Fused-kernel tuning: variant 0 auto, 1 one vector in flight per thread,
- * 2 two vectors, 3 two vectors + >=3 CTAs/SM, 4 one vector + >=4 CTAs/SM;
+ * 2 two vectors, 3 two vectors + >=3 CTAs/SM, 4 one vector + >=4 CTAs/SM,
+ * 5 TMA bulk-copy pipeline (3 stages), 6 TMA (6 stages) -- 5/6 need W = 1
+ * and 8-element-aligned segments;
  * grid 0 = SMs x resident CTAs (persistent). */
 int amsp_engine_tune(amsp_engine_t* e, int variant, int grid);
 /* All-gather kernel grid (0 = 4 CTAs per SM; -1 = copy engines instead of

@@ -111,7 +111,8 @@ class EngineInfo(C.Structure):
                 ("master", C.c_void_p), ("exp_avg", C.c_void_p),
                 ("exp_avg_sq", C.c_void_p), ("device_bytes", C.c_uint64),
                 ("sp", C.c_int), ("p_position", C.c_int), ("param_elems", C.c_uint64),
-                ("n_units", C.c_int), ("slot_elems", C.c_uint64)]
+                ("n_units", C.c_int), ("slot_elems", C.c_uint64),
+                ("variant", C.c_int)]
 
 
 class SchedConfig(C.Structure):

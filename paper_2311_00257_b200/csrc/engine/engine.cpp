@@ -234,6 +234,7 @@ int amsp_engine_info(const amsp_engine_t* e, amsp_engine_info_t* info) {
     info->param_elems = e->param_elems;
     info->n_units = static_cast<int>(e->units.size());
     info->slot_elems = e->slot_elems;
+    info->variant = e->variant;
   });
 }
 
@@ -424,7 +425,6 @@ int amsp_engine_tune(amsp_engine_t* e, int variant, int grid) {
     if (!e) throw Error("engine: null argument");
     if (variant < 0 || variant > 6) throw Error("engine: unknown kernel variant");
     if (variant >= 5) {
-      if (e->world != 1) throw Error("engine: the TMA variant is single-rank only");
       for (const auto& s : e->layout.segs)
         if ((s.flat | s.os | s.dst | s.len) & 7u)
           throw Error("engine: the TMA variant needs 8-element-aligned segments");

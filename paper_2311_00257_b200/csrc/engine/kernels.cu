@@ -510,23 +510,31 @@ __global__ void spin_kernel(unsigned long long ns, float* sink) {
 }
 
 // ---------------------------------------------------------------------------
-// TMA-pipelined fused step for a single rank (W = 1; variant 5).
+// TMA-pipelined fused step (variants 5 / 6), any W.
 //
-// Warp 8 is a producer: one lane walks the CTA's tiles and, per tile, issues
-// four bulk async copies (cp.async.bulk, the TMA engine's 1-D path) of the
-// bf16 gradients and fp32 master / m / v into a kStages-deep shared-memory
-// ring, signalling completion through an mbarrier transaction count. Warps
-// 0-7 consume: each thread reads its 8 elements from shared memory, applies
-// AdamW and streams master / m / v / bf16 params straight to global memory.
-// Memory-level parallelism now comes from the ring (kStages x 28 KB in
-// flight per CTA) instead of registers, which is what limits the LDG
-// version at 16 warps / SM (ncu: long-scoreboard stalls).
-// Ring depth is a template parameter: 3 stages (84 KB, 2 CTAs / SM) or 6
-// stages (168 KB, 1 CTA / SM).
+// The last warp is a producer: one lane walks the CTA's tiles and, per tile,
+// issues W + 3 bulk async copies (cp.async.bulk, the TMA engine's 1-D path):
+// the bf16 gradients of every DP rank (local HBM for r = rank, NVLink peer
+// memory otherwise) and the fp32 master / m / v of this rank's shard, into a
+// kStages-deep shared-memory ring; completion is signalled through an
+// mbarrier transaction count. Warps 0-7 consume: each thread sums its 8
+// elements' gradients in fixed rank order from shared memory, applies AdamW
+// and streams master / m / v locally and the bf16 params into every OS-group
+// peer. Memory-level parallelism comes from the ring (kStages x stage bytes
+// in flight per CTA) instead of registers, which is what limits the LDG
+// version at 16 warps / SM (ncu: long-scoreboard stalls) -- and the NVLink
+// pulls need the most bytes in flight of all (peer latency ~2x HBM).
+// Ring depth: variant 5 sizes the ring for 2 CTAs / SM (<= 100 KB), variant
+// 6 for 1 CTA / SM (<= 220 KB).
 constexpr int kTmaConsumers = 256;
 constexpr int kTmaTile = kTmaConsumers * 8;  // elements per stage (2048)
-constexpr int kTmaStageBytes = kTmaTile * (2 + 4 + 4 + 4);
-constexpr int tma_smem(int stages) { return stages * kTmaStageBytes + 1024; }
+constexpr int tma_stage_bytes(int w) { return kTmaTile * (2 * w + 12); }
+constexpr int tma_stages(int w, int variant) {
+  return (variant == 5 ? 100 * 1024 : 220 * 1024) / tma_stage_bytes(w) < 2
+             ? 2
+             : (variant == 5 ? 100 * 1024 : 220 * 1024) / tma_stage_bytes(w);
+}
+constexpr int tma_smem(int w, int stages) { return stages * tma_stage_bytes(w) + 1024; }
 
 struct TmaStageMeta {
   unsigned long long os, dst, len;
@@ -571,21 +579,21 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
       : "memory");
 }
 
-template <int kTmaStages>
-__global__ void __launch_bounds__(kTmaConsumers + 32, kTmaStages <= 3 ? 2 : 1)
+template <int W, int kStages, int kMinBlocks>
+__global__ void __launch_bounds__(kTmaConsumers + 32, kMinBlocks)
 fused_step_tma_kernel(const FusedArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  uint16_t* s_g = reinterpret_cast<uint16_t*>(smem);
-  float* s_p = reinterpret_cast<float*>(smem + kTmaStages * kTmaTile * 2);
-  float* s_m = s_p + kTmaStages * kTmaTile;
-  float* s_v = s_m + kTmaStages * kTmaTile;
-  uint64_t* full = reinterpret_cast<uint64_t*>(s_v + kTmaStages * kTmaTile);
-  uint64_t* empty = full + kTmaStages;
-  TmaStageMeta* meta = reinterpret_cast<TmaStageMeta*>(empty + kTmaStages);
+  uint16_t* s_g = reinterpret_cast<uint16_t*>(smem);  // [kStages][W][kTmaTile]
+  float* s_p = reinterpret_cast<float*>(smem + kStages * W * kTmaTile * 2);
+  float* s_m = s_p + kStages * kTmaTile;
+  float* s_v = s_m + kStages * kTmaTile;
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_v + kStages * kTmaTile);
+  uint64_t* empty = full + kStages;
+  TmaStageMeta* meta = reinterpret_cast<TmaStageMeta*>(empty + kStages);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kTmaConsumers / 32);
     }
@@ -606,18 +614,20 @@ fused_step_tma_kernel(const FusedArgs a) {
       cur.staged = false;
       int k = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-        const int s = k % kTmaStages;
-        if (k >= kTmaStages) mbar_wait(&empty[s], ((k / kTmaStages) - 1) & 1);
+        const int s = k % kStages;
+        if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
         const Seg& sg = cur.at(t / 2);
         const unsigned long long base =
             (static_cast<unsigned long long>(t / 2) - sg.tile0) * kTile + (t & 1) * kTmaTile;
         unsigned long long len = 0;
         if (base < sg.len) len = sg.len - base < kTmaTile ? sg.len - base : kTmaTile;
         meta[s] = {sg.os + base, sg.dst + base, len};
-        const uint32_t bytes = static_cast<uint32_t>(len * 14);
-        mbar_expect_tx(&full[s], bytes);
+        mbar_expect_tx(&full[s], static_cast<uint32_t>(len * (2 * W + 12)));
         if (len) {
-          bulk_g2s(s_g + s * kTmaTile, a.grads[0] + sg.flat + base, len * 2, &full[s]);
+#pragma unroll
+          for (int r = 0; r < W; ++r)
+            bulk_g2s(s_g + (s * W + r) * kTmaTile, a.grads[r] + sg.flat + base, len * 2,
+                     &full[s]);
           bulk_g2s(s_p + s * kTmaTile, a.master + sg.os + base, len * 4, &full[s]);
           bulk_g2s(s_m + s * kTmaTile, a.exp_avg + sg.os + base, len * 4, &full[s]);
           bulk_g2s(s_v + s * kTmaTile, a.exp_avg_sq + sg.os + base, len * 4, &full[s]);
@@ -630,12 +640,15 @@ fused_step_tma_kernel(const FusedArgs a) {
   float sq = 0.0f;
   int k = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-    const int s = k % kTmaStages;
-    mbar_wait(&full[s], (k / kTmaStages) & 1);
+    const int s = k % kStages;
+    mbar_wait(&full[s], (k / kStages) & 1);
     const TmaStageMeta md = meta[s];
     const unsigned long long e = static_cast<unsigned long long>(threadIdx.x) * 8;
     if (e < md.len) {  // segment lengths are multiples of 8 on this path
-      const uint4 graw = *reinterpret_cast<const uint4*>(s_g + s * kTmaTile + e);
+      uint4 graw[W];
+#pragma unroll
+      for (int r = 0; r < W; ++r)
+        graw[r] = *reinterpret_cast<const uint4*>(s_g + (s * W + r) * kTmaTile + e);
       float4 p[2], m[2], v[2];
       p[0] = *reinterpret_cast<const float4*>(s_p + s * kTmaTile + e);
       p[1] = *reinterpret_cast<const float4*>(s_p + s * kTmaTile + e + 4);
@@ -646,12 +659,19 @@ fused_step_tma_kernel(const FusedArgs a) {
       float* pf = reinterpret_cast<float*>(p);
       float* mf = reinterpret_cast<float*>(m);
       float* vf = reinterpret_cast<float*>(v);
-      const uint32_t* gw = reinterpret_cast<const uint32_t*>(&graw);
       uint32_t packed[4];
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        const float glo = __fmul_rn(bf16_lo(gw[w]), a.s.grad_scale);
-        const float ghi = __fmul_rn(bf16_hi(gw[w]), a.s.grad_scale);
+        const uint32_t* g0 = reinterpret_cast<const uint32_t*>(&graw[0]);
+        float glo = bf16_lo(g0[w]), ghi = bf16_hi(g0[w]);
+#pragma unroll
+        for (int r = 1; r < W; ++r) {  // fixed rank order, as the LDG kernel
+          const uint32_t* gr = reinterpret_cast<const uint32_t*>(&graw[r]);
+          glo = __fadd_rn(glo, bf16_lo(gr[w]));
+          ghi = __fadd_rn(ghi, bf16_hi(gr[w]));
+        }
+        glo = __fmul_rn(glo, a.s.grad_scale);
+        ghi = __fmul_rn(ghi, a.s.grad_scale);
         sq += glo * glo + ghi * ghi;
         adamw(a.s, glo, pf[2 * w], mf[2 * w], vf[2 * w]);
         adamw(a.s, ghi, pf[2 * w + 1], mf[2 * w + 1], vf[2 * w + 1]);
@@ -664,11 +684,15 @@ fused_step_tma_kernel(const FusedArgs a) {
       st_stream_v4(a.exp_avg + o + 4, m[1]);
       st_stream_v4(a.exp_avg_sq + o, v[0]);
       st_stream_v4(a.exp_avg_sq + o + 4, v[1]);
-      st_v4(a.dsts[0] + md.dst + e, make_uint4(packed[0], packed[1], packed[2], packed[3]));
+      const uint4 out = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      for (int d = 0; d < a.ndst; ++d) st_v4(a.dsts[d] + md.dst + e, out);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
+  // Peer parameter stores must be visible system-wide before the trailing
+  // cross-GPU barrier releases the other ranks.
+  if (a.fence_peers) __threadfence_system();
   if (a.stats != nullptr) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
@@ -718,35 +742,64 @@ FusedFn select_fused(int world, int variant) {
 
 }  // namespace
 
-// Variants 5 / 6: the TMA pipeline with a 3- / 6-stage ring.
-template <int kStages>
-cudaError_t tma_prepare() {
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      fused_step_tma_kernel<kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-      tma_smem(kStages));
-  return attr;
+// Variants 5 / 6: the TMA pipeline, ring sized for 2 / 1 CTAs per SM.
+template <int W, int V>
+struct Tma {
+  static constexpr int kStages = tma_stages(W, V);
+  static constexpr int kSmem = tma_smem(W, kStages);
+  static cudaError_t prepare() {
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        fused_step_tma_kernel<W, kStages, V == 5 ? 2 : 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    return attr;
+  }
+  static int blocks_per_sm() {
+    int blocks = 0;
+    if (prepare() == cudaSuccess)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fused_step_tma_kernel<W, kStages, V == 5 ? 2 : 1>,
+                                                    kTmaConsumers + 32, kSmem);
+    return blocks > 0 ? blocks : 1;
+  }
+  static cudaError_t launch(const FusedArgs& a, int grid, cudaStream_t stream) {
+    const cudaError_t attr = prepare();
+    if (attr != cudaSuccess) return attr;
+    fused_step_tma_kernel<W, kStages, V == 5 ? 2 : 1><<<grid, kTmaConsumers + 32, kSmem, stream>>>(a);
+    return cudaGetLastError();
+  }
+};
+
+template <int V>
+int tma_blocks_per_sm(int world) {
+  switch (world) {
+    case 1: return Tma<1, V>::blocks_per_sm();
+    case 2: return Tma<2, V>::blocks_per_sm();
+    case 3: return Tma<3, V>::blocks_per_sm();
+    case 4: return Tma<4, V>::blocks_per_sm();
+    case 5: return Tma<5, V>::blocks_per_sm();
+    case 6: return Tma<6, V>::blocks_per_sm();
+    case 7: return Tma<7, V>::blocks_per_sm();
+    case 8: return Tma<8, V>::blocks_per_sm();
+    default: return 1;
+  }
 }
 
-template <int kStages>
-int tma_blocks_per_sm() {
-  int blocks = 0;
-  if (tma_prepare<kStages>() == cudaSuccess)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fused_step_tma_kernel<kStages>,
-                                                  kTmaConsumers + 32, tma_smem(kStages));
-  return blocks > 0 ? blocks : 1;
-}
-
-template <int kStages>
-cudaError_t tma_launch(const FusedArgs& a, int grid, cudaStream_t stream) {
-  const cudaError_t attr = tma_prepare<kStages>();
-  if (attr != cudaSuccess) return attr;
-  fused_step_tma_kernel<kStages><<<grid, kTmaConsumers + 32, tma_smem(kStages), stream>>>(a);
-  return cudaGetLastError();
+template <int V>
+cudaError_t tma_launch(const FusedArgs& a, int world, int grid, cudaStream_t stream) {
+  switch (world) {
+    case 1: return Tma<1, V>::launch(a, grid, stream);
+    case 2: return Tma<2, V>::launch(a, grid, stream);
+    case 3: return Tma<3, V>::launch(a, grid, stream);
+    case 4: return Tma<4, V>::launch(a, grid, stream);
+    case 5: return Tma<5, V>::launch(a, grid, stream);
+    case 6: return Tma<6, V>::launch(a, grid, stream);
+    case 7: return Tma<7, V>::launch(a, grid, stream);
+    case 8: return Tma<8, V>::launch(a, grid, stream);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 int fused_blocks_per_sm(int world, int variant) {
-  if (variant == 5) return tma_blocks_per_sm<3>();
-  if (variant == 6) return tma_blocks_per_sm<6>();
+  if (variant == 5) return tma_blocks_per_sm<5>(world);
+  if (variant == 6) return tma_blocks_per_sm<6>(world);
   FusedFn f = select_fused(world, variant);
   int blocks = 0;
   if (f) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f, kBlock, 0);
@@ -756,10 +809,8 @@ int fused_blocks_per_sm(int world, int variant) {
 cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int variant,
                               cudaStream_t stream) {
   if (a.ntiles == 0) return cudaSuccess;
-  if (variant == 5 || variant == 6) {  // TMA pipeline: single rank, 8-aligned segments
-    if (world != 1) return cudaErrorInvalidValue;
-    return variant == 5 ? tma_launch<3>(a, grid, stream) : tma_launch<6>(a, grid, stream);
-  }
+  if (variant == 5) return tma_launch<5>(a, world, grid, stream);  // 8-aligned segments only
+  if (variant == 6) return tma_launch<6>(a, world, grid, stream);
   FusedFn f = select_fused(world, variant);
   if (!f) return cudaErrorInvalidValue;
   f<<<grid, kBlock, 0, stream>>>(a);

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--sched", action="store_true")
     ap.add_argument("--model", default="tiny")
     ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (5/6 = TMA)")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
@@ -45,6 +46,8 @@ def main():
     e = Engine(S.model(args.model), plan, dp, rank=rank, device=local, layout=args.layout,
                skip_gathers=args.sched)
     e.connect()
+    if args.variant:
+        e.tune(args.variant)
     e.init_state()
     sched = None
     if args.sched:  # overlap scheduler: real cross-GPU barriers per bucket / module

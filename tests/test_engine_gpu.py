@@ -96,18 +96,23 @@ def test_ragged_tensors_scalar_path(cuda):
             e.close()
 
 
-@pytest.mark.parametrize("world,os_k,layout", [(2, 2, "greedy"), (4, 4, "greedy"),
-                                               (4, 2, "greedy"), (8, 8, "greedy"),
-                                               (4, 4, "contiguous"), (8, 2, "contiguous")])
-def test_emulated_dp_group_bit_exact(cuda, world, os_k, layout):
+@pytest.mark.parametrize("world,os_k,layout,variant", [
+    (2, 2, "greedy", 0), (4, 4, "greedy", 0), (4, 2, "greedy", 0), (8, 8, "greedy", 0),
+    (4, 4, "contiguous", 0), (8, 2, "contiguous", 0),
+    (2, 2, "greedy", 5), (4, 4, "greedy", 5), (4, 2, "greedy", 6), (8, 8, "greedy", 5),
+    (8, 8, "greedy", 6), (8, 2, "greedy", 5)])
+def test_emulated_dp_group_bit_exact(cuda, world, os_k, layout, variant):
     """W ranks of one DP group emulated on one GPU (link_local): fixed-order
     fp32 gradient sum over all W ranks, AdamW on each OS shard, bf16 params
-    gathered into every rank of the OS group (and replicas)."""
+    gathered into every rank of the OS group (and replicas). Variants 5 / 6:
+    the TMA pipeline with W gradient sources per stage."""
     model = S.model("tiny")
     plan = _plan(M(os_k, 1))
     engines = [Engine(model, plan, M(world, 1), rank=r, layout=layout) for r in range(world)]
     link_local(engines)
     for e in engines:
+        if variant:
+            e.tune(variant)
         e.init_state()
     steps = 4
     for t in range(1, steps + 1):

@@ -24,10 +24,15 @@ CASES = [(2, "2x1", None, "greedy", None), (2, "2x1", None, "contiguous", None),
          (4, "4x1", None, "greedy", "2x1"),                      # AMSP-13B-style
          (2, "2x1", None, "greedy", "sched"), (4, "4x1", None, "greedy", "sched"),
          (4, "4x1", None, "greedy", "4x1+sched"), (4, "2x1", None, "greedy", "sched")]
+CASES = [c + (0,) for c in CASES] + [
+    # TMA bulk-copy pipeline (variants 5 / 6) pulling peer gradients over NVLink
+    (2, "2x1", None, "greedy", None, 5), (2, "2x1", None, "greedy", None, 6),
+    (4, "4x1", None, "greedy", None, 5), (4, "4x1", None, "greedy", None, 6),
+    (4, "2x1", None, "greedy", None, 5)]
 
 
-@pytest.mark.parametrize("world,os_mesh,dp_mesh,layout,p_mesh", CASES)
-def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh):
+@pytest.mark.parametrize("world,os_mesh,dp_mesh,layout,p_mesh,variant", CASES)
+def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh, variant):
     sched = p_mesh is not None and "sched" in p_mesh
     if sched:
         p_mesh = p_mesh.split("+")[0] if "+" in p_mesh else None
@@ -42,6 +47,8 @@ def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh):
         cmd += ["--p-mesh", p_mesh]
     if sched:
         cmd += ["--sched"]
+    if variant:
+        cmd += ["--variant", str(variant)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=REPO,
                        env={**os.environ, "OMP_NUM_THREADS": "4"})
     out = r.stdout + r.stderr
