@@ -144,11 +144,14 @@ struct amsp_engine {
   }
   void use_device() const { ck(cudaSetDevice(cfg.device), "cudaSetDevice"); }
 
-  // Auto (v = 0) for one rank: the TMA bulk-copy pipeline (variant 5, 3-stage
-  // ring, 1 CTA per SM: 29.9 ms = 96.8% of measured copy bandwidth on
-  // LLaMA-7B, profiles/r01_tune_tma.jsonl) when every segment is 8-element
-  // aligned, else the LDG kernel with one vector in flight, <= 64 registers,
-  // 2 CTAs per SM (profiles/r01_tune_7b.jsonl).
+  // Auto (v = 0): the TMA bulk-copy pipeline (variant 5) when every segment
+  // is 8-element aligned. For one rank: 3-stage ring, 1 CTA per SM (29.9 ms =
+  // 96.8% of measured copy bandwidth on LLaMA-7B, profiles/r01_tune_tma.jsonl).
+  // For W > 1 the ring also carries the W-1 NVLink gradient pulls; 2 CTAs per
+  // SM (7B ZeRO-1: 21.7 ms vs 23.3 ms for the LDG kernel at W = 2, 30.8 vs
+  // 32.3 ms at W = 4; profiles/r01_tma_w_*.json). Unaligned segments fall back
+  // to the LDG kernel: one vector in flight, <= 64 registers, 2 CTAs per SM
+  // for one rank (profiles/r01_tune_7b.jsonl), the U = 2 kernel otherwise.
   bool segments_aligned() const {
     for (const auto& s : layout.segs)
       if ((s.flat | s.os | s.dst | s.len) & 7u) return false;
@@ -157,9 +160,12 @@ struct amsp_engine {
 
   void retune(int v, int forced_grid) {
     int g = 0;
-    if (v == 0 && world == 1) {
-      variant = segments_aligned() ? 5 : 4;
-      g = variant == 5 ? sms : 2 * sms;
+    if (v == 0 && segments_aligned()) {
+      variant = 5;
+      g = world == 1 ? sms : sms * amsp::fused_blocks_per_sm(world, variant);
+    } else if (v == 0 && world == 1) {
+      variant = 4;
+      g = 2 * sms;
     } else {
       variant = v;
       g = sms * amsp::fused_blocks_per_sm(world, variant);

@@ -99,13 +99,13 @@ def test_ragged_tensors_scalar_path(cuda):
 @pytest.mark.parametrize("world,os_k,layout,variant", [
     (2, 2, "greedy", 0), (4, 4, "greedy", 0), (4, 2, "greedy", 0), (8, 8, "greedy", 0),
     (4, 4, "contiguous", 0), (8, 2, "contiguous", 0),
-    (2, 2, "greedy", 5), (4, 4, "greedy", 5), (4, 2, "greedy", 6), (8, 8, "greedy", 5),
-    (8, 8, "greedy", 6), (8, 2, "greedy", 5)])
+    (2, 2, "greedy", 5), (4, 4, "greedy", 6), (4, 2, "greedy", 6), (8, 8, "greedy", 6),
+    (2, 2, "greedy", 2), (4, 4, "greedy", 1), (8, 8, "greedy", 2), (8, 2, "greedy", 1)])
 def test_emulated_dp_group_bit_exact(cuda, world, os_k, layout, variant):
     """W ranks of one DP group emulated on one GPU (link_local): fixed-order
     fp32 gradient sum over all W ranks, AdamW on each OS shard, bf16 params
-    gathered into every rank of the OS group (and replicas). Variants 5 / 6:
-    the TMA pipeline with W gradient sources per stage."""
+    gathered into every rank of the OS group (and replicas). Auto (0) and 5 /
+    6: the TMA pipeline with W gradient sources per stage; 1 / 2: LDG."""
     model = S.model("tiny")
     plan = _plan(M(os_k, 1))
     engines = [Engine(model, plan, M(world, 1), rank=r, layout=layout) for r in range(world)]

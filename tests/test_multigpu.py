@@ -25,10 +25,11 @@ CASES = [(2, "2x1", None, "greedy", None), (2, "2x1", None, "contiguous", None),
          (2, "2x1", None, "greedy", "sched"), (4, "4x1", None, "greedy", "sched"),
          (4, "4x1", None, "greedy", "4x1+sched"), (4, "2x1", None, "greedy", "sched")]
 CASES = [c + (0,) for c in CASES] + [
-    # TMA bulk-copy pipeline (variants 5 / 6) pulling peer gradients over NVLink
-    (2, "2x1", None, "greedy", None, 5), (2, "2x1", None, "greedy", None, 6),
-    (4, "4x1", None, "greedy", None, 5), (4, "4x1", None, "greedy", None, 6),
-    (4, "2x1", None, "greedy", None, 5)]
+    # auto (0) is the TMA bulk-copy pipeline (variant 5) for aligned layouts;
+    # variant 6 = the deeper 1-CTA/SM ring, 1 / 2 = the LDG kernels
+    (2, "2x1", None, "greedy", None, 6), (4, "4x1", None, "greedy", None, 6),
+    (2, "2x1", None, "greedy", None, 2), (4, "4x1", None, "greedy", None, 1),
+    (4, "2x1", None, "greedy", None, 2)]
 
 
 @pytest.mark.parametrize("world,os_mesh,dp_mesh,layout,p_mesh,variant", CASES)
