@@ -68,8 +68,11 @@ def parse():
     ap.add_argument("--optimizer-overlap", type=int, default=-1,
                     help="1: AdamW+push per bucket/module inside backward; 0: after the "
                          "barrier; -1: auto")
-    ap.add_argument("--gather", default="dma", choices=["dma", "sm"],
-                    help="overlapped all-gathers on copy engines (dma) or an SM kernel")
+    ap.add_argument("--gather", default="dma", choices=["dma", "sm", "tma"],
+                    help="overlapped all-gathers on copy engines (dma), the SM kernel or the "
+                         "TMA bulk-copy kernel")
+    ap.add_argument("--step-gather", default="sm", choices=["sm", "dma", "tma"],
+                    help="all-gather implementation inside the pipeline-only step (s_p > 1)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -371,6 +374,8 @@ def run_ours(args):
     eng.connect()
     if args.variant or args.grid:
         eng.tune(args.variant, args.grid)
+    if args.step_gather != "sm":
+        eng.tune_gather(args.step_gather)
     info = eng.info
     stream = torch.cuda.Stream(device=local)
     eng.init_state(stream)
@@ -433,7 +438,9 @@ def run_ours(args):
     t_meas = kernel_ms if info.sp == 1 else ms_per_step
     kname = "fused_step_tma_kernel" if info.variant in (5, 6) else "fused_step_kernel"
     scope = (f"{kname} (reduce + AdamW + gather), variant {info.variant}" if info.sp == 1 else
-             "whole step: 2 all-gather passes (gather_kernel) + fused reduce/AdamW + barriers")
+             "whole step: 2 all-gather passes (" +
+             {"sm": "gather_kernel", "dma": "copy engines", "tma": "gather_tma_kernel"}[args.step_gather] +
+             ") + fused reduce/AdamW + barriers")
     hbm_ach = hbm_b / (t_meas * 1e-3) / 1e9
     nvl_ach = nvl_b / (t_meas * 1e-3) / 1e9
     t_hbm = hbm_b / (pk["hbm_gbs"] * 1e9)
@@ -541,7 +548,8 @@ def run_ours(args):
                 "tokens_per_microbatch": args.micro_batch * args.seq_len,
                 "optimizer": "in backward (per bucket/module)" if opt
                              else "after the step barrier (paper)",
-                "gather": "copy engines" if args.gather == "dma" else "SM kernel",
+                "gather": {"dma": "copy engines", "sm": "SM kernel",
+                           "tma": "TMA bulk-copy kernel"}[args.gather],
                 "comm_ctas": ctas,
                 "step_ms": round(t_b, 3), "compute_only_ms": round(t_c, 3),
                 "compute_plus_optimizer_ms": round(t_o, 3),
@@ -595,7 +603,11 @@ def run_ours(args):
         e2e = {"value": phi / e2e_s, "unit": "params/s", "ms_per_step": round(e2e_s * 1e3, 3),
                "h2d_bytes_per_step": 2 * phi * world, "d2h_bytes_per_step": 8 * world,
                "steps": args.e2e_steps,
-               "path": "amsp_engine_step_host: pinned host bf16 grads -> H2D -> step -> D2H stats"}
+               "path": ("amsp_engine_step_host: pinned host bf16 grads -> chunked H2D (2^28 "
+                        "elements) on a copy stream, each chunk's fused update (W > 1: after a "
+                        "cross-GPU barrier) behind it -> D2H stats"
+                        if info.sp == 1 else
+                        "amsp_engine_step_host: pinned host bf16 grads -> H2D -> step -> D2H stats")}
         del host
 
     cpu = None

@@ -303,8 +303,10 @@ int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t cou
  * and 8-element-aligned segments;
  * grid 0 = SMs x resident CTAs (persistent). */
 int amsp_engine_tune(amsp_engine_t* e, int variant, int grid);
-/* All-gather kernel grid (0 = 4 CTAs per SM; -1 = copy engines instead of
- * an SM kernel). */
+/* All-gather implementation: grid > 0 = the SM (LDG/STG) kernel with that
+ * many CTAs, 0 = the SM kernel with 4 CTAs per SM, -1 = copy engines (one
+ * peer-to-local DMA per P-group member), -2 = the TMA bulk-copy kernel
+ * (single-warp CTAs; needs 8-element-aligned P slices). */
 int amsp_engine_tune_gather(amsp_engine_t* e, int grid);
 /* Bracket every fused launch with CUDA events on the step's stream (enable
  * != 0), then read the summed kernel time of the launches since enabling
@@ -348,7 +350,9 @@ typedef struct {
                                    SM-count target = SMs - margin) */
   int gather_mode;              /* all-gathers: 0 = SM kernel (NVLink pulls,
                                    tile-interleaved sources); 1 = copy
-                                   engines (peer cudaMemcpyAsync, no SMs) */
+                                   engines (peer cudaMemcpyAsync, no SMs);
+                                   2 = TMA bulk-copy kernel (single-warp
+                                   CTAs, 8-element-aligned P slices) */
 } amsp_sched_config_t;
 
 typedef struct {

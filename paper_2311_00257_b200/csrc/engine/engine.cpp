@@ -352,11 +352,11 @@ int amsp_engine_step_host(amsp_engine_t* e, int step, const void* host_grads,
     e->use_device();
     cudaStream_t s = e->pick(stream);
     if (step < 1) throw Error("engine: step index must be >= 1");
-    if (e->world == 1) {
+    if (e->sp == 1) {
       e->step_host_pipelined(step, host_grads, s);
     } else {
-      // Multi-rank: every rank's full gradient must be resident before any
-      // owner pulls, so upload first, then the barrier-bracketed step.
+      // Parameter sharding: upload first, then the barrier-bracketed step
+      // (its all-gathers run before the fused update).
       const std::size_t total = e->phi * 2, chunk = std::size_t{1} << 30;
       char* dst = reinterpret_cast<char*>(e->grads_of(e->rank));
       const char* src = static_cast<const char*>(host_grads);
@@ -415,7 +415,9 @@ int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t cou
 
 int amsp_engine_tune_gather(amsp_engine_t* e, int grid) {
   return amsp::guarded([&] {
-    if (!e || grid < -1) throw Error("engine: bad argument");
+    if (!e || grid < -2) throw Error("engine: bad argument");
+    if (grid == amsp_engine::kGatherTma && !e->copies_aligned())
+      throw Error("engine: the TMA all-gather needs 8-element-aligned P slices");
     e->gather_grid = grid;
   });
 }

@@ -89,6 +89,14 @@ struct amsp_engine {
   uint32_t** d_peer_flags = nullptr;
   int nseg = 0, ntiles = 0, npseg = 0, nptiles = 0;
   int grid = 0, variant = 0, sms = 148, gather_grid = 0;
+  // gather_grid: > 0 SM-kernel grid, 0 SM kernel with its default grid,
+  // kGatherDma copy engines, kGatherTma the bulk-copy kernel.
+  static constexpr int kGatherDma = -1, kGatherTma = -2;
+  bool copies_aligned() const {
+    for (std::size_t t = 0; t < pmap.slice_len.size(); ++t)
+      if ((pmap.slice_len[t] | pmap.pshard_offset[t] | pmap.tensor_offset[t]) & 7u) return false;
+    return true;
+  }
   std::uint64_t device_bytes = 0;
 
   cudaStream_t own_stream = nullptr;
@@ -196,9 +204,12 @@ struct amsp_engine {
     if (h) throw amsp::CudaFailure("cross-GPU barrier timed out (a peer did not arrive)");
   }
 
-  // Host-buffer step of a single rank, pipelined: the gradient upload is cut
-  // into chunks on a copy stream and the fused update of chunk c runs as
-  // soon as chunk c has landed, so the PCIe copy hides the HBM-bound update.
+  // Host-buffer step (s_p = 1), pipelined: the gradient upload is cut into
+  // chunks of the flat index space on a copy stream, and the fused update of
+  // chunk c runs as soon as chunk c has landed, so the PCIe copy hides the
+  // update. With W > 1 a cross-GPU barrier per chunk proves every rank's
+  // chunk c is resident before the owners pull it; a final barrier proves
+  // every owner's parameter stores have landed.
   static constexpr std::uint64_t kHostChunk = std::uint64_t{1} << 28;  // elements (512 MB)
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> chunk_events;
@@ -233,35 +244,44 @@ struct amsp_engine {
   }
 
   void step_host_pipelined(int t, const void* host, cudaStream_t s) {
+    if (sp != 1) throw Error("engine: the pipelined host step needs s_p = 1");
+    require_peers();
     if (chunk_begin.empty()) build_chunks();
     const char* src = static_cast<const char*>(host);
     char* dst = reinterpret_cast<char*>(grads_of(rank));
     ck(cudaMemsetAsync(stats, 0, 2 * sizeof(float), s), "reset stats");
-    // The copies must not overwrite gradients the previous work still reads.
+    // The copies must not overwrite gradients the previous work still reads
+    // (for W > 1 the previous step ended with a barrier after every pull).
     ck(cudaEventRecord(chunk_events[0], s), "event record");
     ck(cudaStreamWaitEvent(copy_stream, chunk_events[0], 0), "stream wait");
     amsp::FusedArgs a{};
-    a.grads[0] = grads_of(rank);
-    a.ndst = 1;
-    a.dsts[0] = params_of(rank);
+    for (int r = 0; r < world; ++r) a.grads[r] = grads_of(r);
+    a.ndst = static_cast<int>(dst_members.size());
+    for (int d = 0; d < a.ndst; ++d) a.dsts[d] = params_of(dst_members[d]);
     a.master = master;
     a.exp_avg = exp_avg;
     a.exp_avg_sq = exp_avg_sq;
-    a.s = amsp::make_adam_scalars(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, t, 1.0);
+    a.s = amsp::make_adam_scalars(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, t,
+                                  1.0 / world);
     a.stats = stats;
+    a.fence_peers = (world > 1 && !local_linked) ? 1 : 0;
     for (std::size_t c = 0; c < chunk_begin.size(); ++c) {
       const std::uint64_t lo = c * kHostChunk, n = std::min(kHostChunk, phi - lo);
       ck(cudaMemcpyAsync(dst + lo * 2, src + lo * 2, n * 2, cudaMemcpyHostToDevice, copy_stream),
          "H2D gradients");
       ck(cudaEventRecord(chunk_events[c], copy_stream), "event record");
       ck(cudaStreamWaitEvent(s, chunk_events[c], 0), "stream wait");
+      barrier(s);  // chunk c of every rank is resident
       a.segs = d_chunk_segs + chunk_begin[c];
       a.nseg = chunk_nseg[c];
       a.ntiles = chunk_ntiles[c];
-      ck(amsp::launch_fused_step(a, 1, std::max(1, std::min(a.ntiles, grid)), variant, s),
-         "fused step launch");
-      ++launches;
+      if (a.ntiles > 0) {
+        ck(amsp::launch_fused_step(a, world, std::max(1, std::min(a.ntiles, grid)), variant, s),
+           "fused step launch");
+        ++launches;
+      }
     }
+    barrier(s);  // every owner's parameter stores have landed
   }
 
   void require_peers() const {
@@ -276,7 +296,7 @@ struct amsp_engine {
       throw Error("engine: gather unit out of range");
     require_peers();
     const GatherUnit& u = units[unit];
-    if (gather_grid < 0) {
+    if (gather_grid == kGatherDma) {
       // Copy-engine all-gather: per tensor of the unit, one peer-to-local
       // DMA per P-group member (rotated start), no SMs involved.
       uint16_t* dst = slots[slot & 1];
@@ -300,10 +320,11 @@ struct amsp_engine {
     g.ntiles = u.ntiles;
     for (int q = 0; q < sp; ++q) g.src[q] = params_of(p_group.members[q]);
     g.dst = slots[slot & 1];
-    g.grid = gather_grid;
+    g.grid = gather_grid > 0 ? gather_grid : 0;
     g.sp = sp;
     g.rot = (p_group.position + 1) % sp;
-    ck(amsp::launch_gather(g, s), "gather launch");
+    ck(gather_grid == kGatherTma ? amsp::launch_gather_tma(g, s) : amsp::launch_gather(g, s),
+       "gather launch");
     ++launches;
   }
 

@@ -700,6 +700,71 @@ fused_step_tma_kernel(const FusedArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA all-gather of one unit (s_p > 1): one thread per CTA drives a ring of
+// kGatherStages 8 KB shared-memory stages. Each tile is one bulk load
+// (cp.async.bulk, peer P shard over NVLink -> shared memory, completion on an
+// mbarrier) followed by one bulk store (shared -> the local gathered buffer,
+// bulk async-group). Loads of the next kGatherStages - 1 tiles are in flight
+// while a store drains, so the NVLink pulls keep ~32 KB in flight per CTA
+// with no register staging, and the CTA is a single warp: it leaves the
+// SM's warps, registers and most of its shared memory to the GEMMs it
+// overlaps with. Tiles and source interleaving are those of gather_kernel.
+// Every CopySeg must be 8-element aligned (16-byte bulk granularity).
+constexpr int kGatherStages = 5;
+
+__device__ __forceinline__ void bulk_s2g(void* gmem_dst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
+               "r"(smem_addr(smem_src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(32) gather_tma_kernel(const GatherArgs a) {
+  __shared__ __align__(128) uint16_t buf[kGatherStages][kTile];
+  __shared__ __align__(8) uint64_t full[kGatherStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kGatherStages; ++s) mbar_init(&full[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+  const int n = a.ntiles > static_cast<int>(blockIdx.x)
+                    ? (a.ntiles - 1 - static_cast<int>(blockIdx.x)) / gridDim.x + 1
+                    : 0;
+  SegCursor<CopySeg, 1> cur;  // global-table search from a forward cursor
+  cur.table = a.segs;
+  cur.n = a.nseg;
+  cur.cur = 0;
+  cur.staged = false;
+  uint16_t* dst_of[kGatherStages];
+  uint32_t bytes_of[kGatherStages];
+  auto load = [&](int i) {
+    const int tile = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
+    const CopySeg& cs = cur.at(tile);
+    const unsigned long long v = static_cast<unsigned long long>(tile) - cs.tile0;
+    const unsigned long long chunk = v / a.sp;
+    const int q = static_cast<int>((v % a.sp + a.rot) % a.sp);
+    const unsigned long long off = chunk * kTile;
+    const unsigned long long len = cs.len - off < kTile ? cs.len - off : kTile;
+    const int s = i % kGatherStages;
+    dst_of[s] = a.dst + cs.dst + static_cast<unsigned long long>(q) * cs.len + off;
+    bytes_of[s] = static_cast<uint32_t>(len * 2);
+    mbar_expect_tx(&full[s], bytes_of[s]);
+    bulk_g2s(buf[s], a.src[q] + cs.src + off, bytes_of[s], &full[s]);
+  };
+  for (int i = 0; i < n && i < kGatherStages; ++i) load(i);
+  for (int i = 0; i < n; ++i) {
+    const int s = i % kGatherStages;
+    mbar_wait(&full[s], (i / kGatherStages) & 1);
+    bulk_s2g(dst_of[s], buf[s], bytes_of[s]);
+    const int j = i - 1 + kGatherStages;  // refill the stage tile i-1 used
+    if (i >= 1 && j < n) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      load(j);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int sm_count() {
   static int n = [] {
     int dev = 0, c = 148;
@@ -864,6 +929,13 @@ cudaError_t launch_gather(const GatherArgs& a, cudaStream_t stream) {
   if (a.ntiles == 0) return cudaSuccess;
   const int grid = a.grid > 0 ? a.grid : sm_count() * 4;
   gather_kernel<<<std::min(a.ntiles, grid), 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_tma(const GatherArgs& a, cudaStream_t stream) {
+  if (a.ntiles == 0) return cudaSuccess;
+  const int grid = a.grid > 0 ? a.grid : sm_count() * 4;
+  gather_tma_kernel<<<std::min(a.ntiles, grid), 32, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -110,6 +110,9 @@ cudaError_t launch_spin(int ctas, unsigned long long ns, cudaStream_t stream);
 cudaError_t launch_init_params(const Seg* psegs, int nseg, int ntiles, uint16_t* params,
                                uint64_t seed, cudaStream_t stream);
 cudaError_t launch_gather(const GatherArgs& a, cudaStream_t stream);
+// Bulk-copy (TMA) variant of launch_gather: 32-thread CTAs, every CopySeg
+// 8-element aligned (see kernels.cu gather_tma_kernel).
+cudaError_t launch_gather_tma(const GatherArgs& a, cudaStream_t stream);
 cudaError_t launch_init_state(const Seg* segs, int nseg, int ntiles, float* master,
                               float* m, float* v, uint64_t seed, int grid,
                               cudaStream_t stream);

@@ -82,6 +82,10 @@ struct amsp_sched {
   int n_barriers = 0, end_a = 0, end_b = 0, n_buckets = 0, n_gather = 0, n_reduce = 0,
       n_compute = 0;
   Table resid, pending;  // end of step: fused update / AdamW-from-reduced update
+  // The end-of-step fused update runs after compute, alone on the GPU: it
+  // takes the engine's tuned kernel (the TMA pipeline when the residual
+  // table is 8-element aligned) instead of the co-resident LDG kernel.
+  int resid_variant = 0;
   amsp::Seg* d_rsegs = nullptr;
   amsp::CopySeg* d_tcopy = nullptr;
   float* red = nullptr;
@@ -90,6 +94,7 @@ struct amsp_sched {
   // and a head-weight scratch (the head is never gathered by the graph).
   bool gemm_mode = false;
   bool gather_dma = false;  // all-gathers on the copy engines
+  bool gather_tma = false;  // all-gathers by the bulk-copy (TMA) kernel
   int tokens = 0, layers_k = 1, gemm_sm_target = 0;
   uint16_t* act = nullptr;
   uint16_t* dout = nullptr;
@@ -254,7 +259,7 @@ struct amsp_sched {
     ++e->launches;
   }
 
-  void fused(const Table& t, int grid, cudaStream_t s) {
+  void fused(const Table& t, int grid, cudaStream_t s, int variant = 0) {
     if (t.ntiles == 0) return;
     amsp::FusedArgs a{};
     a.segs = d_rsegs + t.begin;
@@ -269,7 +274,8 @@ struct amsp_sched {
     a.s = scalars;
     a.stats = nullptr;
     a.fence_peers = (e->world > 1 && !e->local_linked) ? 1 : 0;
-    ck(amsp::launch_fused_step(a, e->world, grid, 0, s), "sched fused");
+    ck(amsp::launch_fused_step(a, e->world, std::max(1, std::min(t.ntiles, grid)), variant, s),
+       "sched fused");
     ++e->launches;
   }
 
@@ -298,7 +304,7 @@ struct amsp_sched {
     for (int q = 0; q < e->sp; ++q) g.src[q] = e->params_of(e->p_group.members[q]);
     g.dst = gather_dst(t);
     g.grid = comm_ctas;
-    ck(amsp::launch_gather(g, s), "sched gather");
+    ck(gather_tma ? amsp::launch_gather_tma(g, s) : amsp::launch_gather(g, s), "sched gather");
     ++e->launches;
   }
 
@@ -375,16 +381,20 @@ struct amsp_sched {
       a.exp_avg = e->exp_avg;
       a.exp_avg_sq = e->exp_avg_sq;
       a.s = scalars;
-      ck(amsp::launch_fused_step(a, 1, e->sms * 2, 4, main), "local optimizer");
+      // the engine's single-rank choice: TMA (1 CTA / SM) when aligned, else LDG
+      const bool tma = e->variant == 5 || e->variant == 6;
+      ck(amsp::launch_fused_step(a, 1, tma ? e->sms : e->sms * 2, tma ? e->variant : 4, main),
+         "local optimizer");
       ++e->launches;
       return;
     }
     if (!with_comm) return;
     // Barrier semantics (overlap_sim.cpp:166-174): every gradient is reduced
     // on every rank before the remaining owners update and push.
-    const int full_grid = e->sms * amsp::fused_blocks_per_sm(e->world, 0);
+    const int full_grid =
+        resid_variant ? e->grid : e->sms * amsp::fused_blocks_per_sm(e->world, 0);
     barrier(end_a, main);
-    fused(resid, full_grid, main);
+    fused(resid, full_grid, main, resid_variant);
     adam_push(pending, e->sms * 2, main);
     barrier(end_b, main);
   }
@@ -510,6 +520,10 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
 
   s->gemm_mode = cfg->compute_mode == 1;
   s->gather_dma = cfg->gather_mode == 1;
+  s->gather_tma = cfg->gather_mode == 2;
+  if (cfg->gather_mode < 0 || cfg->gather_mode > 2) throw Error("sched: unknown gather_mode");
+  if (s->gather_tma && e->sp > 1 && !e->copies_aligned())
+    throw Error("sched: the TMA all-gather needs 8-element-aligned P slices");
   s->layers_k = K;
   std::uint64_t max_out = 0;
   std::vector<amsp::Seg> rsegs;
@@ -651,6 +665,14 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     else if (!updated[t]) pend.push_back(range_of(static_cast<int>(t)));
   }
   s->resid = owned_pieces(e->layout, rest, rsegs);
+  {
+    bool aligned = true;
+    for (int i = s->resid.begin; i < s->resid.begin + s->resid.nseg; ++i) {
+      const amsp::Seg& g = rsegs[static_cast<std::size_t>(i)];
+      if ((g.flat | g.os | g.dst | g.len) & 7u) aligned = false;
+    }
+    s->resid_variant = (aligned && (e->variant == 5 || e->variant == 6)) ? e->variant : 0;
+  }
   s->pending = owned_pieces(e->layout, pend, rsegs);
   s->end_a = next_barrier++;
   s->end_b = next_barrier++;

@@ -133,6 +133,13 @@ class Engine:
         N.check(N.lib().amsp_engine_tune(self._h, variant, grid))
         self.info = self._info()
 
+    def tune_gather(self, mode) -> None:
+        """All-gather implementation of engine.step / gather(): an SM-kernel
+        grid (int > 0), "sm" (default grid), "dma" (copy engines) or "tma"
+        (bulk-copy kernel)."""
+        grid = {"sm": 0, "dma": -1, "tma": -2}.get(mode, mode)
+        N.check(N.lib().amsp_engine_tune_gather(self._h, int(grid)))
+
     def time_kernel(self, enable: bool = True) -> None:
         N.check(N.lib().amsp_engine_time_kernel(self._h, int(enable)))
 
@@ -207,7 +214,7 @@ class Scheduler:
                          sim.head_fwd_time, sim.head_bwd_time)
         cfg = N.SchedConfig(m, cost._c(), sc, comm_ctas, compute_ctas, time_scale,
                             int(optimizer_overlap), {"standin": 0, "gemm": 1}[compute], tokens,
-                            gemm_sm_margin, {"sm": 0, "dma": 1}[gather])
+                            gemm_sm_margin, {"sm": 0, "dma": 1, "tma": 2}[gather])
         self.engine = engine
         self._h = C.c_void_p()
         N.check(N.lib().amsp_sched_create(engine._h, C.byref(cfg), profile._h, C.byref(self._h)))

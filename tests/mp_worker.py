@@ -28,9 +28,13 @@ def main():
     ap.add_argument("--layout", default="greedy")
     ap.add_argument("--p-mesh", default=None)
     ap.add_argument("--sched", action="store_true")
+    ap.add_argument("--gather", default="sm", choices=["sm", "tma", "dma"])
     ap.add_argument("--model", default="tiny")
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (5/6 = TMA)")
+    ap.add_argument("--host", action="store_true",
+                    help="amsp_engine_step_host: pinned host gradients, chunked H2D + per-chunk "
+                         "barrier + fused update")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
@@ -43,18 +47,24 @@ def main():
     p_mesh = mesh(args.p_mesh) if args.p_mesh else M(1, 1)
     g_mesh = p_mesh if p_mesh == os_mesh or args.p_mesh else M(1, 1)
     plan = S.ShardingPlan(p_mesh, g_mesh, os_mesh)
-    e = Engine(S.model(args.model), plan, dp, rank=rank, device=local, layout=args.layout,
+    # "chunky": three raw tensors (300M params) so the host-buffer step spans
+    # two 2^28-element upload chunks, with the chunk boundary inside a tensor.
+    model = [200_000_000, 100_000_008, 64] if args.model == "chunky" else S.model(args.model)
+    e = Engine(model, plan, dp, rank=rank, device=local, layout=args.layout,
                skip_gathers=args.sched)
     e.connect()
     if args.variant:
         e.tune(args.variant)
+    if plan.sp() > 1:
+        e.tune_gather(args.gather)
     e.init_state()
     sched = None
     if args.sched:  # overlap scheduler: real cross-GPU barriers per bucket / module
         from paper_2311_00257_b200.engine import Scheduler, b200_profile
         sched = Scheduler(e, S.model(args.model), b200_profile(),
                           S.CostConfig(bucket_size=1 << 20),
-                          S.SimConfig(overlap_tier="ag_rs_ar_bc", peak_flops_per_gpu=1e16))
+                          S.SimConfig(overlap_tier="ag_rs_ar_bc", peak_flops_per_gpu=1e16),
+                          gather=args.gather)
     for t in range(1, args.steps + 1):
         e.synth_grads(t)
         if sched:
@@ -62,6 +72,10 @@ def main():
             sched.step(t)
             torch.cuda.synchronize()
             dist.barrier()
+        elif args.host:
+            g = e.read("grads")  # this rank's step-t gradients, staged through host memory
+            host = torch.from_numpy(g.view(np.int16)).pin_memory()
+            e.step_host(t, host.data_ptr())
         else:
             e.step(t)
     if sched:
@@ -69,10 +83,12 @@ def main():
     torch.cuda.synchronize()
     phi = e.info.total_params
     segs, owned = e.segments()
-    idx = np.concatenate([np.arange(f, f + ln, dtype=np.uint64) for f, _, ln in segs])
-    want = O.trajectory(idx, DEFAULT_SEED, args.steps, world, O.hyper())
     ok = True
-    for name, ref in zip(("master", "exp_avg", "exp_avg_sq"), want[:3]):
+    # a rank may own no tensor (greedy layout, fewer tensors than ranks)
+    idx = np.concatenate([np.arange(f, f + ln, dtype=np.uint64) for f, _, ln in segs]
+                         or [np.empty(0, np.uint64)])
+    want = O.trajectory(idx, DEFAULT_SEED, args.steps, world, O.hyper()) if owned else [[]] * 3
+    for name, ref in zip(("master", "exp_avg", "exp_avg_sq") if owned else (), want[:3]):
         got = e.read(name)
         if not np.array_equal(got.view(np.uint32), ref.view(np.uint32)):
             print(f"RANK {rank} MISMATCH {name}: {int(np.sum(got != ref))}", flush=True)

@@ -210,8 +210,8 @@ def test_invalid_plans_fail_loudly(cuda):
                                                (4, 1, 4, "none"), (4, 1, 2, "ag_rs_ar"),
                                                (2, 2, 2, "ag_rs_ar_bc"), (4, 4, 4, "ag_rs"),
                                                (4, 2, 4, "ag_rs_ar_bc")])
-@pytest.mark.parametrize("opt_overlap", [True, False])
-def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap):
+@pytest.mark.parametrize("opt_overlap,gather", [(True, "sm"), (False, "sm"), (True, "tma")])
+def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap, gather):
     """The overlap scheduler replays the reference event graph (gradient
     buckets / module reduce-scatters / all-gathers on comm streams, compute
     stand-ins on the compute stream) and its split reduce -> AdamW + push
@@ -225,7 +225,7 @@ def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap):
     prof = b200_profile()
     cost = S.CostConfig(bucket_size=1 << 20)  # several buckets on the tiny model
     sim = S.SimConfig(overlap_tier=tier, peak_flops_per_gpu=1e18)
-    scheds = [Scheduler(e, model, prof, cost, sim, optimizer_overlap=opt_overlap)
+    scheds = [Scheduler(e, model, prof, cost, sim, optimizer_overlap=opt_overlap, gather=gather)
               for e in engines]
     info = scheds[0].info
     assert info.n_events > 0 and info.n_compute > 0
@@ -296,18 +296,23 @@ def test_scheduler_real_gemm_compute(cuda, world, p):
         e.close()
 
 
-@pytest.mark.parametrize("world,p,os_k,layout", [(2, 2, 2, "greedy"), (4, 4, 4, "greedy"),
-                                                 (4, 2, 4, "greedy"), (4, 2, 2, "greedy"),
-                                                 (4, 2, 4, "contiguous"), (8, 8, 8, "greedy")])
-def test_emulated_parameter_sharding_bit_exact(cuda, world, p, os_k, layout):
+@pytest.mark.parametrize("world,p,os_k,layout,gather", [
+    (2, 2, 2, "greedy", "sm"), (4, 4, 4, "greedy", "sm"), (4, 2, 4, "greedy", "sm"),
+    (4, 2, 2, "greedy", "sm"), (4, 2, 4, "contiguous", "sm"), (8, 8, 8, "greedy", "sm"),
+    (2, 2, 2, "greedy", "tma"), (4, 4, 4, "greedy", "tma"), (8, 8, 8, "greedy", "tma"),
+    (4, 2, 4, "greedy", "dma")])
+def test_emulated_parameter_sharding_bit_exact(cuda, world, p, os_k, layout, gather):
     """s_p > 1 (ZeRO-3 / AMSP-13B-style): intra-tensor P shards, forward and
     backward all-gathers inside the step, RS fused into the optimizer kernel;
-    P shards, OS shards and gathered units checked against the oracle."""
+    P shards, OS shards and gathered units checked against the oracle. The
+    all-gathers run as the SM kernel, the TMA bulk-copy kernel or copy-engine
+    DMAs."""
     model = S.model("tiny")
     plan = S.ShardingPlan(M(p, 1), M(p, 1) if os_k == p else M(os_k, 1), M(os_k, 1))
     engines = [Engine(model, plan, M(world, 1), rank=r, layout=layout) for r in range(world)]
     link_local(engines)
     for e in engines:
+        e.tune_gather(gather)
         e.init_state()
     steps = 3
     for t in range(1, steps + 1):

@@ -29,14 +29,21 @@ CASES = [c + (0,) for c in CASES] + [
     # variant 6 = the deeper 1-CTA/SM ring, 1 / 2 = the LDG kernels
     (2, "2x1", None, "greedy", None, 6), (4, "4x1", None, "greedy", None, 6),
     (2, "2x1", None, "greedy", None, 2), (4, "4x1", None, "greedy", None, 1),
-    (4, "2x1", None, "greedy", None, 2)]
+    (4, "2x1", None, "greedy", None, 2),
+    # host-buffer step: chunked H2D pipelined with per-chunk barriers
+    (2, "2x1", None, "greedy", "host", 0), (4, "4x1", None, "greedy", "host", 0),
+    (4, "2x1", None, "greedy", "host", 0),
+    # ZeRO-3 all-gathers by the TMA bulk-copy kernel, in the step and in the scheduler
+    (4, "4x1", None, "greedy", "4x1+tma", 0), (4, "4x1", None, "greedy", "4x1+sched+tma", 0)]
 
 
 @pytest.mark.parametrize("world,os_mesh,dp_mesh,layout,p_mesh,variant", CASES)
 def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh, variant):
-    sched = p_mesh is not None and "sched" in p_mesh
-    if sched:
-        p_mesh = p_mesh.split("+")[0] if "+" in p_mesh else None
+    # p_mesh: "[AxB][+sched][+tma]" or "sched" / "host"
+    words = (p_mesh or "").split("+")
+    host, sched, tma = "host" in words, "sched" in words, "tma" in words
+    meshes = [w for w in words if "x" in w]
+    p_mesh = meshes[0] if meshes else None
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
@@ -50,6 +57,10 @@ def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh, variant):
         cmd += ["--sched"]
     if variant:
         cmd += ["--variant", str(variant)]
+    if host:
+        cmd += ["--host", "--model", "chunky", "--steps", "2"]
+    if tma:
+        cmd += ["--gather", "tma"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=REPO,
                        env={**os.environ, "OMP_NUM_THREADS": "4"})
     out = r.stdout + r.stderr
