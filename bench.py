@@ -71,8 +71,9 @@ def parse():
     ap.add_argument("--gather", default="dma", choices=["dma", "sm", "tma"],
                     help="overlapped all-gathers on copy engines (dma), the SM kernel or the "
                          "TMA bulk-copy kernel")
-    ap.add_argument("--step-gather", default="sm", choices=["sm", "dma", "tma"],
-                    help="all-gather implementation inside the pipeline-only step (s_p > 1)")
+    ap.add_argument("--step-gather", default="auto", choices=["auto", "sm", "dma", "tma"],
+                    help="all-gather implementation inside the pipeline-only step (s_p > 1); "
+                         "auto = the engine's default (TMA when the P slices are aligned)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -374,7 +375,7 @@ def run_ours(args):
     eng.connect()
     if args.variant or args.grid:
         eng.tune(args.variant, args.grid)
-    if args.step_gather != "sm":
+    if args.step_gather != "auto":
         eng.tune_gather(args.step_gather)
     info = eng.info
     stream = torch.cuda.Stream(device=local)
@@ -439,7 +440,8 @@ def run_ours(args):
     kname = "fused_step_tma_kernel" if info.variant in (5, 6) else "fused_step_kernel"
     scope = (f"{kname} (reduce + AdamW + gather), variant {info.variant}" if info.sp == 1 else
              "whole step: 2 all-gather passes (" +
-             {"sm": "gather_kernel", "dma": "copy engines", "tma": "gather_tma_kernel"}[args.step_gather] +
+             {"sm": "gather_kernel", "dma": "copy engines", "tma": "gather_tma_kernel",
+              "auto": "engine default: gather_tma_kernel when aligned"}[args.step_gather] +
              ") + fused reduce/AdamW + barriers")
     hbm_ach = hbm_b / (t_meas * 1e-3) / 1e9
     nvl_ach = nvl_b / (t_meas * 1e-3) / 1e9

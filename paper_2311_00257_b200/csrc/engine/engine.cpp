@@ -121,6 +121,11 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   plan_groups(e.get(), dp, plan);
   std::vector<amsp::CopySeg> copy;
   plan_units(e.get(), copy);
+  // In-step all-gathers default to the TMA bulk-copy kernel when every P
+  // slice is 8-element aligned: 640 vs 608 GB/s ingress for the SM kernel
+  // and 357 for the copy engines on 13B ZeRO-3 at W = 4
+  // (profiles/r01_tune_gather_tma.jsonl).
+  if (e->sp > 1 && e->copies_aligned()) e->gather_grid = amsp_engine::kGatherTma;
 
   e->use_device();
   ck(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "stream");
