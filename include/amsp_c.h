@@ -396,6 +396,18 @@ int amsp_k_adamw(const void* grad, int grad_is_bf16, float* master, float* m,
 int amsp_k_upcast_scale(const void* src_bf16, float* dst, uint64_t n, float scale,
                         void* stream);
 
+/* Reduce-scatter epilogue (north-star item 1) over plain pointers:
+ * dst[k] = (sum_{r<nsrc} bf16 srcs[r][offset+k]) * scale in fixed rank order
+ * (the fused kernel's rounding sequence). srcs may be cudaIpc peer pointers
+ * (the RS pull) or local buffers; 1 <= nsrc <= 8. */
+int amsp_k_rs_upcast_scale(const void* const* srcs_bf16, int nsrc, uint64_t offset,
+                           float* dst, uint64_t n, float scale, void* stream);
+/* All-gather epilogue (north-star item 3): bf16(src[k]) stored into
+ * dsts[d][dst_offset + k] for every destination d < ndst (local or peer
+ * parameter buffers); 1 <= ndst <= 8. */
+int amsp_k_ag_downcast(const float* src, uint64_t n, void* const* dsts_bf16, int ndst,
+                       uint64_t dst_offset, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -204,6 +204,8 @@ SIGNATURES = {
                                C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                vp]),
     "amsp_k_upcast_scale": (C.c_int, [vp, vp, u64, C.c_float, vp]),
+    "amsp_k_rs_upcast_scale": (C.c_int, [P(vp), C.c_int, u64, vp, u64, C.c_float, vp]),
+    "amsp_k_ag_downcast": (C.c_int, [vp, u64, P(vp), C.c_int, u64, vp]),
 }
 
 _lib: C.CDLL | None = None

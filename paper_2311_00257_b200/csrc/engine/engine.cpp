@@ -534,4 +534,26 @@ int amsp_k_upcast_scale(const void* src_bf16, float* dst, uint64_t n, float scal
   });
 }
 
+int amsp_k_rs_upcast_scale(const void* const* srcs_bf16, int nsrc, uint64_t offset,
+                           float* dst, uint64_t n, float scale, void* stream) {
+  return amsp::guarded([&] {
+    if (!srcs_bf16 || (n && !dst)) throw Error("rs_upcast_scale: null argument");
+    if (nsrc < 1 || nsrc > amsp::kMaxRanks) throw Error("rs_upcast_scale: 1..8 sources");
+    ck(amsp::launch_rs_upcast_scale(reinterpret_cast<const uint16_t* const*>(srcs_bf16), nsrc,
+                                    offset, dst, n, scale, static_cast<cudaStream_t>(stream)),
+       "rs_upcast_scale");
+  });
+}
+
+int amsp_k_ag_downcast(const float* src, uint64_t n, void* const* dsts_bf16, int ndst,
+                       uint64_t dst_offset, void* stream) {
+  return amsp::guarded([&] {
+    if (!dsts_bf16 || (n && !src)) throw Error("ag_downcast: null argument");
+    if (ndst < 1 || ndst > amsp::kMaxRanks) throw Error("ag_downcast: 1..8 destinations");
+    ck(amsp::launch_ag_downcast(src, n, reinterpret_cast<uint16_t* const*>(dsts_bf16), ndst,
+                                dst_offset, static_cast<cudaStream_t>(stream)),
+       "ag_downcast");
+  });
+}
+
 }  // extern "C"

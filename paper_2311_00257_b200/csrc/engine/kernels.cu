@@ -390,6 +390,43 @@ __global__ void upcast_scale_kernel(const uint16_t* __restrict__ src, float* __r
     dst[i] = __fmul_rn(bf16_at(src[i]), scale);
 }
 
+// Raw reduce-scatter epilogue over plain pointers (amsp_k_rs_upcast_scale):
+// dst[k] = (sum_r bf16 srcs[r][offset + k]) * scale, fixed rank order, the
+// same rounding sequence as the fused kernel. srcs may be peer pointers.
+struct RsArgs {
+  const uint16_t* srcs[kMaxRanks];
+  int nsrc;
+  unsigned long long offset, n;
+  float* dst;
+  float scale;
+};
+
+__global__ void rs_upcast_scale_kernel(const RsArgs a) {
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  for (unsigned long long k = blockIdx.x * blockDim.x + threadIdx.x; k < a.n; k += stride) {
+    float g = bf16_at(a.srcs[0][a.offset + k]);
+    for (int r = 1; r < a.nsrc; ++r) g = __fadd_rn(g, bf16_at(a.srcs[r][a.offset + k]));
+    a.dst[k] = __fmul_rn(g, a.scale);
+  }
+}
+
+// Raw all-gather epilogue (amsp_k_ag_downcast): bf16(src[k]) stored into
+// dsts[d][dst_offset + k] for every destination (local or peer pointers).
+struct AgArgs {
+  uint16_t* dsts[kMaxRanks];
+  int ndst;
+  unsigned long long dst_offset, n;
+  const float* src;
+};
+
+__global__ void ag_downcast_kernel(const AgArgs a) {
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  for (unsigned long long k = blockIdx.x * blockDim.x + threadIdx.x; k < a.n; k += stride) {
+    const uint16_t b = to_bf16(a.src[k]);
+    for (int d = 0; d < a.ndst; ++d) a.dsts[d][a.dst_offset + k] = b;
+  }
+}
+
 // Reduce half of the split step: red[os] = (sum_r grads_r[flat]) * scale,
 // fixed rank order (bit-equal to the fused kernel's sum).
 template <int W>
@@ -965,6 +1002,36 @@ cudaError_t launch_adamw_flat(const void* grad, bool bf16_grad, float* master, f
     adamw_flat_kernel<true><<<grid, 256, 0, stream>>>(grad, master, m, v, param_out, n, s);
   else
     adamw_flat_kernel<false><<<grid, 256, 0, stream>>>(grad, master, m, v, param_out, n, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_upcast_scale(const uint16_t* const* srcs, int nsrc,
+                                   unsigned long long offset, float* dst,
+                                   unsigned long long n, float scale, cudaStream_t stream) {
+  if (nsrc < 1 || nsrc > kMaxRanks) return cudaErrorInvalidValue;
+  if (n == 0) return cudaSuccess;
+  RsArgs a{};
+  for (int r = 0; r < nsrc; ++r) a.srcs[r] = srcs[r];
+  a.nsrc = nsrc;
+  a.offset = offset;
+  a.n = n;
+  a.dst = dst;
+  a.scale = scale;
+  rs_upcast_scale_kernel<<<sm_count() * 8, 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ag_downcast(const float* src, unsigned long long n, uint16_t* const* dsts,
+                               int ndst, unsigned long long dst_offset, cudaStream_t stream) {
+  if (ndst < 1 || ndst > kMaxRanks) return cudaErrorInvalidValue;
+  if (n == 0) return cudaSuccess;
+  AgArgs a{};
+  for (int d = 0; d < ndst; ++d) a.dsts[d] = dsts[d];
+  a.ndst = ndst;
+  a.dst_offset = dst_offset;
+  a.n = n;
+  a.src = src;
+  ag_downcast_kernel<<<sm_count() * 8, 256, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

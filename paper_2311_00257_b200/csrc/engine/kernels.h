@@ -123,6 +123,11 @@ cudaError_t launch_adamw_flat(const void* grad, bool bf16_grad, float* master,
                               float* m, float* v, uint16_t* param_out,
                               unsigned long long n, const AdamScalars& s,
                               cudaStream_t stream);
+cudaError_t launch_rs_upcast_scale(const uint16_t* const* srcs, int nsrc,
+                                   unsigned long long offset, float* dst,
+                                   unsigned long long n, float scale, cudaStream_t stream);
+cudaError_t launch_ag_downcast(const float* src, unsigned long long n, uint16_t* const* dsts,
+                               int ndst, unsigned long long dst_offset, cudaStream_t stream);
 cudaError_t launch_upcast_scale(const uint16_t* src, float* dst,
                                 unsigned long long n, float scale,
                                 cudaStream_t stream);
