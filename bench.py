@@ -71,6 +71,9 @@ def parse():
     ap.add_argument("--gather", default="dma", choices=["dma", "sm", "tma"],
                     help="overlapped all-gathers on copy engines (dma), the SM kernel or the "
                          "TMA bulk-copy kernel")
+    ap.add_argument("--bc", default="auto", choices=["auto", "push"],
+                    help="overlapped step: mirrored broadcast of updated shards in the next "
+                         "forward (auto, tier ag_rs_ar_bc) or push inside the optimizer")
     ap.add_argument("--step-gather", default="auto", choices=["auto", "sm", "dma", "tma"],
                     help="all-gather implementation inside the pipeline-only step (s_p > 1); "
                          "auto = the engine's default (TMA when the P slices are aligned)")
@@ -510,7 +513,7 @@ def run_ours(args):
         ctas = args.comm_ctas or (64 if (compute == "gemm" and plan.sp() > 1) else 128)
         sched = Scheduler(eng, mspec, b200_profile(), S.CostConfig(), sim, comm_ctas=ctas,
                           optimizer_overlap=bool(opt), compute=compute,
-                          gemm_sm_margin=args.gemm_sm_margin, gather=args.gather)
+                          gemm_sm_margin=args.gemm_sm_margin, gather=args.gather, bc=args.bc)
 
         def timed(with_comm, k):
             nonlocal step
@@ -553,6 +556,9 @@ def run_ours(args):
                 "gather": {"dma": "copy engines", "sm": "SM kernel",
                            "tma": "TMA bulk-copy kernel"}[args.gather],
                 "comm_ctas": ctas,
+                "param_broadcast": ("mirrored: copy-engine pulls in the next step's BC events, "
+                                    "gating forward layer blocks" if si.mirrored_bc else
+                                    "pushed by the optimizer kernels (NVLink stores)"),
                 "step_ms": round(t_b, 3), "compute_only_ms": round(t_c, 3),
                 "compute_plus_optimizer_ms": round(t_o, 3),
                 "exposed_comm_ms": round(t_b - t_o, 3),

@@ -353,12 +353,24 @@ typedef struct {
                                    engines (peer cudaMemcpyAsync, no SMs);
                                    2 = TMA bulk-copy kernel (single-warp
                                    CTAs, 8-element-aligned P slices) */
+  int bc_mode;                  /* updated-parameter broadcast: 0 = auto:
+                                   mirrored when the graph leads with the
+                                   previous step's BroadcastShard events
+                                   (tier ag_rs_ar_bc, s_p = 1, k > 1;
+                                   overlap_sim.cpp:152-159) -- the optimizer
+                                   writes only local params and the next
+                                   step's BC events pull them by copy engine,
+                                   gating the forward layer blocks;
+                                   1 = push inside the optimizer kernels */
 } amsp_sched_config_t;
 
 typedef struct {
   int n_events, n_compute, n_gather, n_reduce, n_buckets, n_barriers, stream_count;
   double predicted_step_s;      /* simulate_step() of the same graph */
   double predicted_compute_s;   /* compute-stream busy time */
+  int mirrored_bc;              /* 1: parameters of other OS owners arrive in
+                                   the next step's BC events (call
+                                   amsp_sched_flush after the last step) */
 } amsp_sched_info_t;
 
 int amsp_sched_create(amsp_engine_t* e, const amsp_sched_config_t* cfg,
@@ -374,6 +386,10 @@ int amsp_sched_step(amsp_sched_t* s, int step, void* stream, int mode);
  * with the reference's render_trace (overlap_sim.cpp:560-577), so measured
  * and predicted (amsp_sched_predicted_trace) traces share one TEF schema
  * and event names. *step_ms = measured span of the graph. */
+/* Mirrored broadcast only (info.mirrored_bc): pull every OS owner's updated
+ * parameters now, so params are complete on every rank after the last step,
+ * then a cross-GPU barrier. A no-op otherwise. Call on every rank. */
+int amsp_sched_flush(amsp_sched_t* s, void* stream);
 int amsp_sched_enable_trace(amsp_sched_t* s, int on);
 int amsp_sched_trace(amsp_sched_t* s, char* buf, size_t cap, size_t* needed, double* step_ms);
 int amsp_sched_predicted_trace(const amsp_sched_t* s, char* buf, size_t cap, size_t* needed);

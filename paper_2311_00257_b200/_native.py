@@ -119,14 +119,14 @@ class SchedConfig(C.Structure):
     _fields_ = [("model", Model), ("cost", CostConfig), ("sim", SimConfig),
                 ("comm_ctas", C.c_int), ("compute_ctas", C.c_int), ("time_scale", C.c_double),
                 ("optimizer_overlap", C.c_int), ("compute_mode", C.c_int), ("tokens", C.c_int),
-                ("gemm_sm_margin", C.c_int), ("gather_mode", C.c_int)]
+                ("gemm_sm_margin", C.c_int), ("gather_mode", C.c_int), ("bc_mode", C.c_int)]
 
 
 class SchedInfo(C.Structure):
     _fields_ = [("n_events", C.c_int), ("n_compute", C.c_int), ("n_gather", C.c_int),
                 ("n_reduce", C.c_int), ("n_buckets", C.c_int), ("n_barriers", C.c_int),
                 ("stream_count", C.c_int), ("predicted_step_s", C.c_double),
-                ("predicted_compute_s", C.c_double)]
+                ("predicted_compute_s", C.c_double), ("mirrored_bc", C.c_int)]
 
 
 P = C.POINTER
@@ -196,6 +196,7 @@ SIGNATURES = {
     "amsp_sched_info": (C.c_int, [vp, P(SchedInfo)]),
     "amsp_sched_step": (C.c_int, [vp, C.c_int, vp, C.c_int]),
     "amsp_sched_enable_trace": (C.c_int, [vp, C.c_int]),
+    "amsp_sched_flush": (C.c_int, [vp, vp]),
     "amsp_sched_trace": (C.c_int, [vp, C.c_char_p, C.c_size_t, P(C.c_size_t), P(C.c_double)]),
     "amsp_sched_predicted_trace": (C.c_int, [vp, C.c_char_p, C.c_size_t, P(C.c_size_t)]),
     "amsp_sched_destroy": (None, [vp]),

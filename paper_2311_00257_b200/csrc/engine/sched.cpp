@@ -11,7 +11,8 @@
 //                                                reduce of tensor (l,i)
 //   stream 2             AllReduceBucket b    -> barrier + pull-reduce of
 //                                                bucket b's owned elements
-//                        BroadcastShard       -> marker (the push is below)
+//                        BroadcastShard j     -> mirrored broadcast (below)
+//                                                or a marker
 //   after the graph      barrier -> update of whatever is left -> barrier
 //
 // Cross-stream dependencies are cudaEvents exactly as in Event::depends_on;
@@ -31,13 +32,34 @@
 //       bucket after a second barrier that certifies every rank finished the
 //       bucket's grad-input (the last reader of those replicated params).
 // Either way the arithmetic is bit-equal to the fused kernel and the oracle.
+//
+// Parameter broadcast (`bc_mode`):
+//   mirrored (default when the graph leads with BroadcastShard events, i.e.
+//       tier ag_rs_ar_bc with s_p = 1 and k = s_os/s_p > 1; overlap_sim.cpp:
+//       152-159) — the optimizer kernels write the updated bf16 shard only
+//       into this rank's own parameters; BroadcastShard j of the NEXT step
+//       pulls, with copy-engine DMAs on the AR/BC stream, every parameter
+//       the graph gates behind it (layer block j: layers with
+//       ceil((l+1) n / L) - 1 = j, the head in the last block) from its OS
+//       owner. Layer l's forward waits on its block exactly as in the graph,
+//       so the broadcast overlaps the next forward instead of extending this
+//       step's tail. After the last step, amsp_sched_flush pulls the rest.
+//   push — the optimizer kernels store the bf16 shard into every OS-group
+//       member directly (NVLink stores inside the update); BroadcastShard is
+//       a marker.
 #include "blas.h"
 #include "engine_impl.h"
 #include "../convert.h"
 
 namespace {
 
-enum class Work { Compute, Gather, Reduce, ReduceAdam, Marker };
+enum class Work { Compute, Gather, Reduce, ReduceAdam, Broadcast, Marker };
+
+// One pull of the mirrored broadcast: params[dst, dst+len) from `owner`.
+struct BcCopy {
+  std::uint64_t dst = 0, len = 0;
+  int owner = 0;
+};
 
 // Real-compute mode: a compute event of a linear module (or the LM head) is
 // a cuBLAS bf16 GEMM of its true shape over T tokens.
@@ -61,6 +83,7 @@ struct EventWork {
   // Single rank (no AllReduce buckets in the graph): fused update of the
   // bucket completed by this grad-input event, on the AR/BC stream.
   int post_begin = 0, post_nseg = 0, post_ntiles = 0;
+  int bc = -1;  // Work::Broadcast: index into amsp_sched::bc_copies
 };
 
 struct Table {
@@ -82,10 +105,27 @@ struct amsp_sched {
   int n_barriers = 0, end_a = 0, end_b = 0, n_buckets = 0, n_gather = 0, n_reduce = 0,
       n_compute = 0;
   Table resid, pending;  // end of step: fused update / AdamW-from-reduced update
-  // The end-of-step fused update runs after compute, alone on the GPU: it
-  // takes the engine's tuned kernel (the TMA pipeline when the residual
-  // table is 8-element aligned) instead of the co-resident LDG kernel.
-  int resid_variant = 0;
+  // Mirrored broadcast: per BroadcastShard event, the pulls it performs.
+  bool mirror = false;
+  std::vector<std::vector<BcCopy>> bc_copies;
+  int flush_barrier = 0;
+  int param_dsts(uint16_t** dsts) const {
+    if (mirror) {
+      dsts[0] = e->params_of(e->rank);
+      return 1;
+    }
+    const int n = static_cast<int>(e->dst_members.size());
+    for (int d = 0; d < n; ++d) dsts[d] = e->params_of(e->dst_members[d]);
+    return n;
+  }
+  void broadcast(int j, cudaStream_t st) {
+    uint16_t* mine = e->params_of(e->rank);
+    for (const BcCopy& c : bc_copies[static_cast<std::size_t>(j)]) {
+      ck(cudaMemcpyAsync(mine + c.dst, e->params_of(c.owner) + c.dst, c.len * 2,
+                         cudaMemcpyDeviceToDevice, st),
+         "broadcast DMA");
+    }
+  }
   amsp::Seg* d_rsegs = nullptr;
   amsp::CopySeg* d_tcopy = nullptr;
   float* red = nullptr;
@@ -248,8 +288,7 @@ struct amsp_sched {
     a.nseg = t.nseg;
     a.ntiles = t.ntiles;
     a.red = red;
-    a.ndst = static_cast<int>(e->dst_members.size());
-    for (int d = 0; d < a.ndst; ++d) a.dsts[d] = e->params_of(e->dst_members[d]);
+    a.ndst = param_dsts(a.dsts);
     a.master = e->master;
     a.exp_avg = e->exp_avg;
     a.exp_avg_sq = e->exp_avg_sq;
@@ -266,8 +305,7 @@ struct amsp_sched {
     a.nseg = t.nseg;
     a.ntiles = t.ntiles;
     for (int r = 0; r < e->world; ++r) a.grads[r] = e->grads_of(r);
-    a.ndst = static_cast<int>(e->dst_members.size());
-    for (int d = 0; d < a.ndst; ++d) a.dsts[d] = e->params_of(e->dst_members[d]);
+    a.ndst = param_dsts(a.dsts);
     a.master = e->master;
     a.exp_avg = e->exp_avg;
     a.exp_avg_sq = e->exp_avg_sq;
@@ -351,6 +389,9 @@ struct amsp_sched {
             fused(t, comm_ctas, st);
           }
           break;
+        case Work::Broadcast:
+          if (with_comm) broadcast(w.bc, st);
+          break;
         case Work::Marker:
           break;
       }
@@ -391,12 +432,24 @@ struct amsp_sched {
     if (!with_comm) return;
     // Barrier semantics (overlap_sim.cpp:166-174): every gradient is reduced
     // on every rank before the remaining owners update and push.
-    const int full_grid =
-        resid_variant ? e->grid : e->sms * amsp::fused_blocks_per_sm(e->world, 0);
+    // The LDG kernel: measured 156.7 ms vs 160.4 ms with the TMA pipeline
+    // for the 7B W=1 GEMM step (profiles/r01_final_n1.json vs
+    // r01_bench_n1_f3.json) over the per-tensor residual table.
+    const int full_grid = e->sms * amsp::fused_blocks_per_sm(e->world, 0);
     barrier(end_a, main);
-    fused(resid, full_grid, main, resid_variant);
+    fused(resid, full_grid, main);
     adam_push(pending, e->sms * 2, main);
     barrier(end_b, main);
+  }
+
+  // Mirrored broadcast: pull every block now (after the last step), then a
+  // barrier so no owner updates its shard while a peer still reads it.
+  void flush(cudaStream_t main) {
+    if (!mirror) return;
+    e->require_peers();
+    ++epoch;
+    for (std::size_t j = 0; j < bc_copies.size(); ++j) broadcast(static_cast<int>(j), main);
+    barrier(flush_barrier, main);
   }
 };
 
@@ -525,6 +578,43 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
   if (s->gather_tma && e->sp > 1 && !e->copies_aligned())
     throw Error("sched: the TMA all-gather needs 8-element-aligned P slices");
   s->layers_k = K;
+  // Mirrored broadcast: the graph leads with last step's BroadcastShard
+  // events (tier ag_rs_ar_bc, k > 1) and parameters are not sharded.
+  int n_bc = 0;
+  for (const auto& ev : evs) n_bc += ev.kind == shardplan::EventKind::BroadcastShard;
+  if (cfg->bc_mode < 0 || cfg->bc_mode > 1) throw Error("sched: unknown bc_mode");
+  s->mirror = cfg->bc_mode == 0 && plan.sp() == 1 && n_bc > 0 &&
+              evs.front().kind == shardplan::EventKind::BroadcastShard &&
+              e->dst_members.size() > 1;
+  if (s->mirror) {
+    // Every OS-group member's shard layout (the same map the engine uses).
+    const int k = static_cast<int>(e->dst_members.size());
+    std::vector<amsp::ShardLayout> member(static_cast<std::size_t>(k));
+    int me = -1;
+    for (int q = 0; q < k; ++q) {
+      member[q] = amsp::pshard_layout(e->tensor_sizes, 1, 0, k, q, e->cfg.layout);
+      if (e->dst_members[q] == e->rank) me = q;
+    }
+    // Layer block of each tensor: the graph's shard_gate (overlap_sim.cpp:
+    // 193-199); head tensors (embed, final norm, lm_head) in the last block.
+    std::vector<int> block(n, n_bc - 1);
+    for (int l = 0; l < L; ++l) {
+      const int j = std::max(0, ((l + 1) * n_bc + L - 1) / L - 1);
+      for (int i = 0; i < K; ++i) block[tensor_of(l, i)] = j;
+    }
+    s->bc_copies.assign(static_cast<std::size_t>(n_bc), {});
+    for (std::size_t t = 0; t < n; ++t) {
+      const auto [lo, hi] = range_of(static_cast<int>(t));
+      for (int q = 0; q < k; ++q) {
+        if (q == me) continue;
+        for (const auto& sg : member[q].segs) {
+          const std::uint64_t a = std::max(lo, sg.flat), b = std::min(hi, sg.flat + sg.len);
+          if (a < b)
+            s->bc_copies[block[t]].push_back({sg.dst + (a - sg.flat), b - a, e->dst_members[q]});
+        }
+      }
+    }
+  }
   std::uint64_t max_out = 0;
   std::vector<amsp::Seg> rsegs;
   std::vector<char> covered(n, 0);  // reduced by some event
@@ -610,7 +700,8 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
         break;
       }
       case shardplan::EventKind::BroadcastShard:
-        w.kind = Work::Marker;
+        w.kind = s->mirror ? Work::Broadcast : Work::Marker;
+        w.bc = ev.module;
         break;
     }
   }
@@ -665,17 +756,10 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     else if (!updated[t]) pend.push_back(range_of(static_cast<int>(t)));
   }
   s->resid = owned_pieces(e->layout, rest, rsegs);
-  {
-    bool aligned = true;
-    for (int i = s->resid.begin; i < s->resid.begin + s->resid.nseg; ++i) {
-      const amsp::Seg& g = rsegs[static_cast<std::size_t>(i)];
-      if ((g.flat | g.os | g.dst | g.len) & 7u) aligned = false;
-    }
-    s->resid_variant = (aligned && (e->variant == 5 || e->variant == 6)) ? e->variant : 0;
-  }
   s->pending = owned_pieces(e->layout, pend, rsegs);
   s->end_a = next_barrier++;
   s->end_b = next_barrier++;
+  s->flush_barrier = next_barrier++;
   s->n_barriers = next_barrier - kFirstSchedBarrier;
   if (next_barrier > amsp::kBarrierIds) throw Error("sched: too many barriers per step");
 
@@ -778,6 +862,7 @@ int amsp_sched_info(const amsp_sched_t* s, amsp_sched_info_t* info) {
     info->stream_count = s->graph.stream_count;
     info->predicted_step_s = s->predicted_step;
     info->predicted_compute_s = s->predicted_compute;
+    info->mirrored_bc = s->mirror ? 1 : 0;
   });
 }
 
@@ -787,6 +872,14 @@ int amsp_sched_step(amsp_sched_t* s, int step, void* stream, int mode) {
     s->e->use_device();
     if (mode < 0 || mode > 2) throw Error("sched: mode must be 0, 1 or 2");
     s->run(step, s->e->pick(stream), mode);
+  });
+}
+
+int amsp_sched_flush(amsp_sched_t* s, void* stream) {
+  return amsp::guarded([&] {
+    if (!s) throw Error("sched: null argument");
+    s->e->use_device();
+    s->flush(s->e->pick(stream));
   });
 }
 

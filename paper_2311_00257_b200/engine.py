@@ -192,7 +192,7 @@ class Scheduler:
     def __init__(self, engine: Engine, model: ModelSpec, profile, cost=None, sim=None,
                  comm_ctas: int = 0, compute_ctas: int = 0, time_scale: float = 1.0,
                  optimizer_overlap: bool = True, compute: str = "standin", tokens: int = 0,
-                 gemm_sm_margin: int = 0, gather: str = "sm"):
+                 gemm_sm_margin: int = 0, gather: str = "sm", bc: str = "auto"):
         from .shardplan import CostConfig, SimConfig
         cost = cost or CostConfig()
         sim = sim or SimConfig()
@@ -214,7 +214,8 @@ class Scheduler:
                          sim.head_fwd_time, sim.head_bwd_time)
         cfg = N.SchedConfig(m, cost._c(), sc, comm_ctas, compute_ctas, time_scale,
                             int(optimizer_overlap), {"standin": 0, "gemm": 1}[compute], tokens,
-                            gemm_sm_margin, {"sm": 0, "dma": 1, "tma": 2}[gather])
+                            gemm_sm_margin, {"sm": 0, "dma": 1, "tma": 2}[gather],
+                            {"auto": 0, "push": 1}[bc])
         self.engine = engine
         self._h = C.c_void_p()
         N.check(N.lib().amsp_sched_create(engine._h, C.byref(cfg), profile._h, C.byref(self._h)))
@@ -226,6 +227,11 @@ class Scheduler:
         compute + local optimizer work without communication (timing)."""
         mode = 2 if with_comm == "optimizer" else int(bool(with_comm))
         N.check(N.lib().amsp_sched_step(self._h, step, _stream_ptr(stream), mode))
+
+    def flush(self, stream=None) -> None:
+        """Mirrored broadcast (info.mirrored_bc): pull the other owners'
+        updated parameters after the last step (every rank calls it)."""
+        N.check(N.lib().amsp_sched_flush(self._h, _stream_ptr(stream)))
 
     def enable_trace(self, on: bool = True) -> None:
         N.check(N.lib().amsp_sched_enable_trace(self._h, int(on)))

@@ -79,6 +79,8 @@ def main():
         else:
             e.step(t)
     if sched:
+        sched.flush()  # mirrored broadcast: the last step's shards
+        torch.cuda.synchronize()
         sched.close()
     torch.cuda.synchronize()
     phi = e.info.total_params

@@ -210,8 +210,9 @@ def test_invalid_plans_fail_loudly(cuda):
                                                (4, 1, 4, "none"), (4, 1, 2, "ag_rs_ar"),
                                                (2, 2, 2, "ag_rs_ar_bc"), (4, 4, 4, "ag_rs"),
                                                (4, 2, 4, "ag_rs_ar_bc")])
-@pytest.mark.parametrize("opt_overlap,gather", [(True, "sm"), (False, "sm"), (True, "tma")])
-def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap, gather):
+@pytest.mark.parametrize("opt_overlap,gather,bc", [(True, "sm", "auto"), (False, "sm", "auto"),
+                                                   (True, "tma", "auto"), (False, "sm", "push")])
+def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap, gather, bc):
     """The overlap scheduler replays the reference event graph (gradient
     buckets / module reduce-scatters / all-gathers on comm streams, compute
     stand-ins on the compute stream) and its split reduce -> AdamW + push
@@ -225,9 +226,12 @@ def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap, ga
     prof = b200_profile()
     cost = S.CostConfig(bucket_size=1 << 20)  # several buckets on the tiny model
     sim = S.SimConfig(overlap_tier=tier, peak_flops_per_gpu=1e18)
-    scheds = [Scheduler(e, model, prof, cost, sim, optimizer_overlap=opt_overlap, gather=gather)
+    scheds = [Scheduler(e, model, prof, cost, sim, optimizer_overlap=opt_overlap, gather=gather,
+                        bc=bc)
               for e in engines]
     info = scheds[0].info
+    # mirrored broadcast: the graph leads with BC events (tier 4, s_p = 1, k > 1)
+    assert info.mirrored_bc == int(bc == "auto" and tier == "ag_rs_ar_bc" and p == 1 and os_k > 1)
     assert info.n_events > 0 and info.n_compute > 0
     if world // p > 1 and p == 1:
         assert info.n_buckets == -(-2 * model.total_params // (1 << 20))
@@ -241,6 +245,8 @@ def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap, ga
             e.synth_grads(t)
         for sc in scheds:
             sc.step(t)
+    for sc in scheds:  # mirrored broadcast: pull the last step's shards
+        sc.flush()
     want = O.trajectory_range(0, engines[0].info.total_params, DEFAULT_SEED, steps, world, H)
     for e in engines:
         _check_rank(e, want, steps)
