@@ -55,10 +55,12 @@ namespace {
 
 enum class Work { Compute, Gather, Reduce, ReduceAdam, Broadcast, Marker };
 
-// One pull of the mirrored broadcast: params[dst, dst+len) from `owner`.
+// One pull of the mirrored broadcast: params[dst, dst+len) from `owner`,
+// part of layer `layer` (the head tensors: layer = L).
 struct BcCopy {
   std::uint64_t dst = 0, len = 0;
   int owner = 0;
+  int layer = 0;
 };
 
 // Real-compute mode: a compute event of a linear module (or the LM head) is
@@ -107,7 +109,8 @@ struct amsp_sched {
   Table resid, pending;  // end of step: fused update / AdamW-from-reduced update
   // Mirrored broadcast: per BroadcastShard event, the pulls it performs.
   bool mirror = false;
-  std::vector<std::vector<BcCopy>> bc_copies;
+  std::vector<std::vector<BcCopy>> bc_copies;  // per BC event, in layer order
+  std::vector<cudaEvent_t> layer_ev;          // per layer (+ head): pulls landed
   int flush_barrier = 0;
   int param_dsts(uint16_t** dsts) const {
     if (mirror) {
@@ -118,12 +121,19 @@ struct amsp_sched {
     for (int d = 0; d < n; ++d) dsts[d] = e->params_of(e->dst_members[d]);
     return n;
   }
+  // BC event j: the pulls of its layer block, layer by layer, recording each
+  // layer's event so that layer l's forward waits for its own parameters
+  // only (a refinement of the graph's block gate: same data dependency).
   void broadcast(int j, cudaStream_t st) {
     uint16_t* mine = e->params_of(e->rank);
-    for (const BcCopy& c : bc_copies[static_cast<std::size_t>(j)]) {
+    const auto& cs = bc_copies[static_cast<std::size_t>(j)];
+    for (std::size_t i = 0; i < cs.size(); ++i) {
+      const BcCopy& c = cs[i];
       ck(cudaMemcpyAsync(mine + c.dst, e->params_of(c.owner) + c.dst, c.len * 2,
                          cudaMemcpyDeviceToDevice, st),
          "broadcast DMA");
+      if (i + 1 == cs.size() || cs[i + 1].layer != c.layer)
+        ck(cudaEventRecord(layer_ev[static_cast<std::size_t>(c.layer)], st), "event record");
     }
   }
   amsp::Seg* d_rsegs = nullptr;
@@ -246,6 +256,8 @@ struct amsp_sched {
     if (start_ev) cudaEventDestroy(start_ev);
     for (auto ev : join_ev)
       if (ev) cudaEventDestroy(ev);
+    for (auto ev : layer_ev)
+      if (ev) cudaEventDestroy(ev);
     for (auto s : comm)
       if (s) cudaStreamDestroy(s);
     cudaFree(d_rsegs);
@@ -360,9 +372,17 @@ struct amsp_sched {
     for (std::size_t i = 0; i < evs.size(); ++i) {
       const EventWork& w = work[i];
       cudaStream_t st = stream_of(w.stream, main);
-      for (int d : evs[i].depends_on)
-        if (work[d].stream != w.stream && work[d].record)
+      for (int d : evs[i].depends_on) {
+        if (work[d].stream == w.stream || !work[d].record) continue;
+        if (with_comm && work[d].kind == Work::Broadcast &&
+            evs[i].kind == shardplan::EventKind::FwdCompute) {
+          // mirrored broadcast: this layer's own pulls (head: index L)
+          const int l = evs[i].layer < 0 ? static_cast<int>(layer_ev.size()) - 1 : evs[i].layer;
+          ck(cudaStreamWaitEvent(st, layer_ev[static_cast<std::size_t>(l)], 0), "stream wait");
+        } else {
           ck(cudaStreamWaitEvent(st, events[d], 0), "stream wait");
+        }
+      }
       if (tracing) ck(cudaEventRecord(t_begin[i], st), "event record");
       const Table t{w.seg_begin, w.nseg, w.ntiles};
       switch (w.kind) {
@@ -597,10 +617,13 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     }
     // Layer block of each tensor: the graph's shard_gate (overlap_sim.cpp:
     // 193-199); head tensors (embed, final norm, lm_head) in the last block.
-    std::vector<int> block(n, n_bc - 1);
+    std::vector<int> block(n, n_bc - 1), layer(n, L);
     for (int l = 0; l < L; ++l) {
       const int j = std::max(0, ((l + 1) * n_bc + L - 1) / L - 1);
-      for (int i = 0; i < K; ++i) block[tensor_of(l, i)] = j;
+      for (int i = 0; i < K; ++i) {
+        block[tensor_of(l, i)] = j;
+        layer[tensor_of(l, i)] = l;
+      }
     }
     s->bc_copies.assign(static_cast<std::size_t>(n_bc), {});
     for (std::size_t t = 0; t < n; ++t) {
@@ -610,10 +633,15 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
         for (const auto& sg : member[q].segs) {
           const std::uint64_t a = std::max(lo, sg.flat), b = std::min(hi, sg.flat + sg.len);
           if (a < b)
-            s->bc_copies[block[t]].push_back({sg.dst + (a - sg.flat), b - a, e->dst_members[q]});
+            s->bc_copies[block[t]].push_back(
+                {sg.dst + (a - sg.flat), b - a, e->dst_members[q], layer[t]});
         }
       }
     }
+    for (auto& cs : s->bc_copies)  // layer order inside each block (head last)
+      std::stable_sort(cs.begin(), cs.end(),
+                       [](const BcCopy& x, const BcCopy& y) { return x.layer < y.layer; });
+    s->layer_ev.assign(static_cast<std::size_t>(L) + 1, nullptr);
   }
   std::uint64_t max_out = 0;
   std::vector<amsp::Seg> rsegs;
@@ -794,6 +822,7 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
       ck(cudaEventCreateWithFlags(&s->events[i], cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&s->start_ev, cudaEventDisableTiming), "event");
   for (auto& ev : s->join_ev) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+  for (auto& ev : s->layer_ev) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
   // Communication streams get the highest priority so their CTAs are placed
   // first whenever SMs free up between compute CTAs.
   int lo_prio = 0, hi_prio = 0;

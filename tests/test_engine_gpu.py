@@ -289,6 +289,8 @@ def test_scheduler_real_gemm_compute(cuda, world, p):
     for t in (1, 2):
         for sc in scheds:
             sc.step(t)
+    for sc in scheds:  # mirrored broadcast (W > 1): the last step's shards
+        sc.flush()
     params = [e.read("params").view(np.int16).astype(np.uint16) for e in engines]
     for prm in params:
         f = (prm.astype(np.uint32) << 16).view(np.float32)
