@@ -169,7 +169,9 @@ struct amsp_engine {
   void retune(int v, int forced_grid) {
     int g = 0;
     if (v == 0 && segments_aligned()) {
-      variant = 5;
+      // Variant 5 needs 2 CTAs per SM to beat the deep single-CTA ring; at
+      // W = 8 its 2-stage ring (2 x 57 KB) no longer fits twice, so take 6.
+      variant = (world > 1 && amsp::fused_blocks_per_sm(world, 5) < 2) ? 6 : 5;
       g = world == 1 ? sms : sms * amsp::fused_blocks_per_sm(world, variant);
     } else if (v == 0 && world == 1) {
       variant = 4;

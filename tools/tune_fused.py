@@ -58,7 +58,8 @@ def main():
             for e in engines:
                 e.time_kernel(False)
             bytes_ = sum(24 * e.info.owned for e in engines) + 4 * phi * W
-            rec = {"variant": v, "grid": engines[0].info.grid, "ms": round(ms, 3),
+            rec = {"variant": v, "chosen": engines[0].info.variant,
+                   "grid": engines[0].info.grid, "ms": round(ms, 3),
                    "GBps": round(bytes_ / (ms * 1e-3) / 1e9, 1)}
             out.append(rec)
             print(json.dumps(rec), flush=True)
