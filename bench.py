@@ -426,6 +426,9 @@ def run_ours(args):
 
     # The fused kernel alone (barriers excluded), bracketed by CUDA events on
     # the engine stream inside the same timed region.
+    # Raises if a cross-GPU barrier of the timed steps timed out (device
+    # error flag); a run with a lost peer never reports a number.
+    eng.stats()
     k_total, k_n = eng.kernel_ms()
     g_total, g_n = eng.gather_ms()
     eng.time_kernel(False)
@@ -548,6 +551,7 @@ def run_ours(args):
                 (Path(args.trace_dir) / f"measured_{tag}.json").write_text(text)
                 (Path(args.trace_dir) / f"predicted_{tag}.json").write_text(
                     sched.predicted_trace())
+        eng.stats()  # barrier error flag of the scheduled steps
         sched.close()
         return {"compute": compute, "tier": args.tier,
                 "tokens_per_microbatch": args.micro_batch * args.seq_len,
