@@ -100,7 +100,9 @@ def test_ragged_tensors_scalar_path(cuda):
     (2, 2, "greedy", 0), (4, 4, "greedy", 0), (4, 2, "greedy", 0), (8, 8, "greedy", 0),
     (4, 4, "contiguous", 0), (8, 2, "contiguous", 0),
     (2, 2, "greedy", 5), (4, 4, "greedy", 6), (4, 2, "greedy", 6), (8, 8, "greedy", 6),
-    (2, 2, "greedy", 2), (4, 4, "greedy", 1), (8, 8, "greedy", 2), (8, 2, "greedy", 1)])
+    (2, 2, "greedy", 2), (4, 4, "greedy", 1), (8, 8, "greedy", 2), (8, 2, "greedy", 1),
+    # non-power-of-two groups (tensor counts not divisible by k, ragged shards)
+    (3, 3, "greedy", 0), (6, 3, "greedy", 0), (6, 6, "contiguous", 0), (5, 5, "greedy", 6)])
 def test_emulated_dp_group_bit_exact(cuda, world, os_k, layout, variant):
     """W ranks of one DP group emulated on one GPU (link_local): fixed-order
     fp32 gradient sum over all W ranks, AdamW on each OS shard, bf16 params
