@@ -231,6 +231,18 @@ def cpu_baseline(phi_total, world, steps_budget_s=12.0, sample=None):
             "ms_per_step_extrapolated": best * phi_total / n * 1e3}
 
 
+def workload_config(args, S, world, phi):
+    """The `config` object both arms print (same workload, same keys)."""
+    dp = mesh_of(args.mesh, S) if args.mesh else S.DeviceMesh(world, 1)
+    plan = plan_of(args, S, dp)
+    return {"workload": f"{args.model} model states ({phi} params: bf16 P/G, fp32 "
+                        f"master+m+v), AMSP step = grad reduce + AdamW + param gather",
+            "model": args.model, "phi": phi, "plan": str(plan), "dp_mesh": str(dp),
+            "layout": args.layout,
+            "l2": f"inputs ({(16 * phi) / 1e9:.0f} GB of model state) >> 126 MB L2",
+            "parallelism": f"dp{world}"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -267,9 +279,7 @@ def run_reference(args):
         "ms_per_step": dt * phi / n * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "fp32 (bf16 in/out)",
         "data": "synthetic",
-        "config": {"workload": f"{args.model} model states, ZeRO-1 equiv over {world} ranks, "
-                               "AMSP optimizer step (CPU port, bounded sample)",
-                   "model": args.model, "phi": phi},
+        "config": workload_config(args, S, world, phi),
         "cpu_baseline": {"value": value, "unit": "params/s", "cores": cores, "kind": "port",
                          "sample": f"{n} consecutive params per step, {world} rank gradients"},
         "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0,
@@ -636,12 +646,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "fp32 (bf16 grads/params)", "data": "synthetic",
-            "config": {"workload": f"{args.model} model states ({phi} params: bf16 P/G, fp32 "
-                                   f"master+m+v), AMSP step = grad reduce + AdamW + param gather",
-                       "model": args.model, "phi": phi, "plan": str(plan), "dp_mesh": str(dp),
-                       "layout": args.layout,
-                       "l2": f"inputs ({(16 * phi) / 1e9:.0f} GB of model state) >> 126 MB L2",
-                       "parallelism": f"dp{world}"},
+            "config": workload_config(args, S, world, phi),
             "roofline": roof, "busbw": busbw, "overlap": overlap, "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches, "clocks": clk,
