@@ -192,10 +192,12 @@ def step_bytes(phi, owned, world, k, sp=1, sos=None, gathers=2):
     return hbm, max(nvl_in, nvl_out)
 
 
-def cpu_baseline(phi_total, world, steps_budget_s=12.0, sample=None):
+def cpu_baseline(phi_total, world, steps_budget_s=12.0, sample=None, max_steps=1000):
     """The oracle's CPU step (C + OpenMP, all host cores) on a bounded sample
     of the same workload: `sample` consecutive params of the flat model,
-    `world` ranks' gradients reduced, one OS owner per element (ZeRO-1)."""
+    `world` ranks' gradients reduced, one OS owner per element (ZeRO-1).
+    Steps repeat over the sample until `steps_budget_s` of CPU work is done
+    (about 10 s by default); the value is the median step."""
     import numpy as np
 
     from oracle import cpu as O
@@ -220,15 +222,16 @@ def cpu_baseline(phi_total, world, steps_budget_s=12.0, sample=None):
         O.step(grads, segs, master, m, v, params, s)
         times.append(time.perf_counter() - t0)
         t += 1
-        if time.perf_counter() - t_start > steps_budget_s or len(times) >= 5:
+        if time.perf_counter() - t_start > steps_budget_s or len(times) >= max_steps:
             break
-    best = min(times)
+    med = sorted(times)[len(times) // 2]
     cores = O.use_all_threads()
-    return {"value": n / best, "unit": "params/s", "cores": cores, "kind": "port",
+    return {"value": n / med, "unit": "params/s", "cores": cores, "kind": "port",
             "sample": f"{n} consecutive params of the {phi_total}-param flat model, {world} "
                       f"rank gradients reduced + AdamW + bf16 into {world} param copies; "
-                      f"best of {len(times)} steps, {best * 1e3:.1f} ms/step",
-            "ms_per_step_extrapolated": best * phi_total / n * 1e3}
+                      f"median of {len(times)} steps ({sum(times):.1f} s of CPU work), "
+                      f"{med * 1e3:.1f} ms/step",
+            "ms_per_step_extrapolated": med * phi_total / n * 1e3}
 
 
 def workload_config(args, S, world, phi):
@@ -251,7 +254,7 @@ def run_reference(args):
     model = S.model(args.model)
     phi = model.total_params
     world = args.gpus
-    cpu = cpu_baseline(phi, world, steps_budget_s=5.0)
+    cpu = cpu_baseline(phi, world, steps_budget_s=10.0)
     # K timed steps on the bounded sample (each step = one sample pass).
     import numpy as np
 
@@ -378,9 +381,18 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # More ranks than GPUs (e.g. --gpus 8 on a 4-GPU box) is a functional
+    # check of the W-rank path only: ranks share devices, NCCL refuses
+    # duplicate GPUs, so plumbing falls back to gloo and the line says so.
+    oversub = world > torch.cuda.device_count()
+    if oversub:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
     dp = mesh_of(args.mesh, S) if args.mesh else S.DeviceMesh(world, 1)
     model = S.model(args.model)
     plan = plan_of(args, S, dp)
@@ -403,7 +415,7 @@ def run_ours(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if oversub else f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -635,7 +647,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(phi, world)
+            cpu = cpu_baseline(phi, world, steps_budget_s=10.0)
         except Exception as ex:  # the baseline is reported, never required
             cpu = {"error": str(ex)}
 
@@ -651,6 +663,9 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "gpu_launches": launches, "clocks": clk,
         }
+        if oversub:
+            line["oversubscribed"] = (f"{world} ranks on {torch.cuda.device_count()} GPUs: "
+                                      "functional check, not a measurement")
         print(json.dumps(line), flush=True)
     eng.close()
     if world > 1:

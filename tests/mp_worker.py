@@ -37,7 +37,10 @@ def main():
                          "barrier + fused update")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ["LOCAL_RANK"])
+    # More ranks than GPUs (W=8 on a 2- or 4-GPU box) places several ranks on
+    # one device: the peer-memory path is the same (cudaIpc handles, flags),
+    # only the timing is meaningless.
+    local = int(os.environ["LOCAL_RANK"]) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     M = S.DeviceMesh

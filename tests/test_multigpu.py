@@ -34,7 +34,12 @@ CASES = [c + (0,) for c in CASES] + [
     (2, "2x1", None, "greedy", "host", 0), (4, "4x1", None, "greedy", "host", 0),
     (4, "2x1", None, "greedy", "host", 0),
     # ZeRO-3 all-gathers by the TMA bulk-copy kernel, in the step and in the scheduler
-    (4, "4x1", None, "greedy", "4x1+tma", 0), (4, "4x1", None, "greedy", "4x1+sched+tma", 0)]
+    (4, "4x1", None, "greedy", "4x1+tma", 0), (4, "4x1", None, "greedy", "4x1+sched+tma", 0),
+    # W=8 (the BASELINE 8xB200 meshes) with several ranks per GPU: ZeRO-1, ZeRO-1
+    # on the 2x4 virtual-node mesh, ZeRO-3, AMSP-13B (p=4, os=8)
+    (8, "8x1", None, "greedy", "oversub", 0), (8, "2x4", "2x4", "greedy", "oversub", 0),
+    (8, "8x1", None, "greedy", "8x1+oversub", 0), (8, "8x1", None, "greedy", "4x1+oversub", 0),
+    (8, "8x1", None, "greedy", "sched+oversub", 0), (8, "4x1", None, "greedy", "oversub", 2)]
 
 
 @pytest.mark.parametrize("world,os_mesh,dp_mesh,layout,p_mesh,variant", CASES)
@@ -44,8 +49,9 @@ def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh, variant):
     host, sched, tma = "host" in words, "sched" in words, "tma" in words
     meshes = [w for w in words if "x" in w]
     p_mesh = meshes[0] if meshes else None
-    if _ngpus() < world:
-        pytest.skip(f"needs {world} GPUs")
+    need = 2 if "oversub" in words else world
+    if _ngpus() < need:
+        pytest.skip(f"needs {need} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29531",
            str(REPO / "tests" / "mp_worker.py"), "--os-mesh", os_mesh, "--layout", layout]
