@@ -123,19 +123,19 @@ void amsp_o_adam_elem(const amsp_o_scalars* s, float g, float* p, float* m,
   *p = pp;
 }
 
+/* sc[t-1] = amsp_o_adam_scalars(..., t, world): hoisted out of the element
+ * loop (two pow() per step dominated the per-element cost); same values. */
 static void one_index(uint64_t i, uint64_t seed, int steps, int world,
-                      const amsp_o_hyper* h, float* mo, float* mmo, float* vo,
+                      const amsp_o_scalars* sc, float* mo, float* mmo, float* vo,
                       uint16_t* po) {
   float p = amsp_o_master_init(seed, i), m = 0.0f, v = 0.0f;
   for (int t = 1; t <= steps; ++t) {
-    amsp_o_scalars s;
-    amsp_o_adam_scalars(h->lr, h->beta1, h->beta2, h->eps, h->weight_decay, t,
-                        world, &s);
+    const amsp_o_scalars* s = &sc[t - 1];
     float g = amsp_o_bf16_to_f32(amsp_o_grad_bf16(seed, (uint32_t)t, 0, i));
     for (int r = 1; r < world; ++r)
       g = g + amsp_o_bf16_to_f32(amsp_o_grad_bf16(seed, (uint32_t)t, (uint32_t)r, i));
-    g = g * s.grad_scale;
-    amsp_o_adam_elem(&s, g, &p, &m, &v);
+    g = g * s->grad_scale;
+    amsp_o_adam_elem(s, g, &p, &m, &v);
   }
   if (mo) *mo = p;
   if (mmo) *mmo = m;
@@ -143,23 +143,35 @@ static void one_index(uint64_t i, uint64_t seed, int steps, int world,
   if (po) *po = amsp_o_f32_to_bf16(p);
 }
 
+static amsp_o_scalars* step_scalars(int steps, int world, const amsp_o_hyper* h) {
+  amsp_o_scalars* sc = (amsp_o_scalars*)malloc(sizeof(amsp_o_scalars) * (size_t)(steps > 0 ? steps : 1));
+  for (int t = 1; t <= steps; ++t)
+    amsp_o_adam_scalars(h->lr, h->beta1, h->beta2, h->eps, h->weight_decay, t, world,
+                        &sc[t - 1]);
+  return sc;
+}
+
 void amsp_o_trajectory(const uint64_t* index, size_t n, uint64_t seed,
                        int steps, int world, const amsp_o_hyper* h,
                        float* master, float* m, float* v, uint16_t* param) {
+  amsp_o_scalars* sc = step_scalars(steps, world, h);
 #pragma omp parallel for schedule(static)
   for (size_t k = 0; k < n; ++k)
-    one_index(index[k], seed, steps, world, h, master ? master + k : NULL,
+    one_index(index[k], seed, steps, world, sc, master ? master + k : NULL,
               m ? m + k : NULL, v ? v + k : NULL, param ? param + k : NULL);
+  free(sc);
 }
 
 void amsp_o_trajectory_range(uint64_t start, size_t n, uint64_t seed,
                              int steps, int world, const amsp_o_hyper* h,
                              float* master, float* m, float* v,
                              uint16_t* param) {
+  amsp_o_scalars* sc = step_scalars(steps, world, h);
 #pragma omp parallel for schedule(static)
   for (size_t k = 0; k < n; ++k)
-    one_index(start + k, seed, steps, world, h, master ? master + k : NULL,
+    one_index(start + k, seed, steps, world, sc, master ? master + k : NULL,
               m ? m + k : NULL, v ? v + k : NULL, param ? param + k : NULL);
+  free(sc);
 }
 
 void amsp_o_fill_grads(uint16_t* dst, uint64_t start, size_t n, uint64_t seed,

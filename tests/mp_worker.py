@@ -32,6 +32,9 @@ def main():
     ap.add_argument("--model", default="tiny")
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (5/6 = TMA)")
+    ap.add_argument("--full", action="store_true",
+                    help="check every element at full model size, streamed in chunks "
+                         "(tests/fullcheck.py) instead of materialising the whole model")
     ap.add_argument("--host", action="store_true",
                     help="amsp_engine_step_host: pinned host gradients, chunked H2D + per-chunk "
                          "barrier + fused update")
@@ -86,6 +89,19 @@ def main():
         torch.cuda.synchronize()
         sched.close()
     torch.cuda.synchronize()
+    if args.full:
+        from fullcheck import check_engine
+        per_proc = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        O.lib().amsp_o_set_threads(max(1, (os.cpu_count() or 1) // per_proc))
+        bad = check_engine(e, args.steps, world, log=lambda m: print(f"RANK {rank} {m}",
+                                                                     flush=True))
+        for b in bad:
+            print(f"RANK {rank} MISMATCH {b}", flush=True)
+        e.close()
+        dist.barrier()
+        print(f"RANK {rank} {'OK' if not bad else 'FAIL'} full-size", flush=True)
+        dist.destroy_process_group()
+        sys.exit(0 if not bad else 1)
     phi = e.info.total_params
     segs, owned = e.segments()
     ok = True

@@ -195,6 +195,22 @@ def test_llama1b_sampled_after_3_steps(cuda):
     e.close()
 
 
+def test_llama7b_every_element_after_2_steps(cuda):
+    """The bench's default workload at full size (LLaMA-7B replica, 108 GB of
+    state on one B200): every master/m/v/bf16 element bit-exact vs the oracle,
+    streamed in chunks (tests/fullcheck.py)."""
+    from fullcheck import check_engine
+    e = Engine(S.model("llama-7b"), _plan(M(1, 1)), M(1, 1))
+    e.init_state()
+    for t in (1, 2):
+        e.synth_grads(t)
+        e.step(t)
+    O.use_all_threads()
+    bad = check_engine(e, 2, 1)
+    e.close()
+    assert not bad, bad
+
+
 def test_invalid_plans_fail_loudly(cuda):
     from paper_2311_00257_b200 import _native as N
     model = S.model("tiny")

@@ -72,3 +72,27 @@ def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh, variant):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count(" OK ") == world, out[-4000:]
+
+
+# Every element at the BASELINE model sizes (streamed oracle, tests/fullcheck.py):
+# LLaMA-7B ZeRO-1 at W=2 and W=4, 7B on the 2x2 virtual-node mesh, 13B ZeRO-3 at W=4.
+FULL = [(2, "llama-7b", "2x1", None, None), (4, "llama-7b", "4x1", None, None),
+        (4, "llama-7b", "2x2", "2x2", None), (4, "llama-13b", "4x1", None, "4x1")]
+
+
+@pytest.mark.parametrize("world,model,os_mesh,dp_mesh,p_mesh", FULL)
+def test_torchrun_fullsize_every_element(world, model, os_mesh, dp_mesh, p_mesh):
+    if _ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29532",
+           str(REPO / "tests" / "mp_worker.py"), "--os-mesh", os_mesh, "--model", model,
+           "--steps", "2", "--full"]
+    if dp_mesh:
+        cmd += ["--dp-mesh", dp_mesh]
+    if p_mesh:
+        cmd += ["--p-mesh", p_mesh]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=REPO)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert out.count(" OK full-size") == world, out[-4000:]

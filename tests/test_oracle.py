@@ -193,3 +193,44 @@ def test_pshard_layout_partitions(sp, k, layout):
     assert all(a[1] == b[0] for a, b in zip(flat_spans, flat_spans[1:]))
     with pytest.raises(Exception, match="not divisible"):
         pshard_layout([10, 7], 2, 0, 1, 0, layout)
+
+
+def test_fullcheck_streams_every_element_and_catches_a_flip():
+    """tests/fullcheck.py (the full-size GPU parity checker) on a host-side
+    stand-in engine: rank 1 of a 2-rank ZeRO-1 greedy layout of the tiny model,
+    buffers filled from the oracle; one flipped bit in each buffer is found."""
+    from types import SimpleNamespace
+
+    from fullcheck import check_engine
+    from paper_2311_00257_b200.engine import DEFAULT_SEED, pshard_layout
+    sizes = S.llama_tensors(S.model("tiny"))
+    segs, owned = pshard_layout(sizes, 1, 0, 2, 1, "greedy")
+    phi = sum(sizes)
+    want = O.trajectory_range(0, phi, DEFAULT_SEED, 2, 2, O.hyper())
+    bufs = {"params": want[3].copy()}
+    for name, ref in zip(("master", "exp_avg", "exp_avg_sq"), want[:3]):
+        b = np.empty(owned, np.float32)
+        for f, o, _, ln in segs:
+            b[o:o + ln] = ref[f:f + ln]
+        bufs[name] = b
+
+    class Fake:
+        tensor_sizes = sizes
+        plan = SimpleNamespace(sp=lambda: 1)
+        info = SimpleNamespace(p_position=0, owned=owned)
+
+        def segments(self):
+            return [(f, o, ln) for f, o, _, ln in segs], owned
+
+        def read(self, which, off, n):
+            return bufs[which][off:off + n].copy()
+
+    logs = []
+    assert check_engine(Fake(), 2, 2, chunk=1 << 20, log=logs.append) == []
+    assert f"{phi} params + {owned} x 3" in logs[0]
+    for name in ("params", "master", "exp_avg_sq"):
+        b = bufs[name]
+        b.view(np.uint16 if name == "params" else np.uint32)[owned // 3] ^= 1
+        bad = check_engine(Fake(), 2, 2, chunk=1 << 20, log=logs.append)
+        assert len(bad) == 1 and bad[0].startswith(name), bad
+        b.view(np.uint16 if name == "params" else np.uint32)[owned // 3] ^= 1
