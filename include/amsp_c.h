@@ -362,6 +362,13 @@ typedef struct {
                                    step's BC events pull them by copy engine,
                                    gating the forward layer blocks;
                                    1 = push inside the optimizer kernels */
+  int optimizer_variant;        /* kernel of the optimizer updates that run
+                                   inside backward (optimizer_overlap = 1):
+                                   0 = LDG fused kernel (small smem, co-resides
+                                   with GEMM CTAs); 5 / 6 = the TMA bulk-copy
+                                   pipeline (2 / 1 CTAs per SM; 8-element-aligned
+                                   segments) on comm_ctas SMs, meant with
+                                   gemm_sm_margin = comm_ctas */
 } amsp_sched_config_t;
 
 typedef struct {

@@ -103,6 +103,7 @@ struct amsp_sched {
   int comm_ctas = 128, compute_ctas = 148;
   double time_scale = 1.0;
   bool optimizer_overlap = true;
+  int opt_variant = 0;  // kernel of the in-backward optimizer updates (cfg)
   std::vector<EventWork> work;
   int n_barriers = 0, end_a = 0, end_b = 0, n_buckets = 0, n_gather = 0, n_reduce = 0,
       n_compute = 0;
@@ -406,7 +407,7 @@ struct amsp_sched {
         case Work::ReduceAdam:
           if (with_comm) {
             barrier(w.barrier, st);
-            fused(t, comm_ctas, st);
+            fused(t, comm_ctas, st, opt_variant);
           }
           break;
         case Work::Broadcast:
@@ -419,7 +420,7 @@ struct amsp_sched {
       if (w.record) ck(cudaEventRecord(events[i], st), "event record");
       if (with_comm && w.post_ntiles > 0) {
         ck(cudaStreamWaitEvent(comm[1], events[i], 0), "stream wait");
-        fused(Table{w.post_begin, w.post_nseg, w.post_ntiles}, comm_ctas, comm[1]);
+        fused(Table{w.post_begin, w.post_nseg, w.post_ntiles}, comm_ctas, comm[1], opt_variant);
       }
     }
     for (int k = 0; k < 2; ++k) {
@@ -529,6 +530,11 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     return FlatRange{a, a + e->tensor_sizes[t]};
   };
   s->optimizer_overlap = cfg->optimizer_overlap != 0;
+  if (cfg->optimizer_variant != 0 && cfg->optimizer_variant != 5 && cfg->optimizer_variant != 6)
+    throw Error("sched: optimizer_variant must be 0 (LDG) or 5 / 6 (TMA)");
+  if (cfg->optimizer_variant != 0 && !e->segments_aligned())
+    throw Error("sched: the TMA optimizer variant needs 8-element-aligned segments");
+  s->opt_variant = cfg->optimizer_variant;
 
   shardplan::ClusterSpec cl;
   const DeviceMesh dp = to_mesh(e->cfg.dp_mesh);
@@ -857,6 +863,10 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     }
     ck(cudaDeviceSynchronize(), "gemm buffers");
   }
+  if (s->opt_variant != 0)
+    for (const auto& sg : rsegs)
+      if ((sg.flat | sg.os | sg.dst | sg.len) & 7u)
+        throw Error("sched: the TMA optimizer variant needs 8-element-aligned bucket pieces");
   s->comm_ctas = cfg->comm_ctas > 0 ? cfg->comm_ctas : 128;
   s->compute_ctas = cfg->compute_ctas > 0 ? cfg->compute_ctas : e->sms;
   s->time_scale = cfg->time_scale > 0 ? cfg->time_scale : 1.0;

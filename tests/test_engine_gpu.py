@@ -228,9 +228,14 @@ def test_invalid_plans_fail_loudly(cuda):
                                                (4, 1, 4, "none"), (4, 1, 2, "ag_rs_ar"),
                                                (2, 2, 2, "ag_rs_ar_bc"), (4, 4, 4, "ag_rs"),
                                                (4, 2, 4, "ag_rs_ar_bc")])
-@pytest.mark.parametrize("opt_overlap,gather,bc", [(True, "sm", "auto"), (False, "sm", "auto"),
-                                                   (True, "tma", "auto"), (False, "sm", "push")])
-def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap, gather, bc):
+@pytest.mark.parametrize("opt_overlap,gather,bc,ov", [(True, "sm", "auto", 0),
+                                                      (False, "sm", "auto", 0),
+                                                      (True, "tma", "auto", 0),
+                                                      (False, "sm", "push", 0),
+                                                      # in-backward optimizer on the TMA kernel
+                                                      (True, "tma", "auto", 6),
+                                                      (True, "sm", "push", 5)])
+def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap, gather, bc, ov):
     """The overlap scheduler replays the reference event graph (gradient
     buckets / module reduce-scatters / all-gathers on comm streams, compute
     stand-ins on the compute stream) and its split reduce -> AdamW + push
@@ -245,7 +250,7 @@ def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap, ga
     cost = S.CostConfig(bucket_size=1 << 20)  # several buckets on the tiny model
     sim = S.SimConfig(overlap_tier=tier, peak_flops_per_gpu=1e18)
     scheds = [Scheduler(e, model, prof, cost, sim, optimizer_overlap=opt_overlap, gather=gather,
-                        bc=bc)
+                        bc=bc, optimizer_variant=ov, comm_ctas=24 if ov else 0)
               for e in engines]
     info = scheds[0].info
     # mirrored broadcast: the graph leads with BC events (tier 4, s_p = 1, k > 1)

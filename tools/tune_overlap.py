@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--margins", default="0,16,32")
     ap.add_argument("--opt", default="1")
     ap.add_argument("--gather", default="sm")
+    ap.add_argument("--opt-variant", default="0", help="in-backward optimizer kernel(s): 0 LDG, 5/6 TMA")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--seq-len", type=int, default=4096)
     args = ap.parse_args()
@@ -66,20 +67,22 @@ def main():
         return float(t)
 
     sim = S.SimConfig(peak_flops_per_gpu=1413.6e12, compute_efficiency=0.6)
-    for cc, mg, oo, ga in itertools.product([int(x) for x in args.comm_ctas.split(",")],
-                                            [int(x) for x in args.margins.split(",")],
-                                            [int(x) for x in args.opt.split(",")],
-                                            args.gather.split(",")):
+    margins = args.margins.split(",")
+    for cc, mg, oo, ga, ov in itertools.product([int(x) for x in args.comm_ctas.split(",")],
+                                                margins, [int(x) for x in args.opt.split(",")],
+                                                args.gather.split(","),
+                                                [int(x) for x in args.opt_variant.split(",")]):
+        mg = cc if mg == "cc" else int(mg)  # "cc": withhold exactly the comm CTAs' SMs
         sched = Scheduler(eng, model, b200_profile(), S.CostConfig(), sim, comm_ctas=cc,
                           optimizer_overlap=bool(oo), compute=args.compute, gemm_sm_margin=mg,
-                          gather=ga)
+                          gather=ga, optimizer_variant=ov)
         timed(sched, True, 1)
         tb = timed(sched, True, args.steps)
         tc = timed(sched, False, args.steps)
         to = timed(sched, "optimizer", args.steps)
         if rank == 0:
             print(json.dumps({"comm_ctas": cc, "gemm_sm_margin": mg, "optimizer_overlap": oo,
-                              "gather": ga,
+                              "gather": ga, "optimizer_variant": ov,
                               "step_ms": round(tb, 2), "compute_only_ms": round(tc, 2),
                               "compute_plus_optimizer_ms": round(to, 2),
                               "exposed_comm_frac": round((tb - to) / tb, 4),
