@@ -369,6 +369,13 @@ typedef struct {
                                    pipeline (2 / 1 CTAs per SM; 8-element-aligned
                                    segments) on comm_ctas SMs, meant with
                                    gemm_sm_margin = comm_ctas */
+  int reduce_mode;              /* gradient reduce inside the step (W > 1):
+                                   0 = SM kernels pull peers' bf16 gradients
+                                   over NVLink; 1 = copy engines stage every
+                                   rank's gradients of the event's owned
+                                   pieces into local HBM after the barrier,
+                                   then the same kernels reduce locally (the
+                                   NVLink traffic leaves the SMs to compute) */
 } amsp_sched_config_t;
 
 typedef struct {

@@ -139,6 +139,36 @@ struct amsp_sched {
   }
   amsp::Seg* d_rsegs = nullptr;
   amsp::CopySeg* d_tcopy = nullptr;
+  // Copy-engine staged reduce (reduce_mode 1): after the barrier, every
+  // rank's bf16 gradients of the event's owned pieces are DMA'd (peer ->
+  // local, rotated start) into stage[r * stage_slot + ...]; the reduce /
+  // fused kernel then reads only local HBM through d_ssegs, a copy of the
+  // event's table whose `flat` is the staging offset. NVLink traffic moves
+  // off the SMs, which stay with the GEMMs.
+  bool reduce_dma = false;
+  amsp::Seg* d_ssegs = nullptr;
+  std::vector<amsp::Seg> h_rsegs, h_ssegs;
+  uint16_t* stage = nullptr;
+  std::uint64_t stage_slot = 0;
+
+  void stage_in(const Table& t, cudaStream_t st) {
+    for (int i = 0; i < e->world; ++i) {
+      const int r = (e->rank + 1 + i) % e->world;
+      uint16_t* dst = stage + static_cast<std::uint64_t>(r) * stage_slot;
+      const uint16_t* src = e->grads_of(r);
+      int j = t.begin;
+      while (j < t.begin + t.nseg) {  // coalesce pieces contiguous in both spaces
+        const std::uint64_t flat = h_rsegs[j].flat, off = h_ssegs[j].flat;
+        std::uint64_t len = h_rsegs[j].len;
+        ++j;
+        while (j < t.begin + t.nseg && h_rsegs[j].flat == flat + len &&
+               h_ssegs[j].flat == off + len)
+          len += h_rsegs[j++].len;
+        ck(cudaMemcpyAsync(dst + off, src + flat, len * 2, cudaMemcpyDeviceToDevice, st),
+           "staged reduce DMA");
+      }
+    }
+  }
   float* red = nullptr;
   // Real-compute mode buffers: activations / output-grads / outputs of
   // T x max-dim bf16, a 3-layer ring of gathered module weights (s_p > 1)
@@ -263,6 +293,8 @@ struct amsp_sched {
       if (s) cudaStreamDestroy(s);
     cudaFree(d_rsegs);
     cudaFree(d_tcopy);
+    cudaFree(d_ssegs);
+    cudaFree(stage);
     cudaFree(red);
     for (void* p : {static_cast<void*>(act), static_cast<void*>(dout), static_cast<void*>(yout),
                     static_cast<void*>(ring), static_cast<void*>(head_w)})
@@ -284,10 +316,13 @@ struct amsp_sched {
   void reduce(const Table& t, int grid, cudaStream_t s) {
     if (t.ntiles == 0) return;
     amsp::ReduceArgs a{};
-    a.segs = d_rsegs + t.begin;
+    a.segs = (reduce_dma ? d_ssegs : d_rsegs) + t.begin;
     a.nseg = t.nseg;
     a.ntiles = t.ntiles;
-    for (int r = 0; r < e->world; ++r) a.grads[r] = e->grads_of(r);
+    if (reduce_dma) stage_in(t, s);
+    for (int r = 0; r < e->world; ++r)
+      a.grads[r] = reduce_dma ? stage + static_cast<std::uint64_t>(r) * stage_slot
+                              : e->grads_of(r);
     a.red = red;
     a.scale = static_cast<float>(1.0 / e->world);
     ck(amsp::launch_reduce(a, e->world, grid, s), "sched reduce");
@@ -311,13 +346,16 @@ struct amsp_sched {
     ++e->launches;
   }
 
-  void fused(const Table& t, int grid, cudaStream_t s, int variant = 0) {
+  void fused(const Table& t, int grid, cudaStream_t s, int variant = 0, bool staged = false) {
     if (t.ntiles == 0) return;
     amsp::FusedArgs a{};
-    a.segs = d_rsegs + t.begin;
+    staged = staged && reduce_dma;
+    a.segs = (staged ? d_ssegs : d_rsegs) + t.begin;
     a.nseg = t.nseg;
     a.ntiles = t.ntiles;
-    for (int r = 0; r < e->world; ++r) a.grads[r] = e->grads_of(r);
+    if (staged) stage_in(t, s);
+    for (int r = 0; r < e->world; ++r)
+      a.grads[r] = staged ? stage + static_cast<std::uint64_t>(r) * stage_slot : e->grads_of(r);
     a.ndst = param_dsts(a.dsts);
     a.master = e->master;
     a.exp_avg = e->exp_avg;
@@ -407,7 +445,7 @@ struct amsp_sched {
         case Work::ReduceAdam:
           if (with_comm) {
             barrier(w.barrier, st);
-            fused(t, comm_ctas, st, opt_variant);
+            fused(t, comm_ctas, st, opt_variant, true);
           }
           break;
         case Work::Broadcast:
@@ -802,8 +840,38 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     for (int d : evs[i].depends_on)
       if (s->work[d].stream != s->work[i].stream) s->work[d].record = true;
 
+  if (cfg->reduce_mode < 0 || cfg->reduce_mode > 1) throw Error("sched: unknown reduce_mode");
+  s->reduce_dma = cfg->reduce_mode == 1 && e->world > 1;
+  if (s->reduce_dma) {
+    s->h_rsegs = rsegs;
+    s->h_ssegs = rsegs;
+    std::uint64_t slot = 8;
+    int stage_stream = -1;  // one staging buffer: its users must share a FIFO stream
+    for (const EventWork& w : s->work) {
+      if (w.kind != Work::Reduce && w.kind != Work::ReduceAdam) continue;
+      if (stage_stream >= 0 && w.stream != stage_stream)
+        throw Error("sched: staged reduces on two streams");
+      stage_stream = w.stream;
+      std::uint64_t off = 0;
+      for (int j = w.seg_begin; j < w.seg_begin + w.nseg; ++j) {
+        s->h_ssegs[j].flat = off;  // 8-element aligned staging offsets
+        off += (rsegs[j].len + 7) / 8 * 8;
+      }
+      slot = std::max(slot, off);
+    }
+    s->stage_slot = slot;
+  }
+
   // Device tables and buffers.
   e->use_device();
+  if (s->reduce_dma) {
+    ck(cudaMalloc(&s->stage, s->stage_slot * 2 * static_cast<std::uint64_t>(e->world)),
+       "cudaMalloc reduce staging");
+    ck(cudaMalloc(&s->d_ssegs, rsegs.size() * sizeof(amsp::Seg)), "cudaMalloc staged segs");
+    ck(cudaMemcpy(s->d_ssegs, s->h_ssegs.data(), rsegs.size() * sizeof(amsp::Seg),
+                  cudaMemcpyHostToDevice),
+       "copy staged segs");
+  }
   if (!rsegs.empty()) {
     ck(cudaMalloc(&s->d_rsegs, rsegs.size() * sizeof(amsp::Seg)), "cudaMalloc sched segs");
     ck(cudaMemcpy(s->d_rsegs, rsegs.data(), rsegs.size() * sizeof(amsp::Seg),

@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--p-mesh", default=None)
     ap.add_argument("--sched", action="store_true")
     ap.add_argument("--gather", default="sm", choices=["sm", "tma", "dma"])
+    ap.add_argument("--reduce", default="sm", choices=["sm", "dma"],
+                    help="scheduler gradient reduce: SM NVLink pulls / copy-engine staged")
     ap.add_argument("--model", default="tiny")
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (5/6 = TMA)")
@@ -70,7 +72,7 @@ def main():
         sched = Scheduler(e, S.model(args.model), b200_profile(),
                           S.CostConfig(bucket_size=1 << 20),
                           S.SimConfig(overlap_tier="ag_rs_ar_bc", peak_flops_per_gpu=1e16),
-                          gather=args.gather)
+                          gather=args.gather, reduce=args.reduce)
     for t in range(1, args.steps + 1):
         e.synth_grads(t)
         if sched:

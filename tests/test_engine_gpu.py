@@ -234,7 +234,10 @@ def test_invalid_plans_fail_loudly(cuda):
                                                       (False, "sm", "push", 0),
                                                       # in-backward optimizer on the TMA kernel
                                                       (True, "tma", "auto", 6),
-                                                      (True, "sm", "push", 5)])
+                                                      (True, "sm", "push", 5),
+                                                      # copy-engine staged reduces
+                                                      (True, "tma", "auto", -1),
+                                                      (False, "sm", "auto", -1)])
 def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap, gather, bc, ov):
     """The overlap scheduler replays the reference event graph (gradient
     buckets / module reduce-scatters / all-gathers on comm streams, compute
@@ -250,7 +253,8 @@ def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap, ga
     cost = S.CostConfig(bucket_size=1 << 20)  # several buckets on the tiny model
     sim = S.SimConfig(overlap_tier=tier, peak_flops_per_gpu=1e18)
     scheds = [Scheduler(e, model, prof, cost, sim, optimizer_overlap=opt_overlap, gather=gather,
-                        bc=bc, optimizer_variant=ov, comm_ctas=24 if ov else 0)
+                        bc=bc, optimizer_variant=max(ov, 0), comm_ctas=24 if ov > 0 else 0,
+                        reduce="dma" if ov < 0 else "sm")
               for e in engines]
     info = scheds[0].info
     # mirrored broadcast: the graph leads with BC events (tier 4, s_p = 1, k > 1)

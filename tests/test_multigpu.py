@@ -39,7 +39,11 @@ CASES = [c + (0,) for c in CASES] + [
     # on the 2x4 virtual-node mesh, ZeRO-3, AMSP-13B (p=4, os=8)
     (8, "8x1", None, "greedy", "oversub", 0), (8, "2x4", "2x4", "greedy", "oversub", 0),
     (8, "8x1", None, "greedy", "8x1+oversub", 0), (8, "8x1", None, "greedy", "4x1+oversub", 0),
-    (8, "8x1", None, "greedy", "sched+oversub", 0), (8, "4x1", None, "greedy", "oversub", 2)]
+    (8, "8x1", None, "greedy", "sched+oversub", 0), (8, "4x1", None, "greedy", "oversub", 2),
+    # scheduler with copy-engine staged gradient reduces
+    (2, "2x1", None, "greedy", "sched+dmared", 0), (4, "4x1", None, "greedy", "sched+dmared", 0),
+    (4, "4x1", None, "greedy", "4x1+sched+tma+dmared", 0),
+    (4, "2x1", None, "greedy", "sched+dmared", 0)]
 
 
 @pytest.mark.parametrize("world,os_mesh,dp_mesh,layout,p_mesh,variant", CASES)
@@ -67,6 +71,8 @@ def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh, variant):
         cmd += ["--host", "--model", "chunky", "--steps", "2"]
     if tma:
         cmd += ["--gather", "tma"]
+    if "dmared" in words:
+        cmd += ["--reduce", "dma"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=REPO,
                        env={**os.environ, "OMP_NUM_THREADS": "4"})
     out = r.stdout + r.stderr

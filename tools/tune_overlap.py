@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--opt", default="1")
     ap.add_argument("--gather", default="sm")
     ap.add_argument("--opt-variant", default="0", help="in-backward optimizer kernel(s): 0 LDG, 5/6 TMA")
+    ap.add_argument("--reduce", default="sm", help="gradient reduce: sm (NVLink pulls) / dma (staged)")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--seq-len", type=int, default=4096)
     args = ap.parse_args()
@@ -40,6 +41,7 @@ def main():
     M = S.DeviceMesh
     dp = M(world, 1)
     plan = {"zero1": S.ShardingPlan(M(1, 1), M(1, 1), dp), "zero3": S.ShardingPlan(dp, dp, dp),
+            "zero2": S.ShardingPlan(M(1, 1), dp, dp),
             "replica": S.ShardingPlan()}[args.plan]
     model = S.model(args.model, seq_len=args.seq_len)
     eng = Engine(model, plan, dp, rank=rank, device=local)
@@ -68,21 +70,21 @@ def main():
 
     sim = S.SimConfig(peak_flops_per_gpu=1413.6e12, compute_efficiency=0.6)
     margins = args.margins.split(",")
-    for cc, mg, oo, ga, ov in itertools.product([int(x) for x in args.comm_ctas.split(",")],
-                                                margins, [int(x) for x in args.opt.split(",")],
-                                                args.gather.split(","),
-                                                [int(x) for x in args.opt_variant.split(",")]):
+    for cc, mg, oo, ga, ov, rd in itertools.product(
+            [int(x) for x in args.comm_ctas.split(",")], margins,
+            [int(x) for x in args.opt.split(",")], args.gather.split(","),
+            [int(x) for x in args.opt_variant.split(",")], args.reduce.split(",")):
         mg = cc if mg == "cc" else int(mg)  # "cc": withhold exactly the comm CTAs' SMs
         sched = Scheduler(eng, model, b200_profile(), S.CostConfig(), sim, comm_ctas=cc,
                           optimizer_overlap=bool(oo), compute=args.compute, gemm_sm_margin=mg,
-                          gather=ga, optimizer_variant=ov)
+                          gather=ga, optimizer_variant=ov, reduce=rd)
         timed(sched, True, 1)
         tb = timed(sched, True, args.steps)
         tc = timed(sched, False, args.steps)
         to = timed(sched, "optimizer", args.steps)
         if rank == 0:
             print(json.dumps({"comm_ctas": cc, "gemm_sm_margin": mg, "optimizer_overlap": oo,
-                              "gather": ga, "optimizer_variant": ov,
+                              "gather": ga, "optimizer_variant": ov, "reduce": rd,
                               "step_ms": round(tb, 2), "compute_only_ms": round(tc, 2),
                               "compute_plus_optimizer_ms": round(to, 2),
                               "exposed_comm_frac": round((tb - to) / tb, 4),
