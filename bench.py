@@ -71,6 +71,10 @@ def parse():
     ap.add_argument("--gather", default="dma", choices=["dma", "sm", "tma"],
                     help="overlapped all-gathers on copy engines (dma), the SM kernel or the "
                          "TMA bulk-copy kernel")
+    ap.add_argument("--reduce", default="auto", choices=["auto", "sm", "dma"],
+                    help="overlapped step's gradient reduces: SM NVLink pulls or copy-engine "
+                         "staging (auto: dma when parameters are sharded, "
+                         "profiles/r01_s2_overlap_reduce_dma_*.jsonl)")
     ap.add_argument("--bc", default="auto", choices=["auto", "push"],
                     help="overlapped step: mirrored broadcast of updated shards in the next "
                          "forward (auto, tier ag_rs_ar_bc) or push inside the optimizer")
@@ -535,10 +539,17 @@ def run_ours(args):
         opt = args.optimizer_overlap
         if opt < 0:
             opt = 1 if (compute == "standin" or plan.sp() > 1) else 0
-        ctas = args.comm_ctas or (64 if (compute == "gemm" and plan.sp() > 1) else 128)
+        # Copy-engine staged reduces free the SMs for the GEMMs when P is
+        # sharded (13B ZeRO-3 W=4: 283 vs 295 ms); with s_p = 1 the bucket
+        # reduces share the copy engines with the mirrored broadcast and the
+        # SM pulls win (7B ZeRO-1 W=4: 139.5 vs 150.6 ms).
+        reduce = args.reduce if args.reduce != "auto" else ("dma" if plan.sp() > 1 else "sm")
+        ctas = args.comm_ctas or (64 if (compute == "gemm" and plan.sp() > 1 and reduce == "sm")
+                                  else 128)
         sched = Scheduler(eng, mspec, b200_profile(), S.CostConfig(), sim, comm_ctas=ctas,
                           optimizer_overlap=bool(opt), compute=compute,
-                          gemm_sm_margin=args.gemm_sm_margin, gather=args.gather, bc=args.bc)
+                          gemm_sm_margin=args.gemm_sm_margin, gather=args.gather, bc=args.bc,
+                          reduce=reduce)
 
         def timed(with_comm, k):
             nonlocal step
@@ -582,6 +593,9 @@ def run_ours(args):
                 "gather": {"dma": "copy engines", "sm": "SM kernel",
                            "tma": "TMA bulk-copy kernel"}[args.gather],
                 "comm_ctas": ctas,
+                "reduce": {"sm": "SM kernels pull peers' gradients over NVLink",
+                           "dma": "copy engines stage peers' gradients, SM kernels reduce "
+                                  "locally"}[reduce],
                 "param_broadcast": ("mirrored: copy-engine pulls in the next step's BC events, "
                                     "gating forward layer blocks" if si.mirrored_bc else
                                     "pushed by the optimizer kernels (NVLink stores)"),
