@@ -469,7 +469,7 @@ def run_ours(args):
     # kernel. s_p > 1: the all-gather passes are part of the roofline bytes,
     # so the whole step is the timed unit.
     t_meas = kernel_ms if info.sp == 1 else ms_per_step
-    kname = "fused_step_tma_kernel" if info.variant in (5, 6) else "fused_step_kernel"
+    kname = "fused_step_tma_kernel" if info.variant >= 5 else "fused_step_kernel"
     scope = (f"{kname} (reduce + AdamW + gather), variant {info.variant}" if info.sp == 1 else
              "whole step: 2 all-gather passes (" +
              {"sm": "gather_kernel", "dma": "copy engines", "tma": "gather_tma_kernel",

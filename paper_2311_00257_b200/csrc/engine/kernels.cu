@@ -565,13 +565,27 @@ __global__ void spin_kernel(unsigned long long ns, float* sink) {
 // 6 for 1 CTA / SM (<= 220 KB).
 constexpr int kTmaConsumers = 256;
 constexpr int kTmaTile = kTmaConsumers * 8;  // elements per stage (2048)
-constexpr int tma_stage_bytes(int w) { return kTmaTile * (2 * w + 12); }
-constexpr int tma_stages(int w, int variant) {
-  return (variant == 5 ? 100 * 1024 : 220 * 1024) / tma_stage_bytes(w) < 2
-             ? 2
-             : (variant == 5 ? 100 * 1024 : 220 * 1024) / tma_stage_bytes(w);
+// Variants 7 / 8 add a bf16 output tile per stage: the consumers write the
+// updated master / m / v back into the stage in place and the packed bf16
+// params into it, and the producer drains the stage with bulk stores
+// (cp.async.bulk shared -> global, local HBM and NVLink peers alike), so no
+// thread issues a global store at all.
+constexpr bool tma_bulk_out(int variant) { return variant == 7 || variant == 8; }
+constexpr bool tma_two_ctas(int variant) { return variant == 5 || variant == 7; }
+constexpr int tma_stage_bytes(int w, bool out = false) {
+  return kTmaTile * (2 * w + 12 + (out ? 2 : 0));
 }
-constexpr int tma_smem(int w, int stages) { return stages * tma_stage_bytes(w) + 1024; }
+constexpr int tma_stages(int w, int variant) {
+  return (tma_two_ctas(variant) ? 100 * 1024 : 220 * 1024) /
+                     tma_stage_bytes(w, tma_bulk_out(variant)) <
+                 2
+             ? 2
+             : (tma_two_ctas(variant) ? 100 * 1024 : 220 * 1024) /
+                   tma_stage_bytes(w, tma_bulk_out(variant));
+}
+constexpr int tma_smem(int w, int stages, bool out = false) {
+  return stages * tma_stage_bytes(w, out) + 1024;
+}
 
 struct TmaStageMeta {
   unsigned long long os, dst, len;
@@ -616,7 +630,14 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
       : "memory");
 }
 
-template <int W, int kStages, int kMinBlocks>
+__device__ __forceinline__ void bulk_s2g_nocommit(void* gmem_dst, const void* smem_src,
+                                                  uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
+               "r"(smem_addr(smem_src)), "r"(bytes)
+               : "memory");
+}
+
+template <int W, int kStages, int kMinBlocks, bool kBulkOut>
 __global__ void __launch_bounds__(kTmaConsumers + 32, kMinBlocks)
 fused_step_tma_kernel(const FusedArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -624,7 +645,9 @@ fused_step_tma_kernel(const FusedArgs a) {
   float* s_p = reinterpret_cast<float*>(smem + kStages * W * kTmaTile * 2);
   float* s_m = s_p + kStages * kTmaTile;
   float* s_v = s_m + kStages * kTmaTile;
-  uint64_t* full = reinterpret_cast<uint64_t*>(s_v + kStages * kTmaTile);
+  uint16_t* s_o = reinterpret_cast<uint16_t*>(s_v + kStages * kTmaTile);  // kBulkOut only
+  uint64_t* full = reinterpret_cast<uint64_t*>(kBulkOut ? static_cast<void*>(s_o + kStages * kTmaTile)
+                                                        : static_cast<void*>(s_o));
   uint64_t* empty = full + kStages;
   TmaStageMeta* meta = reinterpret_cast<TmaStageMeta*>(empty + kStages);
 
@@ -649,10 +672,36 @@ fused_step_tma_kernel(const FusedArgs a) {
       cur.n = a.nseg;
       cur.cur = 0;
       cur.staged = false;
+      // kBulkOut: drain stage s (its tile is finished by the consumers) with
+      // bulk stores; always one bulk group per tile, possibly empty.
+      auto store_back = [&](int s) {
+        const TmaStageMeta md = meta[s];
+        if (md.len) {
+          bulk_s2g_nocommit(a.master + md.os, s_p + s * kTmaTile, md.len * 4);
+          bulk_s2g_nocommit(a.exp_avg + md.os, s_m + s * kTmaTile, md.len * 4);
+          bulk_s2g_nocommit(a.exp_avg_sq + md.os, s_v + s * kTmaTile, md.len * 4);
+          for (int d = 0; d < a.ndst; ++d)
+            bulk_s2g_nocommit(a.dsts[d] + md.dst, s_o + s * kTmaTile, md.len * 2);
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      };
       int k = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
         const int s = k % kStages;
-        if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
+        if (kBulkOut) {
+          // Store tile k-S+1 (its stage is refilled next iteration), then make
+          // sure the store of tile k-S, issued one iteration ago, has read
+          // stage s before it is refilled: one tile of prefetch depth is
+          // traded for never waiting on the store just issued.
+          const int j = k - kStages + 1;
+          if (j >= 0) {
+            mbar_wait(&empty[j % kStages], (j / kStages) & 1);
+            store_back(j % kStages);
+          }
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        } else if (k >= kStages) {
+          mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
+        }
         const Seg& sg = cur.at(t / 2);
         const unsigned long long base =
             (static_cast<unsigned long long>(t / 2) - sg.tile0) * kTile + (t & 1) * kTmaTile;
@@ -669,6 +718,16 @@ fused_step_tma_kernel(const FusedArgs a) {
           bulk_g2s(s_m + s * kTmaTile, a.exp_avg + sg.os + base, len * 4, &full[s]);
           bulk_g2s(s_v + s * kTmaTile, a.exp_avg_sq + sg.os + base, len * 4, &full[s]);
         }
+      }
+      if (kBulkOut) {
+        for (int j = k - kStages + 1 > 0 ? k - kStages + 1 : 0; j < k; ++j) {
+          mbar_wait(&empty[j % kStages], (j / kStages) & 1);
+          store_back(j % kStages);
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        // Peer parameter stores visible system-wide before the trailing
+        // cross-GPU barrier releases the other ranks.
+        if (a.fence_peers) __threadfence_system();
       }
     }
     return;
@@ -714,22 +773,34 @@ fused_step_tma_kernel(const FusedArgs a) {
         adamw(a.s, ghi, pf[2 * w + 1], mf[2 * w + 1], vf[2 * w + 1]);
         packed[w] = pack_bf16x2(pf[2 * w], pf[2 * w + 1]);
       }
-      const unsigned long long o = md.os + e;
-      st_stream_v4(a.master + o, p[0]);
-      st_stream_v4(a.master + o + 4, p[1]);
-      st_stream_v4(a.exp_avg + o, m[0]);
-      st_stream_v4(a.exp_avg + o + 4, m[1]);
-      st_stream_v4(a.exp_avg_sq + o, v[0]);
-      st_stream_v4(a.exp_avg_sq + o + 4, v[1]);
       const uint4 out = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-      for (int d = 0; d < a.ndst; ++d) st_v4(a.dsts[d] + md.dst + e, out);
+      if (kBulkOut) {  // in place; the producer's bulk stores drain the stage
+        *reinterpret_cast<float4*>(s_p + s * kTmaTile + e) = p[0];
+        *reinterpret_cast<float4*>(s_p + s * kTmaTile + e + 4) = p[1];
+        *reinterpret_cast<float4*>(s_m + s * kTmaTile + e) = m[0];
+        *reinterpret_cast<float4*>(s_m + s * kTmaTile + e + 4) = m[1];
+        *reinterpret_cast<float4*>(s_v + s * kTmaTile + e) = v[0];
+        *reinterpret_cast<float4*>(s_v + s * kTmaTile + e + 4) = v[1];
+        *reinterpret_cast<uint4*>(s_o + s * kTmaTile + e) = out;
+      } else {
+        const unsigned long long o = md.os + e;
+        st_stream_v4(a.master + o, p[0]);
+        st_stream_v4(a.master + o + 4, p[1]);
+        st_stream_v4(a.exp_avg + o, m[0]);
+        st_stream_v4(a.exp_avg + o + 4, m[1]);
+        st_stream_v4(a.exp_avg_sq + o, v[0]);
+        st_stream_v4(a.exp_avg_sq + o + 4, v[1]);
+        for (int d = 0; d < a.ndst; ++d) st_v4(a.dsts[d] + md.dst + e, out);
+      }
     }
+    // generic-proxy shared-memory writes -> visible to the bulk stores
+    if (kBulkOut) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   // Peer parameter stores must be visible system-wide before the trailing
   // cross-GPU barrier releases the other ranks.
-  if (a.fence_peers) __threadfence_system();
+  if (!kBulkOut && a.fence_peers) __threadfence_system();
   if (a.stats != nullptr) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
@@ -847,24 +918,25 @@ FusedFn select_fused(int world, int variant) {
 // Variants 5 / 6: the TMA pipeline, ring sized for 2 / 1 CTAs per SM.
 template <int W, int V>
 struct Tma {
+  static constexpr bool kOut = tma_bulk_out(V);
   static constexpr int kStages = tma_stages(W, V);
-  static constexpr int kSmem = tma_smem(W, kStages);
+  static constexpr int kSmem = tma_smem(W, kStages, kOut);
+  static constexpr auto kFn = fused_step_tma_kernel<W, kStages, tma_two_ctas(V) ? 2 : 1, kOut>;
   static cudaError_t prepare() {
-    static const cudaError_t attr = cudaFuncSetAttribute(
-        fused_step_tma_kernel<W, kStages, V == 5 ? 2 : 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(kFn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     return attr;
   }
   static int blocks_per_sm() {
     int blocks = 0;
     if (prepare() == cudaSuccess)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fused_step_tma_kernel<W, kStages, V == 5 ? 2 : 1>,
-                                                    kTmaConsumers + 32, kSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kFn, kTmaConsumers + 32, kSmem);
     return blocks > 0 ? blocks : 1;
   }
   static cudaError_t launch(const FusedArgs& a, int grid, cudaStream_t stream) {
     const cudaError_t attr = prepare();
     if (attr != cudaSuccess) return attr;
-    fused_step_tma_kernel<W, kStages, V == 5 ? 2 : 1><<<grid, kTmaConsumers + 32, kSmem, stream>>>(a);
+    kFn<<<grid, kTmaConsumers + 32, kSmem, stream>>>(a);
     return cudaGetLastError();
   }
 };
@@ -902,6 +974,8 @@ cudaError_t tma_launch(const FusedArgs& a, int world, int grid, cudaStream_t str
 int fused_blocks_per_sm(int world, int variant) {
   if (variant == 5) return tma_blocks_per_sm<5>(world);
   if (variant == 6) return tma_blocks_per_sm<6>(world);
+  if (variant == 7) return tma_blocks_per_sm<7>(world);
+  if (variant == 8) return tma_blocks_per_sm<8>(world);
   FusedFn f = select_fused(world, variant);
   int blocks = 0;
   if (f) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f, kBlock, 0);
@@ -913,6 +987,8 @@ cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int varia
   if (a.ntiles == 0) return cudaSuccess;
   if (variant == 5) return tma_launch<5>(a, world, grid, stream);  // 8-aligned segments only
   if (variant == 6) return tma_launch<6>(a, world, grid, stream);
+  if (variant == 7) return tma_launch<7>(a, world, grid, stream);
+  if (variant == 8) return tma_launch<8>(a, world, grid, stream);
   FusedFn f = select_fused(world, variant);
   if (!f) return cudaErrorInvalidValue;
   f<<<grid, kBlock, 0, stream>>>(a);

@@ -482,7 +482,7 @@ struct amsp_sched {
       a.exp_avg_sq = e->exp_avg_sq;
       a.s = scalars;
       // the engine's single-rank choice: TMA (1 CTA / SM) when aligned, else LDG
-      const bool tma = e->variant == 5 || e->variant == 6;
+      const bool tma = e->variant >= 5;
       ck(amsp::launch_fused_step(a, 1, tma ? e->sms : e->sms * 2, tma ? e->variant : 4, main),
          "local optimizer");
       ++e->launches;
@@ -568,8 +568,8 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     return FlatRange{a, a + e->tensor_sizes[t]};
   };
   s->optimizer_overlap = cfg->optimizer_overlap != 0;
-  if (cfg->optimizer_variant != 0 && cfg->optimizer_variant != 5 && cfg->optimizer_variant != 6)
-    throw Error("sched: optimizer_variant must be 0 (LDG) or 5 / 6 (TMA)");
+  if (cfg->optimizer_variant != 0 && (cfg->optimizer_variant < 5 || cfg->optimizer_variant > 8))
+    throw Error("sched: optimizer_variant must be 0 (LDG) or 5..8 (TMA)");
   if (cfg->optimizer_variant != 0 && !e->segments_aligned())
     throw Error("sched: the TMA optimizer variant needs 8-element-aligned segments");
   s->opt_variant = cfg->optimizer_variant;

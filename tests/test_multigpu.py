@@ -40,6 +40,9 @@ CASES = [c + (0,) for c in CASES] + [
     (8, "8x1", None, "greedy", "oversub", 0), (8, "2x4", "2x4", "greedy", "oversub", 0),
     (8, "8x1", None, "greedy", "8x1+oversub", 0), (8, "8x1", None, "greedy", "4x1+oversub", 0),
     (8, "8x1", None, "greedy", "sched+oversub", 0), (8, "4x1", None, "greedy", "oversub", 2),
+    # fused kernel with bulk-store drains (variants 7 / 8)
+    (2, "2x1", None, "greedy", None, 7), (4, "4x1", None, "greedy", None, 7),
+    (4, "2x1", None, "greedy", None, 8),
     # scheduler with copy-engine staged gradient reduces
     (2, "2x1", None, "greedy", "sched+dmared", 0), (4, "4x1", None, "greedy", "sched+dmared", 0),
     (4, "4x1", None, "greedy", "4x1+sched+tma+dmared", 0),
