@@ -171,7 +171,12 @@ struct amsp_engine {
     if (v == 0 && segments_aligned()) {
       // Variant 5 needs 2 CTAs per SM to beat the deep single-CTA ring; at
       // W = 8 its 2-stage ring (2 x 57 KB) no longer fits twice, so take 6.
-      variant = (world > 1 && amsp::fused_blocks_per_sm(world, 5) < 2) ? 6 : 5;
+      // At W = 2 the bulk-store drain (7) wins: 21.03 vs 21.74 ms on 7B
+      // ZeRO-1; at W = 1 and W = 4 it loses (30.2 vs 29.8, 32.0 vs 31.0 ms;
+      // profiles/r01_s2_bulk_*.json).
+      variant = world == 2 ? 7
+                : (world > 1 && amsp::fused_blocks_per_sm(world, 5) < 2) ? 6
+                                                                          : 5;
       g = world == 1 ? sms : sms * amsp::fused_blocks_per_sm(world, variant);
     } else if (v == 0 && world == 1) {
       variant = 4;
