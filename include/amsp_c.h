@@ -300,8 +300,9 @@ int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t cou
 /* Fused-kernel tuning: variant 0 auto, 1 one vector in flight per thread,
  * 2 two vectors, 3 two vectors + >=3 CTAs/SM, 4 one vector + >=4 CTAs/SM,
  * 5 TMA bulk-copy pipeline (ring for 2 CTAs/SM), 6 TMA (ring for 1 CTA/SM),
- * 7 / 8 = 5 / 6 with bulk-store drains (no thread-issued global stores) --
- * 5..8 need 8-element-aligned segments;
+ * 7 / 8 = 5 / 6 with bulk-store drains (no thread-issued global stores),
+ * 9 / 10 = 5 with a 2- / 4-stage ring -- 5..10 need 8-element-aligned
+ * segments;
  * grid 0 = SMs x resident CTAs (persistent). */
 int amsp_engine_tune(amsp_engine_t* e, int variant, int grid);
 /* All-gather implementation: grid > 0 = the SM (LDG/STG) kernel with that

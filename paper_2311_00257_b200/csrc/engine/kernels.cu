@@ -571,12 +571,18 @@ constexpr int kTmaTile = kTmaConsumers * 8;  // elements per stage (2048)
 // (cp.async.bulk shared -> global, local HBM and NVLink peers alike), so no
 // thread issues a global store at all.
 constexpr bool tma_bulk_out(int variant) { return variant == 7 || variant == 8; }
-constexpr bool tma_two_ctas(int variant) { return variant == 5 || variant == 7; }
+constexpr bool tma_two_ctas(int variant) {
+  return variant == 5 || variant == 7 || variant == 9 || variant == 10;
+}
 constexpr int tma_stage_bytes(int w, bool out = false) {
   return kTmaTile * (2 * w + 12 + (out ? 2 : 0));
 }
+// Variants 9 / 10: variant 5's kernel with a fixed 2- / 4-stage ring (ring
+// depth sweep; deeper is not better at W = 1: 7 stages 32.8 ms, 3 stages 29.8).
 constexpr int tma_stages(int w, int variant) {
-  return (tma_two_ctas(variant) ? 100 * 1024 : 220 * 1024) /
+  return variant == 9    ? 2
+         : variant == 10 ? 4
+         : (tma_two_ctas(variant) ? 100 * 1024 : 220 * 1024) /
                      tma_stage_bytes(w, tma_bulk_out(variant)) <
                  2
              ? 2
@@ -976,6 +982,8 @@ int fused_blocks_per_sm(int world, int variant) {
   if (variant == 6) return tma_blocks_per_sm<6>(world);
   if (variant == 7) return tma_blocks_per_sm<7>(world);
   if (variant == 8) return tma_blocks_per_sm<8>(world);
+  if (variant == 9) return tma_blocks_per_sm<9>(world);
+  if (variant == 10) return tma_blocks_per_sm<10>(world);
   FusedFn f = select_fused(world, variant);
   int blocks = 0;
   if (f) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f, kBlock, 0);
@@ -989,6 +997,8 @@ cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int varia
   if (variant == 6) return tma_launch<6>(a, world, grid, stream);
   if (variant == 7) return tma_launch<7>(a, world, grid, stream);
   if (variant == 8) return tma_launch<8>(a, world, grid, stream);
+  if (variant == 9) return tma_launch<9>(a, world, grid, stream);
+  if (variant == 10) return tma_launch<10>(a, world, grid, stream);
   FusedFn f = select_fused(world, variant);
   if (!f) return cudaErrorInvalidValue;
   f<<<grid, kBlock, 0, stream>>>(a);
