@@ -301,8 +301,8 @@ int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t cou
  * 2 two vectors, 3 two vectors + >=3 CTAs/SM, 4 one vector + >=4 CTAs/SM,
  * 5 TMA bulk-copy pipeline (ring for 2 CTAs/SM), 6 TMA (ring for 1 CTA/SM),
  * 7 / 8 = 5 / 6 with bulk-store drains (no thread-issued global stores),
- * 9 / 10 = 5 with a 2- / 4-stage ring -- 5..10 need 8-element-aligned
- * segments;
+ * 9 / 10 / 12 = a 2- / 4- / 5-stage ring, 11 = 5 stages with bulk-store
+ * drains -- 5..12 need 8-element-aligned segments;
  * grid 0 = SMs x resident CTAs (persistent). */
 int amsp_engine_tune(amsp_engine_t* e, int variant, int grid);
 /* All-gather implementation: grid > 0 = the SM (LDG/STG) kernel with that

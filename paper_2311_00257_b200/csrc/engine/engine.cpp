@@ -430,7 +430,7 @@ int amsp_engine_tune_gather(amsp_engine_t* e, int grid) {
 int amsp_engine_tune(amsp_engine_t* e, int variant, int grid) {
   return amsp::guarded([&] {
     if (!e) throw Error("engine: null argument");
-    if (variant < 0 || variant > 10) throw Error("engine: unknown kernel variant");
+    if (variant < 0 || variant > 12) throw Error("engine: unknown kernel variant");
     if (variant >= 5) {
       for (const auto& s : e->layout.segs)
         if ((s.flat | s.os | s.dst | s.len) & 7u)

@@ -570,18 +570,31 @@ constexpr int kTmaTile = kTmaConsumers * 8;  // elements per stage (2048)
 // params into it, and the producer drains the stage with bulk stores
 // (cp.async.bulk shared -> global, local HBM and NVLink peers alike), so no
 // thread issues a global store at all.
-constexpr bool tma_bulk_out(int variant) { return variant == 7 || variant == 8; }
+constexpr bool tma_bulk_out(int variant) {
+  return variant == 7 || variant == 8 || variant == 11;
+}
 constexpr bool tma_two_ctas(int variant) {
   return variant == 5 || variant == 7 || variant == 9 || variant == 10;
+}
+// Fixed ring depths (0 = sized by the smem budget), capped to what fits.
+constexpr int tma_fixed_stages(int variant) {
+  return variant == 9 ? 2 : variant == 10 ? 4 : (variant == 11 || variant == 12) ? 5 : 0;
 }
 constexpr int tma_stage_bytes(int w, bool out = false) {
   return kTmaTile * (2 * w + 12 + (out ? 2 : 0));
 }
-// Variants 9 / 10: variant 5's kernel with a fixed 2- / 4-stage ring (ring
-// depth sweep; deeper is not better at W = 1: 7 stages 32.8 ms, 3 stages 29.8).
+// Variants 9 / 10 / 12: a fixed 2- / 4- / 5-stage ring; 11: 5 stages with
+// the bulk-store drain (ring-depth sweep: at W = 1 three stages are best,
+// 2 -> 36.4, 3 -> 29.9, 4 -> 30.8, 7 -> 32.8 ms; at W = 2 four beat three,
+// profiles/r01_s2_stages_*.json).
 constexpr int tma_stages(int w, int variant) {
-  return variant == 9    ? 2
-         : variant == 10 ? 4
+  return tma_fixed_stages(variant) > 0
+             ? (tma_fixed_stages(variant) * tma_stage_bytes(w, tma_bulk_out(variant)) <=
+                        220 * 1024
+                    ? tma_fixed_stages(variant)
+                    : (220 * 1024 / tma_stage_bytes(w, tma_bulk_out(variant)) < 2
+                           ? 2
+                           : 220 * 1024 / tma_stage_bytes(w, tma_bulk_out(variant))))
          : (tma_two_ctas(variant) ? 100 * 1024 : 220 * 1024) /
                      tma_stage_bytes(w, tma_bulk_out(variant)) <
                  2
@@ -984,6 +997,8 @@ int fused_blocks_per_sm(int world, int variant) {
   if (variant == 8) return tma_blocks_per_sm<8>(world);
   if (variant == 9) return tma_blocks_per_sm<9>(world);
   if (variant == 10) return tma_blocks_per_sm<10>(world);
+  if (variant == 11) return tma_blocks_per_sm<11>(world);
+  if (variant == 12) return tma_blocks_per_sm<12>(world);
   FusedFn f = select_fused(world, variant);
   int blocks = 0;
   if (f) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f, kBlock, 0);
@@ -999,6 +1014,8 @@ cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int varia
   if (variant == 8) return tma_launch<8>(a, world, grid, stream);
   if (variant == 9) return tma_launch<9>(a, world, grid, stream);
   if (variant == 10) return tma_launch<10>(a, world, grid, stream);
+  if (variant == 11) return tma_launch<11>(a, world, grid, stream);
+  if (variant == 12) return tma_launch<12>(a, world, grid, stream);
   FusedFn f = select_fused(world, variant);
   if (!f) return cudaErrorInvalidValue;
   f<<<grid, kBlock, 0, stream>>>(a);

@@ -568,8 +568,8 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     return FlatRange{a, a + e->tensor_sizes[t]};
   };
   s->optimizer_overlap = cfg->optimizer_overlap != 0;
-  if (cfg->optimizer_variant != 0 && (cfg->optimizer_variant < 5 || cfg->optimizer_variant > 10))
-    throw Error("sched: optimizer_variant must be 0 (LDG) or 5..10 (TMA)");
+  if (cfg->optimizer_variant != 0 && (cfg->optimizer_variant < 5 || cfg->optimizer_variant > 12))
+    throw Error("sched: optimizer_variant must be 0 (LDG) or 5..12 (TMA)");
   if (cfg->optimizer_variant != 0 && !e->segments_aligned())
     throw Error("sched: the TMA optimizer variant needs 8-element-aligned segments");
   s->opt_variant = cfg->optimizer_variant;

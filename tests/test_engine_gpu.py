@@ -56,7 +56,8 @@ def _check_rank(e, want_full, steps):
 @pytest.mark.parametrize("layout,variant", [("greedy", 0), ("contiguous", 0), ("greedy", 5),
                                             ("greedy", 1), ("greedy", 2), ("greedy", 3),
                                             ("greedy", 6), ("greedy", 7), ("greedy", 8),
-                                            ("greedy", 9), ("greedy", 10)])
+                                            ("greedy", 9), ("greedy", 10), ("greedy", 11),
+                                            ("greedy", 12)])
 def test_single_gpu_tiny_10_steps_bit_exact(cuda, layout, variant):
     """variants 5 / 6 = the TMA bulk-copy pipeline (cp.async.bulk + mbarrier);
     7 / 8 = the same with bulk-store drains (no thread-issued global stores)."""
@@ -105,6 +106,7 @@ def test_ragged_tensors_scalar_path(cuda):
     (2, 2, "greedy", 5), (4, 4, "greedy", 6), (4, 2, "greedy", 6), (8, 8, "greedy", 6),
     (2, 2, "greedy", 7), (4, 4, "greedy", 7), (4, 2, "greedy", 8), (8, 8, "greedy", 8),
     (8, 2, "greedy", 7), (5, 5, "greedy", 8), (2, 2, "greedy", 9), (4, 4, "greedy", 10),
+    (2, 2, "greedy", 11), (4, 2, "greedy", 11), (2, 2, "greedy", 12), (8, 8, "greedy", 12),
     (2, 2, "greedy", 2), (4, 4, "greedy", 1), (8, 8, "greedy", 2), (8, 2, "greedy", 1),
     # non-power-of-two groups (tensor counts not divisible by k, ragged shards)
     (3, 3, "greedy", 0), (6, 3, "greedy", 0), (6, 6, "contiguous", 0), (5, 5, "greedy", 6)])
