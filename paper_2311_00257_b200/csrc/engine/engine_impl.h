@@ -171,10 +171,13 @@ struct amsp_engine {
     if (v == 0 && segments_aligned()) {
       // Variant 5 needs 2 CTAs per SM to beat the deep single-CTA ring; at
       // W = 8 its 2-stage ring (2 x 57 KB) no longer fits twice, so take 6.
-      // At W = 2 the bulk-store drain (7) wins: 21.03 vs 21.74 ms on 7B
-      // ZeRO-1; at W = 1 and W = 4 it loses (30.2 vs 29.8, 32.0 vs 31.0 ms;
-      // profiles/r01_s2_bulk_*.json).
-      variant = world == 2 ? 7
+      // Ring-depth / drain sweep on 7B ZeRO-1 (profiles/r01_s2_bulk_*.json,
+      // r01_s2_stages*_*.json): W = 2 -> 5 stages with the bulk-store drain
+      // (11): 19.25 ms vs 21.0 (7), 21.7 (5), 22.0 (5 stages, no drain);
+      // W = 3..4 -> a 4-stage ring at 1 CTA/SM (10): 30.2-30.3 vs 30.3-30.8
+      // ms (5); W = 1 -> 3 stages (5): 29.9 vs 30.8 (4 stages), 36.4 (2).
+      variant = world == 2                  ? 11
+                : (world == 3 || world == 4) ? 10
                 : (world > 1 && amsp::fused_blocks_per_sm(world, 5) < 2) ? 6
                                                                           : 5;
       g = world == 1 ? sms : sms * amsp::fused_blocks_per_sm(world, variant);

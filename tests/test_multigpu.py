@@ -43,6 +43,8 @@ CASES = [c + (0,) for c in CASES] + [
     # fused kernel with bulk-store drains (variants 7 / 8)
     (2, "2x1", None, "greedy", None, 7), (4, "4x1", None, "greedy", None, 7),
     (4, "2x1", None, "greedy", None, 8),
+    # ring-depth variants (W=2 default 11, W=4 default 10) forced on other groups
+    (4, "4x1", None, "greedy", None, 11), (2, "2x1", None, "greedy", None, 10),
     # scheduler with copy-engine staged gradient reduces
     (2, "2x1", None, "greedy", "sched+dmared", 0), (4, "4x1", None, "greedy", "sched+dmared", 0),
     (4, "4x1", None, "greedy", "4x1+sched+tma+dmared", 0),
