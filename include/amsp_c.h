@@ -207,6 +207,38 @@ int amsp_pshard_layout(const uint64_t* tensor_sizes, int n_tensors, int sp, int 
                        uint64_t* dst, uint64_t* len, int cap, int* n_segments,
                        uint64_t* owned);
 
+/* B200 roofline of one engine step (engine/roofline.h):
+ * algorithmic HBM / NVLink bytes of `rank` for `plan` on `dp`, with
+ * `gathers` all-gather passes when s_p > 1, and the bound step time
+ * max(hbm/hbm_bw, max(in, out)/nvlink_bw). rank < 0 = the slowest rank
+ * (written to *slowest when non-NULL). No reference counterpart: the
+ * reference costs communication only (cost_model.cpp:128-140). */
+typedef struct {
+  uint64_t owned, hbm_bytes, nvlink_in_bytes, nvlink_out_bytes;
+  double t_hbm, t_nvlink, t_step;
+} amsp_step_roofline_t;
+
+int amsp_step_roofline(const uint64_t* tensor_sizes, int n_tensors, const amsp_plan_t* plan,
+                       amsp_mesh_t dp, int rank, int layout, int gathers, double hbm_bw,
+                       double nvlink_bw, int* slowest, amsp_step_roofline_t* out);
+
+/* The engine's flat tensor list of a LLaMA-style model (embed, L x modules,
+ * final norm, lm_head); *n = count, sizes[0..min(cap, n)) filled. */
+int amsp_model_tensors(const amsp_model_t* model, uint64_t* sizes, int cap, int* n);
+
+/* Roofline solver: the reference's candidates (enumerate_candidates,
+ * planner.cpp:110-129), memory model and feasibility (evaluate_plan,
+ * :131-141), restricted to plans the engine can run, ordered by the B200
+ * step roofline of the slowest rank (2 gather passes when s_p > 1), then
+ * T_comm, then the plan's lex key. Outputs as amsp_solve; code 2 when no
+ * candidate qualifies (best = the leanest candidate). amsp_solve itself
+ * stays the reference objective, bit-exact. */
+int amsp_solve_roofline(const amsp_model_t* model, const amsp_cluster_t* cluster,
+                        const amsp_profile_t* profile, const amsp_cost_config_t* cfg,
+                        double hbm_bw, double nvlink_bw, int layout, amsp_plan_result_t* best,
+                        amsp_step_roofline_t* best_step, amsp_plan_result_t* all,
+                        amsp_step_roofline_t* all_steps, int cap, int* n_all);
+
 /* Group of `rank` for component mesh `mesh` inside the DP mesh `dp`
  * (ranks numbered node-major: rank = node*dp.per_node + local). Returns the
  * block index, the rank's position in its block and the block's members in

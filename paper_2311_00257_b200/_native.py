@@ -79,6 +79,12 @@ class MemoryBreakdown(C.Structure):
                  "d_total")]
 
 
+class StepRoofline(C.Structure):
+    _fields_ = [("owned", C.c_uint64), ("hbm_bytes", C.c_uint64),
+                ("nvlink_in_bytes", C.c_uint64), ("nvlink_out_bytes", C.c_uint64),
+                ("t_hbm", C.c_double), ("t_nvlink", C.c_double), ("t_step", C.c_double)]
+
+
 class PlanResult(C.Structure):
     _fields_ = [("plan", Plan), ("time", TimeBreakdown), ("memory", MemoryBreakdown),
                 ("feasible", C.c_int), ("rank", C.c_int)]
@@ -172,6 +178,12 @@ SIGNATURES = {
     "amsp_pshard_layout": (C.c_int, [P(u64), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                      C.c_int, P(u64), P(u64), P(u64), P(u64), C.c_int,
                                      P(C.c_int), P(u64)]),
+    "amsp_step_roofline": (C.c_int, [P(u64), C.c_int, P(Plan), Mesh, C.c_int, C.c_int, C.c_int,
+                                     C.c_double, C.c_double, P(C.c_int), P(StepRoofline)]),
+    "amsp_model_tensors": (C.c_int, [P(Model), P(u64), C.c_int, P(C.c_int)]),
+    "amsp_solve_roofline": (C.c_int, [P(Model), P(Cluster), vp, P(CostConfig), C.c_double,
+                                      C.c_double, C.c_int, P(PlanResult), P(StepRoofline),
+                                      P(PlanResult), P(StepRoofline), C.c_int, P(C.c_int)]),
     "amsp_engine_create": (C.c_int, [P(EngineConfig), P(vp)]),
     "amsp_engine_info": (C.c_int, [vp, P(EngineInfo)]),
     "amsp_engine_export_handle": (C.c_int, [vp, vp]),

@@ -125,6 +125,8 @@ def cmd_plan(args):
     raw, model, cluster, cost, sim = load_config(args.config)
     prof = load_profile(args.profile or raw.get("profile_path"))
     report = {"version": VERSION, "command": "plan", "config": raw}
+    if args.objective == "roofline":
+        return _plan_roofline(args, model, cluster, cost, prof, report)
     try:
         rep = S.solve(model, cluster, prof, cost, keep_all_results=args.all_candidates)
     except S.NoFeasiblePlanError as e:
@@ -136,6 +138,28 @@ def cmd_plan(args):
                   candidates_filtered=rep.candidates_filtered)
     if rep.all_results is not None:
         report["all_candidates"] = [_result(r) for r in rep.all_results]
+    _emit(report, args)
+    return 0
+
+
+def _plan_roofline(args, model, cluster, cost, prof, report):
+    """`plan --objective roofline`: the reference's candidates ranked by the
+    engine's B200 step roofline (amsp_solve_roofline), not by T_comm."""
+    report["objective"] = {"name": "roofline", "hbm_bytes_per_s": args.hbm_bw,
+                           "nvlink_bytes_per_s": args.nvlink_bw}
+    try:
+        ranked = S.solve_roofline(model, cluster, prof, cost, args.hbm_bw, args.nvlink_bw)
+    except S.NoFeasiblePlanError as e:
+        report.update(feasible=False, error=str(e), closest=_result(e.closest()))
+        _emit(report, args)
+        return 2
+
+    def row(r, st):
+        return dict(_result(r), step_roofline=asdict(st))
+
+    report.update(feasible=True, best=row(*ranked[0]), candidates_evaluated=len(ranked))
+    if args.all_candidates:
+        report["all_candidates"] = [row(r, st) for r, st in ranked]
     _emit(report, args)
     return 0
 
@@ -217,6 +241,11 @@ def main(argv=None) -> int:
         p.add_argument("--pretty", action="store_true")
         if name == "plan":
             p.add_argument("--all-candidates", action="store_true")
+            p.add_argument("--objective", default="comm", choices=["comm", "roofline"],
+                           help="comm: the reference solver (T_comm); roofline: the B200 "
+                                "step roofline of the engine (HBM / NVLink bytes)")
+            p.add_argument("--hbm-bw", type=float, default=S.B200_HBM_BW)
+            p.add_argument("--nvlink-bw", type=float, default=S.B200_NVLINK_BW)
         if name == "simulate":
             p.add_argument("--preset", default=None)
             p.add_argument("--plan", default=None)

@@ -8,6 +8,7 @@
 #include "amsp/plan.hpp"
 #include "amsp_c.h"
 #include "engine/layout.h"
+#include "engine/roofline.h"
 #include "convert.h"
 #include "status.h"
 
@@ -33,6 +34,10 @@ amsp_time_t time_out(const TimeBreakdown& t) {
 
 amsp_memory_t mem_out(const MemoryBreakdown& m) {
   return {m.d_params, m.d_grads, m.d_os, m.d_modelstate, m.d_activation, m.d_tmp, m.d_total};
+}
+
+amsp_step_roofline_t step_out(const amsp::StepTraffic& t) {
+  return {t.owned, t.hbm, t.nvl_in, t.nvl_out, t.t_hbm, t.t_nvlink, t.t_step};
 }
 
 amsp_plan_result_t result_out(const PlanResult& r) {
@@ -293,6 +298,56 @@ int amsp_pshard_layout(const uint64_t* tensor_sizes, int n_tensors, int sp, int 
       if (os) os[i] = L.segs[i].os;
       if (dst) dst[i] = L.segs[i].dst;
       if (len) len[i] = L.segs[i].len;
+    }
+  });
+}
+
+int amsp_step_roofline(const uint64_t* tensor_sizes, int n_tensors, const amsp_plan_t* plan,
+                       amsp_mesh_t dp, int rank, int layout, int gathers, double hbm_bw,
+                       double nvlink_bw, int* slowest, amsp_step_roofline_t* out) {
+  return amsp::guarded([&] {
+    if (n_tensors < 1 || !tensor_sizes || !plan || !out) throw Error("null argument");
+    const std::vector<std::uint64_t> t(tensor_sizes, tensor_sizes + n_tensors);
+    const ShardingPlan p = plan_in(plan);
+    int who = rank;
+    const amsp::StepTraffic s =
+        rank < 0 ? amsp::step_traffic_max(t, p, mesh_in(dp), layout, gathers, hbm_bw,
+                                          nvlink_bw, &who)
+                 : amsp::step_traffic(t, p, mesh_in(dp), rank, layout, gathers, hbm_bw,
+                                      nvlink_bw);
+    if (slowest) *slowest = who;
+    *out = step_out(s);
+  });
+}
+
+int amsp_model_tensors(const amsp_model_t* model, uint64_t* sizes, int cap, int* n) {
+  return amsp::guarded([&] {
+    const std::vector<std::uint64_t> t = amsp::model_tensors(model_in(model));
+    if (n) *n = static_cast<int>(t.size());
+    for (int i = 0; sizes && i < cap && i < static_cast<int>(t.size()); ++i) sizes[i] = t[i];
+  });
+}
+
+int amsp_solve_roofline(const amsp_model_t* model, const amsp_cluster_t* cluster,
+                        const amsp_profile_t* profile, const amsp_cost_config_t* cfg,
+                        double hbm_bw, double nvlink_bw, int layout, amsp_plan_result_t* best,
+                        amsp_step_roofline_t* best_step, amsp_plan_result_t* all,
+                        amsp_step_roofline_t* all_steps, int cap, int* n_all) {
+  return amsp::guarded([&] {
+    if (!profile) throw Error("null profile");
+    try {
+      const auto r = amsp::solve_roofline(model_in(model), cluster_in(cluster), profile->p,
+                                          cost_in(cfg), hbm_bw, nvlink_bw, layout);
+      if (best) *best = result_out(r.front().result);
+      if (best_step) *best_step = step_out(r.front().step);
+      if (n_all) *n_all = static_cast<int>(r.size());
+      for (int i = 0; i < cap && i < static_cast<int>(r.size()); ++i) {
+        if (all) all[i] = result_out(r[i].result);
+        if (all_steps) all_steps[i] = step_out(r[i].step);
+      }
+    } catch (const NoFeasiblePlanError& e) {
+      if (best) *best = result_out(e.closest());
+      throw;
     }
   });
 }

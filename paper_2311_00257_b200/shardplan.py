@@ -396,6 +396,74 @@ def solve(model: ModelSpec, cluster: ClusterSpec, profile: BandwidthProfile,
     return SearchReport(PlanResult._from(best), ev.value, fi.value, all_results)
 
 
+# ----------------------------------------------------------- B200 roofline
+# Not part of the reference API: the engine's step roofline and the solver
+# that ranks the reference's candidates by it (engine/roofline.h).
+
+B200_HBM_BW = 6524e9     # MEASURED_PEAKS.json copy bandwidth (bytes/s)
+B200_NVLINK_BW = 770e9   # measured peer copy per direction (B200_PROFILING.md)
+LAYOUTS = {"greedy": 0, "contiguous": 1}
+
+
+@dataclass
+class StepRoofline:
+    owned: int
+    hbm_bytes: int
+    nvlink_in_bytes: int
+    nvlink_out_bytes: int
+    t_hbm: float
+    t_nvlink: float
+    t_step: float
+
+    @staticmethod
+    def _from(r: N.StepRoofline) -> "StepRoofline":
+        return StepRoofline(r.owned, r.hbm_bytes, r.nvlink_in_bytes, r.nvlink_out_bytes,
+                            r.t_hbm, r.t_nvlink, r.t_step)
+
+
+def model_tensors(model: ModelSpec) -> list:
+    m, _keep = model._c()
+    n = C.c_int()
+    _call(N.lib().amsp_model_tensors, C.byref(m), None, 0, C.byref(n))
+    arr = (C.c_uint64 * max(n.value, 1))()
+    _call(N.lib().amsp_model_tensors, C.byref(m), arr, n.value, C.byref(n))
+    return list(arr)[:n.value]
+
+
+def step_roofline(tensors, plan: ShardingPlan, dp: DeviceMesh, rank: int = -1,
+                  layout: str = "greedy", gathers: int = 2, hbm_bw: float = B200_HBM_BW,
+                  nvlink_bw: float = B200_NVLINK_BW):
+    """(StepRoofline, rank) of one engine step; rank -1 = the slowest rank."""
+    if isinstance(tensors, ModelSpec):
+        tensors = model_tensors(tensors)
+    arr = (C.c_uint64 * len(tensors))(*tensors)
+    p = plan._c()
+    who, out = C.c_int(), N.StepRoofline()
+    _call(N.lib().amsp_step_roofline, arr, len(tensors), C.byref(p), dp._c(), rank,
+          LAYOUTS[layout], gathers, hbm_bw, nvlink_bw, C.byref(who), C.byref(out))
+    return StepRoofline._from(out), who.value
+
+
+def solve_roofline(model: ModelSpec, cluster: ClusterSpec, profile: BandwidthProfile,
+                   cfg: CostConfig = CostConfig(), hbm_bw: float = B200_HBM_BW,
+                   nvlink_bw: float = B200_NVLINK_BW, layout: str = "greedy"):
+    """[(PlanResult, StepRoofline)] fastest B200 step first (amsp_solve_roofline)."""
+    m, _keep = model._c()
+    cl, c = cluster._c(), cfg._c()
+    best, bstep, n_all = N.PlanResult(), N.StepRoofline(), C.c_int()
+    cap = 4096
+    allr, alls = (N.PlanResult * cap)(), (N.StepRoofline * cap)()
+    code = N.lib().amsp_solve_roofline(C.byref(m), C.byref(cl), profile._h, C.byref(c), hbm_bw,
+                                       nvlink_bw, LAYOUTS[layout], C.byref(best),
+                                       C.byref(bstep), allr, alls, cap, C.byref(n_all))
+    if code == N.AMSP_EINFEASIBLE:
+        raise NoFeasiblePlanError(code, N.lib().amsp_last_error().decode(),
+                                  PlanResult._from(best))
+    N.check(code)
+    return [(PlanResult._from(allr[i]), StepRoofline._from(alls[i]))
+            for i in range(min(n_all.value, cap))]
+
+
 def simulate(model: ModelSpec, cluster: ClusterSpec, plan: ShardingPlan,
              profile: BandwidthProfile, cfg: CostConfig = CostConfig(),
              sim: SimConfig = SimConfig(), with_trace: bool = False) -> SimResult:

@@ -97,3 +97,21 @@ def test_import_profile_roundtrip(tmp_path):
                                                        "gpu_memory_capacity": 180e9,
                                                        "dp_mesh": [4, 1]}))
     assert rc == 0 and json.loads(out2)["best"]["plan"]
+
+
+def test_plan_roofline_objective(tmp_path):
+    """`plan --objective roofline` ranks the same candidates by the B200 step
+    roofline: on 8 B200s (180 GB) it picks a plan that shards the optimizer
+    state over all 8 GPUs, where the reference objective keeps the replica."""
+    c = cfg(tmp_path, cluster={"gpus_per_node": 8, "node_count": 1,
+                               "gpu_memory_capacity": 180e9, "dp_mesh": [8, 1]})
+    rc, out, _ = run("plan", "--config", c, "--objective", "roofline", "--all-candidates")
+    assert rc == 0
+    rep = json.loads(out)
+    assert rep["objective"]["name"] == "roofline"
+    best = rep["best"]
+    assert best["plan"].endswith("os=8x1") and best["plan"].startswith("p=1x1")
+    steps = [r["step_roofline"]["t_step"] for r in rep["all_candidates"]]
+    assert steps == sorted(steps) and best["step_roofline"]["t_step"] == steps[0]
+    rc, out, _ = run("plan", "--config", c)
+    assert rc == 0 and json.loads(out)["best"]["plan"] != best["plan"]

@@ -140,6 +140,9 @@ def main():
         pick = str(report.best.plan)
         pick_row = next((r for r in measured if r["plan"] == pick), None)
         ext = min(measured, key=lambda r: r["extended_pred_ms"])
+        # the native roofline solver (amsp_solve_roofline) on the same inputs
+        roof_pick = str(S.solve_roofline(model, cl, prof)[0][0].plan)
+        roof_row = next((r for r in measured if r["plan"] == roof_pick), None)
         res = {"mesh": ms, "model": args.model, "phi": model.total_params,
                "profile": args.profile or "synthetic B200 alpha-beta",
                "combos": len(rows), "valid": sum(1 for r in rows if r["valid"]),
@@ -149,6 +152,9 @@ def main():
                "pick_overlap_ms": pick_row and pick_row["overlap_step_ms"],
                "best_overlap_ms": best["overlap_step_ms"],
                "pick_vs_best": pick_row and round(pick_row["overlap_step_ms"] / best["overlap_step_ms"], 4),
+               "roofline_pick": roof_pick,
+               "roofline_pick_vs_best": roof_row and round(
+                   roof_row["overlap_step_ms"] / best["overlap_step_ms"], 4),
                "extended_pick": ext["plan"],
                "extended_pick_vs_best": round(ext["overlap_step_ms"] / best["overlap_step_ms"], 4),
                "rows": rows}
