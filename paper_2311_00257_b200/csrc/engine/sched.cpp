@@ -481,9 +481,10 @@ struct amsp_sched {
       a.exp_avg = e->exp_avg;
       a.exp_avg_sq = e->exp_avg_sq;
       a.s = scalars;
-      // the engine's single-rank choice: TMA (1 CTA / SM) when aligned, else LDG
+      // the engine's single-rank choice (W = 1 auto): the 3-stage TMA ring,
+      // 1 CTA / SM, when aligned, else LDG
       const bool tma = e->variant >= 5;
-      ck(amsp::launch_fused_step(a, 1, tma ? e->sms : e->sms * 2, tma ? e->variant : 4, main),
+      ck(amsp::launch_fused_step(a, 1, tma ? e->sms : e->sms * 2, tma ? 5 : 4, main),
          "local optimizer");
       ++e->launches;
       return;
