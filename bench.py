@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference", "library"])
     ap.add_argument("--model", default="llama-7b")
     ap.add_argument("--plan", default="zero1",
-                    help="zero1 (P/G replica, OS over dp) | replica | 'p=AxB,g=AxB,os=AxB'")
+                    help="zero1 (P/G replica, OS over dp) | replica | zero3 | roofline (the "
+                         "native B200 roofline solver's pick) | 'p=AxB,g=AxB,os=AxB'")
     ap.add_argument("--mesh", default=None, help="dp mesh per_node x nodes, default Nx1")
     ap.add_argument("--layout", default="greedy", choices=["greedy", "contiguous"])
     ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (0 auto)")
@@ -99,6 +100,13 @@ def plan_of(args, S, dp):
         return S.ShardingPlan()
     if args.plan == "zero3":
         return S.ShardingPlan(dp, dp, dp)
+    if args.plan == "roofline":
+        # the native B200 roofline solver's pick (amsp_solve_roofline) for this
+        # model on this mesh of 180 GB B200s
+        from paper_2311_00257_b200.engine import b200_profile
+        cl = S.ClusterSpec(dp.per_node, dp.nodes, 180_000_000_000, dp,
+                           S.Topology(dp.nodes, 1, 1.0))
+        return S.solve_roofline(S.model(args.model), cl, b200_profile())[0][0].plan
     parts = dict(kv.split("=") for kv in args.plan.split(","))
     return S.ShardingPlan(mesh_of(parts["p"], S), mesh_of(parts["g"], S), mesh_of(parts["os"], S))
 

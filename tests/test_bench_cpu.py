@@ -46,3 +46,15 @@ def test_reference_arm_under_torchrun_rank0_only():
     lines = _lines(r.stdout)
     assert len(lines) == 1
     _check(lines[0], 2)
+
+
+def test_reference_arm_reports_the_roofline_solver_plan():
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1",
+                        "--warmup", "1", "--gpus", "1", "--mesh", "4x1", "--plan", "roofline"],
+                       cwd=REPO, capture_output=True, text=True, timeout=300,
+                       env={**os.environ, "WORLD_SIZE": "1"})
+    # --mesh 4x1 with one process: the plan is still resolved for the 4-GPU mesh
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = _lines(r.stdout)[0]
+    assert line["config"]["plan"] == "p=1x1,g=1x1,os=4x1"
+    assert line["config"]["dp_mesh"] == "4x1"
