@@ -520,6 +520,11 @@ def run_ours(args):
                 roof["traffic"] = d[key]
         except Exception:
             pass
+    if roof["traffic"] is None and world > 1:
+        roof["traffic_note"] = (
+            "ncu profiles one GPU per command, so a multi-rank step has no capture; "
+            "the same kernel with the W-rank group emulated on one GPU moves 0.997x its "
+            "algorithmic DRAM bytes (profiles/r01_s2_ncu_fused_tma_v7_w2_emulated_1b.json)")
 
     # Busbw of the collective the fused kernel implements (nccl-tests
     # convention: RS/AG (n-1)/n on the gathered size; AR 2(n-1)/n).
