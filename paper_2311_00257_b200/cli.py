@@ -5,6 +5,8 @@
   python -m paper_2311_00257_b200.cli simulate  --config run.json [--preset NAME | --plan SPEC]
                                                 [--overlap TIER] [--trace trace.json]
   python -m paper_2311_00257_b200.cli compare   --config run.json
+  python -m paper_2311_00257_b200.cli roofline  --config run.json [--preset NAME | --plan SPEC]
+  python -m paper_2311_00257_b200.cli plan      --config run.json --objective roofline
   python -m paper_2311_00257_b200.cli import-profile profile.csv out.json
 
 Exit codes: 0 ok, 1 configuration / profile error, 2 no
@@ -164,6 +166,36 @@ def _plan_roofline(args, model, cluster, cost, prof, report):
     return 0
 
 
+def cmd_roofline(args):
+    """Per-rank algorithmic bytes and the B200 roofline step time of one
+    engine step for a plan (default: the reference solver's pick), e.g. the
+    8-GPU projections of DESIGN.md."""
+    raw, model, cluster, cost, sim = load_config(args.config)
+    if args.preset:
+        plan = S.preset(args.preset, cluster)
+    elif args.plan:
+        plan = parse_plan(args.plan)
+    else:
+        plan = S.solve(model, cluster, load_profile(args.profile or raw.get("profile_path")),
+                       cost).best.plan
+    v = S.validate_plan(plan, cluster)
+    if not v.ok():
+        raise ConfigError("plan " + str(plan) + " violates " +
+                          "; ".join(f"{x.constraint} ({x.detail})" for x in v.violations))
+    tensors = S.model_tensors(model)
+    dp = cluster.dp_mesh
+    ranks = [asdict(S.step_roofline(tensors, plan, dp, r, gathers=args.gathers,
+                                    hbm_bw=args.hbm_bw, nvlink_bw=args.nvlink_bw)[0])
+             for r in range(dp.size())]
+    worst, who = S.step_roofline(tensors, plan, dp, gathers=args.gathers, hbm_bw=args.hbm_bw,
+                                 nvlink_bw=args.nvlink_bw)
+    _emit({"version": VERSION, "command": "roofline", "config": raw, "plan": str(plan),
+           "hbm_bytes_per_s": args.hbm_bw, "nvlink_bytes_per_s": args.nvlink_bw,
+           "params": sum(tensors), "slowest_rank": who, "step": asdict(worst),
+           "params_per_s_bound": sum(tensors) / worst.t_step, "ranks": ranks}, args)
+    return 0
+
+
 def cmd_simulate(args):
     raw, model, cluster, cost, sim = load_config(args.config)
     prof = load_profile(args.profile or raw.get("profile_path"))
@@ -233,7 +265,7 @@ def cmd_import_profile(args):
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="amsp")
     sub = ap.add_subparsers(dest="cmd", required=True)
-    for name in ("plan", "simulate", "compare"):
+    for name in ("plan", "simulate", "compare", "roofline"):
         p = sub.add_parser(name)
         p.add_argument("--config", required=True)
         p.add_argument("--profile", default=None)
@@ -246,9 +278,14 @@ def main(argv=None) -> int:
                                 "step roofline of the engine (HBM / NVLink bytes)")
             p.add_argument("--hbm-bw", type=float, default=S.B200_HBM_BW)
             p.add_argument("--nvlink-bw", type=float, default=S.B200_NVLINK_BW)
-        if name == "simulate":
+        if name in ("simulate", "roofline"):
             p.add_argument("--preset", default=None)
             p.add_argument("--plan", default=None)
+        if name == "roofline":
+            p.add_argument("--gathers", type=int, default=2)
+            p.add_argument("--hbm-bw", type=float, default=S.B200_HBM_BW)
+            p.add_argument("--nvlink-bw", type=float, default=S.B200_NVLINK_BW)
+        if name == "simulate":
             p.add_argument("--overlap", default=None, choices=S.SimConfig.TIERS)
             p.add_argument("--trace", default=None)
     p = sub.add_parser("import-profile")
@@ -257,7 +294,7 @@ def main(argv=None) -> int:
     args = ap.parse_args(argv)
     try:
         return {"plan": cmd_plan, "simulate": cmd_simulate, "compare": cmd_compare,
-                "import-profile": cmd_import_profile}[args.cmd](args)
+                "roofline": cmd_roofline, "import-profile": cmd_import_profile}[args.cmd](args)
     except (ConfigError, N.InvalidConfig, S.InfeasibleError, KeyError, ValueError,
             TypeError) as e:
         print(f"error: {e}", file=sys.stderr)

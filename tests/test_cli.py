@@ -115,3 +115,30 @@ def test_plan_roofline_objective(tmp_path):
     assert steps == sorted(steps) and best["step_roofline"]["t_step"] == steps[0]
     rc, out, _ = run("plan", "--config", c)
     assert rc == 0 and json.loads(out)["best"]["plan"] != best["plan"]
+
+
+def test_roofline_command_projects_the_8_gpu_configs(tmp_path):
+    """`roofline` on the BASELINE 8xB200 configs: 7B ZeRO-1 and the partial
+    plan (G/OS over the 2x4 mesh) move identical bytes (23.7 GB/dir NVLink,
+    bound 30.8 ms); 13B ZeRO-3 is bound by 68.3 GB/dir."""
+    c = cfg(tmp_path, cluster={"gpus_per_node": 8, "node_count": 1,
+                               "gpu_memory_capacity": 180e9, "dp_mesh": [8, 1]})
+    rc, out, _ = run("roofline", "--config", c, "--plan", "p=1x1,g=1x1,os=8x1")
+    assert rc == 0
+    z1 = json.loads(out)
+    assert len(z1["ranks"]) == 8 and z1["params"] == 6738415616
+    assert abs(z1["step"]["t_step"] - 0.03076) < 1e-4
+    assert z1["step"]["nvlink_in_bytes"] == max(r["nvlink_in_bytes"] for r in z1["ranks"])
+    c2 = cfg(tmp_path, cluster={"gpus_per_node": 2, "node_count": 4,
+                                "gpu_memory_capacity": 180e9, "dp_mesh": [2, 4]})
+    rc, out, _ = run("roofline", "--config", c2, "--plan", "p=1x1,g=2x4,os=2x4")
+    assert rc == 0 and json.loads(out)["step"]["t_step"] == z1["step"]["t_step"]
+    c3 = cfg(tmp_path, model={"llama": "llama-13b"},
+             cluster={"gpus_per_node": 8, "node_count": 1, "gpu_memory_capacity": 180e9,
+                      "dp_mesh": [8, 1]})
+    rc, out, _ = run("roofline", "--config", c3, "--preset", "ZeRO-3")
+    z3 = json.loads(out)
+    assert rc == 0 and z3["plan"] == "p=8x1,g=8x1,os=8x1"
+    assert z3["step"]["nvlink_in_bytes"] == 68333287680
+    rc, _, err = run("roofline", "--config", c, "--plan", "p=1x1,g=4x1,os=8x1")
+    assert rc == 1 and "violates" in err
