@@ -303,6 +303,51 @@ def test_overlap_scheduler_bit_exact(cuda, world, p, os_k, tier, opt_overlap, ga
         e.close()
 
 
+@pytest.mark.parametrize("world,p,os_k,tier,opt_overlap,compute", [
+    (2, 2, 2, "ag_rs_ar_bc", True, "standin"), (4, 4, 4, "ag_rs", False, "standin"),
+    (4, 2, 4, "ag_rs_ar_bc", True, "standin"), (2, 1, 2, "ag_rs_ar_bc", False, "standin")])
+def test_overlap_scheduler_recompute_graph(cuda, world, p, os_k, tier, opt_overlap, compute):
+    """Activation recompute (SimConfig.recompute; overlap_sim.cpp:390-416):
+    the graph re-gathers each layer before its RecomputeFwd and keeps it for
+    the backward. The scheduler replays that graph (recompute events run as
+    compute, the extra all-gathers as NVLink gathers) and the step stays
+    bit-exact with the oracle."""
+    from paper_2311_00257_b200.engine import Scheduler, b200_profile
+    model = S.model("tiny", seq_len=256)
+    plan = S.ShardingPlan(M(p, 1), M(p, 1) if os_k == p else M(os_k, 1), M(os_k, 1))
+    engines = [Engine(model, plan, M(world, 1), rank=r, skip_gathers=True) for r in range(world)]
+    if world > 1:
+        link_local(engines)
+    sim = S.SimConfig(overlap_tier=tier, recompute=True, peak_flops_per_gpu=1e18)
+    plain = S.SimConfig(overlap_tier=tier, recompute=False, peak_flops_per_gpu=1e18)
+    cost = S.CostConfig(bucket_size=1 << 20)
+    scheds = [Scheduler(e, model, b200_profile(), cost, sim, optimizer_overlap=opt_overlap,
+                        compute=compute) for e in engines]
+    ref = Scheduler(engines[0], model, b200_profile(), cost, plain,
+                    optimizer_overlap=opt_overlap)
+    assert scheds[0].info.n_compute > ref.info.n_compute  # RecomputeFwd events
+    if p > 1:
+        assert scheds[0].info.n_gather >= ref.info.n_gather
+    ref.close()
+    for e in engines:
+        e.init_state()
+    steps = 3
+    for t in range(1, steps + 1):
+        for e in engines:
+            e.synth_grads(t)
+        for sc in scheds:
+            sc.step(t)
+    for sc in scheds:
+        sc.flush()
+    want = O.trajectory_range(0, engines[0].info.total_params, DEFAULT_SEED, steps, world, H)
+    for e in engines:
+        _check_rank(e, want, steps)
+    for sc in scheds:
+        sc.close()
+    for e in engines:
+        e.close()
+
+
 @pytest.mark.parametrize("world,p", [(1, 1), (2, 1), (2, 2)])
 def test_scheduler_real_gemm_compute(cuda, world, p):
     """compute='gemm': linear modules run cuBLAS GEMMs of their true shapes,
