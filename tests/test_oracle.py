@@ -77,6 +77,41 @@ def test_oracle_matches_numpy_restatement(world):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_oracle_agrees_with_torch_adamw(world):
+    """Independent check of the oracle's update against torch.optim.AdamW
+    (single-tensor fp32 CPU path; the optimizer a PyTorch executor such as the
+    paper's InternEvo would run) on the same fp32-reduced gradients. Its
+    operation order differs (lerp for m, sqrt(v)/sqrt(bc2) for the
+    denominator), so agreement is to the north-star tolerance (1e-5 relative
+    on master, m and v after 10 steps, with small absolute floors for values
+    that pass through zero), not bit-exact."""
+    import torch
+    n, steps = 1 << 14, 10
+    start = 6_000_000_000  # inside the 7B flat index space
+    h = O.hyper()
+    want = O.trajectory_range(start, n, SEED, steps, world, h)
+    p0 = np.array([O.master_init(SEED, start + i) for i in range(n)], np.float32)
+    param = torch.nn.Parameter(torch.from_numpy(p0.copy()))
+    opt = torch.optim.AdamW([param], lr=h.lr, betas=(h.beta1, h.beta2), eps=h.eps,
+                            weight_decay=h.weight_decay, foreach=False, fused=False)
+    for t in range(1, steps + 1):
+        g = None
+        for r in range(world):  # fixed rank order, fp32 sum, then 1/W (exact here)
+            gr = (O.grads(start, n, SEED, t, r).astype(np.uint32) << 16).view(np.float32)
+            g = gr.copy() if g is None else (g + gr).astype(np.float32)
+        param.grad = torch.from_numpy((g * np.float32(1.0 / world)).astype(np.float32))
+        opt.step()
+    st = opt.state[param]
+    np.testing.assert_allclose(param.detach().numpy(), want[0], rtol=1e-5, atol=1e-5 * h.lr)
+    # moments: relative, with a floor of 1e-6 of the gradient scale (|g| <= 2^-7)
+    # for moments that pass through zero
+    gmax = 2.0 ** -7
+    np.testing.assert_allclose(st["exp_avg"].numpy(), want[1], rtol=1e-5, atol=1e-6 * gmax)
+    np.testing.assert_allclose(st["exp_avg_sq"].numpy(), want[2], rtol=1e-5,
+                               atol=1e-6 * gmax * gmax)
+
+
 def test_gradient_definition():
     g = O.grads(0, 100000, SEED, 3, 1).astype(np.uint32) << 16
     f = g.view(np.float32)
