@@ -1,3 +1,7 @@
+// API declarations derived from the `shardplan` reference headers
+// (proj/include/shardplan/*.hpp), Copyright 2026 The Shardplan Authors,
+// Apache License 2.0; see NOTICE.
+//
 // amsp/plan.hpp — the planner-side API of the AMSP model-state pipeline.
 //
 // Drop-in for the reference `shardplan` library (arXiv 2311.00257 artifact,

@@ -104,6 +104,9 @@ struct amsp_engine {
   // rank's step is ordered after every rank's gradient production.
   cudaStream_t shared_default = nullptr;
   uint32_t epoch = 0;
+  // Epoch of the scheduler barriers (ids >= 16), shared by every scheduler
+  // of this engine so that a flag word never goes backwards (amsp_sched).
+  uint32_t sched_epoch = 0;
   // Optional CUDA-event bracketing of every fused launch (bench roofline).
   bool time_kernel = false;
   using EventPairs = std::vector<std::pair<cudaEvent_t, cudaEvent_t>>;

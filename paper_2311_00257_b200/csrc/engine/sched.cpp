@@ -401,7 +401,10 @@ struct amsp_sched {
     const bool with_comm = mode == 1, local_optimizer = mode == 2;
     if (step < 1) throw Error("sched: step index must be >= 1");
     e->require_peers();
-    ++epoch;
+    // Barrier ids >= kFirstSchedBarrier live in the engine's flag block and
+    // are reused by every scheduler created on this engine: the epoch must
+    // keep growing across schedulers, so it is the engine's counter.
+    epoch = ++e->sched_epoch;
     scalars = amsp::make_adam_scalars(e->cfg.lr, e->cfg.beta1, e->cfg.beta2, e->cfg.eps,
                                       e->cfg.weight_decay, step, 1.0 / e->world);
     ck(cudaEventRecord(start_ev, main), "event record");
@@ -507,7 +510,7 @@ struct amsp_sched {
   void flush(cudaStream_t main) {
     if (!mirror) return;
     e->require_peers();
-    ++epoch;
+    epoch = ++e->sched_epoch;
     for (std::size_t j = 0; j < bc_copies.size(); ++j) broadcast(static_cast<int>(j), main);
     barrier(flush_barrier, main);
   }
