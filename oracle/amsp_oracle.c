@@ -34,6 +34,28 @@
  * Every operation is a single IEEE-754 binary32 op (compiled with
  * -ffp-contract=off); the step scalars are computed in double and rounded
  * once to float by amsp_o_adam_scalars().
+ *
+ * Micro-batches and gradient sharding (the reference
+ * charges them as T_g, cost_model.cpp:119-126, emits one AllReduceBucket per
+ * bucket of every non-last micro-batch when s_g > s_p, overlap_sim.cpp:
+ * 320-330, and stores D_g = b_g*Phi/s_g bytes, cost_model.cpp:151):
+ *   grad[r,mu,t,i] = bf16_rne(2^-7 * u(seed ^ t<<48 ^ mu<<44 ^ r<<40 ^ i))
+ *                    (mu = 0 is the single-micro-batch definition above)
+ *   scale          = fp32(1 / (W*M))
+ *   s_g = 1  ("in place"): every rank accumulates its own gradient in its
+ *            full bf16 gradient buffer over all M micro-batches,
+ *              acc_r = grad[r,0];  acc_r = bf16(acc_r + grad[r,mu]), mu >= 1
+ *            and the step reduces   g = ((acc_0 + acc_1) + ...) * scale.
+ *   s_g > 1  ("staged"): micro-batches 0..M-2 are reduced inside each
+ *            accumulation block (the ranks of one G-mesh block; = the P-mesh
+ *            block when s_g = s_p) into the block's bf16 G shard:
+ *              mu = 0:  acc_b = bf16(grad[m0] + grad[m1] + ...)
+ *              mu > 0:  acc_b = bf16(((acc_b + grad[m0]) + grad[m1]) + ...)
+ *            (members m0 < m1 < ... of block b), and the step reduces the
+ *            block accumulators in block order, then the raw last
+ *            micro-batch of every rank in rank order:
+ *              g = ((((acc_b0 + acc_b1) + ...) + grad[0,M-1]) + ... + grad[W-1,M-1]) * scale
+ *   With M = 1 both reduce to the flat rank-order sum above.
  */
 #include <math.h>
 #include <stddef.h>
@@ -85,10 +107,16 @@ float amsp_o_bf16_to_f32(uint16_t h) {
   return f;
 }
 
+uint16_t amsp_o_grad_bf16_mb(uint64_t seed, uint32_t step, uint32_t micro_batch,
+                             uint32_t rank, uint64_t index) {
+  uint64_t key = seed ^ ((uint64_t)step << 48) ^ ((uint64_t)micro_batch << 44) ^
+                 ((uint64_t)rank << 40) ^ index;
+  return amsp_o_f32_to_bf16(unit(key) * 0.0078125f);
+}
+
 uint16_t amsp_o_grad_bf16(uint64_t seed, uint32_t step, uint32_t rank,
                           uint64_t index) {
-  uint64_t key = seed ^ ((uint64_t)step << 48) ^ ((uint64_t)rank << 40) ^ index;
-  return amsp_o_f32_to_bf16(unit(key) * 0.0078125f);
+  return amsp_o_grad_bf16_mb(seed, step, 0, rank, index);
 }
 
 float amsp_o_master_init(uint64_t seed, uint64_t index) {
@@ -123,18 +151,61 @@ void amsp_o_adam_elem(const amsp_o_scalars* s, float g, float* p, float* m,
   *p = pp;
 }
 
-/* sc[t-1] = amsp_o_adam_scalars(..., t, world): hoisted out of the element
+static float gf(uint64_t seed, int t, int mb, int r, uint64_t i) {
+  return amsp_o_bf16_to_f32(amsp_o_grad_bf16_mb(seed, (uint32_t)t, (uint32_t)mb, (uint32_t)r, i));
+}
+
+static uint16_t accumulate(float acc, float g) { return amsp_o_f32_to_bf16(acc + g); }
+
+/* Unscaled fp32 gradient of element i at step t under the accumulation
+ * recipe `a` (NULL: one micro-batch, flat rank-order sum over `world`). */
+float amsp_o_reduced_grad(uint64_t seed, int t, uint64_t i, int world, const amsp_o_accum* a) {
+  const int M = a ? a->micro_batches : 1;
+  if (M <= 1) {
+    float g = gf(seed, t, 0, 0, i);
+    for (int r = 1; r < world; ++r) g = g + gf(seed, t, 0, r, i);
+    return g;
+  }
+  if (!a->staged) {
+    float g = 0.0f;
+    for (int r = 0; r < world; ++r) {
+      uint16_t acc = amsp_o_grad_bf16_mb(seed, (uint32_t)t, 0, (uint32_t)r, i);
+      for (int mb = 1; mb < M; ++mb)
+        acc = accumulate(amsp_o_bf16_to_f32(acc), gf(seed, t, mb, r, i));
+      g = r == 0 ? amsp_o_bf16_to_f32(acc) : g + amsp_o_bf16_to_f32(acc);
+    }
+    return g;
+  }
+  float g = 0.0f;
+  for (int b = 0; b < a->nblocks; ++b) {
+    uint16_t acc = 0;
+    for (int mb = 0; mb + 1 < M; ++mb) {
+      float s = 0.0f;
+      int first = 1;
+      for (int r = 0; r < world; ++r) {
+        if (a->block_of[r] != b) continue;
+        const float x = gf(seed, t, mb, r, i);
+        if (first) s = mb == 0 ? x : amsp_o_bf16_to_f32(acc) + x;
+        else s = s + x;
+        first = 0;
+      }
+      acc = amsp_o_f32_to_bf16(s);
+    }
+    g = b == 0 ? amsp_o_bf16_to_f32(acc) : g + amsp_o_bf16_to_f32(acc);
+  }
+  for (int r = 0; r < world; ++r) g = g + gf(seed, t, M - 1, r, i);
+  return g;
+}
+
+/* sc[t-1] = amsp_o_adam_scalars(..., t, world*M): hoisted out of the element
  * loop (two pow() per step dominated the per-element cost); same values. */
 static void one_index(uint64_t i, uint64_t seed, int steps, int world,
-                      const amsp_o_scalars* sc, float* mo, float* mmo, float* vo,
-                      uint16_t* po) {
+                      const amsp_o_accum* a, const amsp_o_scalars* sc, float* mo,
+                      float* mmo, float* vo, uint16_t* po) {
   float p = amsp_o_master_init(seed, i), m = 0.0f, v = 0.0f;
   for (int t = 1; t <= steps; ++t) {
     const amsp_o_scalars* s = &sc[t - 1];
-    float g = amsp_o_bf16_to_f32(amsp_o_grad_bf16(seed, (uint32_t)t, 0, i));
-    for (int r = 1; r < world; ++r)
-      g = g + amsp_o_bf16_to_f32(amsp_o_grad_bf16(seed, (uint32_t)t, (uint32_t)r, i));
-    g = g * s->grad_scale;
+    const float g = amsp_o_reduced_grad(seed, t, i, world, a) * s->grad_scale;
     amsp_o_adam_elem(s, g, &p, &m, &v);
   }
   if (mo) *mo = p;
@@ -151,27 +222,50 @@ static amsp_o_scalars* step_scalars(int steps, int world, const amsp_o_hyper* h)
   return sc;
 }
 
+static int divisor(int world, const amsp_o_accum* a) {
+  return world * (a && a->micro_batches > 1 ? a->micro_batches : 1);
+}
+
+void amsp_o_trajectory_acc(const uint64_t* index, size_t n, uint64_t seed, int steps,
+                           int world, const amsp_o_accum* a, const amsp_o_hyper* h,
+                           float* master, float* m, float* v, uint16_t* param) {
+  amsp_o_scalars* sc = step_scalars(steps, divisor(world, a), h);
+#pragma omp parallel for schedule(static)
+  for (size_t k = 0; k < n; ++k)
+    one_index(index[k], seed, steps, world, a, sc, master ? master + k : NULL,
+              m ? m + k : NULL, v ? v + k : NULL, param ? param + k : NULL);
+  free(sc);
+}
+
+void amsp_o_trajectory_range_acc(uint64_t start, size_t n, uint64_t seed, int steps,
+                                 int world, const amsp_o_accum* a, const amsp_o_hyper* h,
+                                 float* master, float* m, float* v, uint16_t* param) {
+  amsp_o_scalars* sc = step_scalars(steps, divisor(world, a), h);
+#pragma omp parallel for schedule(static)
+  for (size_t k = 0; k < n; ++k)
+    one_index(start + k, seed, steps, world, a, sc, master ? master + k : NULL,
+              m ? m + k : NULL, v ? v + k : NULL, param ? param + k : NULL);
+  free(sc);
+}
+
 void amsp_o_trajectory(const uint64_t* index, size_t n, uint64_t seed,
                        int steps, int world, const amsp_o_hyper* h,
                        float* master, float* m, float* v, uint16_t* param) {
-  amsp_o_scalars* sc = step_scalars(steps, world, h);
-#pragma omp parallel for schedule(static)
-  for (size_t k = 0; k < n; ++k)
-    one_index(index[k], seed, steps, world, sc, master ? master + k : NULL,
-              m ? m + k : NULL, v ? v + k : NULL, param ? param + k : NULL);
-  free(sc);
+  amsp_o_trajectory_acc(index, n, seed, steps, world, NULL, h, master, m, v, param);
 }
 
 void amsp_o_trajectory_range(uint64_t start, size_t n, uint64_t seed,
                              int steps, int world, const amsp_o_hyper* h,
                              float* master, float* m, float* v,
                              uint16_t* param) {
-  amsp_o_scalars* sc = step_scalars(steps, world, h);
+  amsp_o_trajectory_range_acc(start, n, seed, steps, world, NULL, h, master, m, v, param);
+}
+
+void amsp_o_fill_grads_mb(uint16_t* dst, uint64_t start, size_t n, uint64_t seed,
+                          uint32_t step, uint32_t micro_batch, uint32_t rank) {
 #pragma omp parallel for schedule(static)
   for (size_t k = 0; k < n; ++k)
-    one_index(start + k, seed, steps, world, sc, master ? master + k : NULL,
-              m ? m + k : NULL, v ? v + k : NULL, param ? param + k : NULL);
-  free(sc);
+    dst[k] = amsp_o_grad_bf16_mb(seed, step, micro_batch, rank, start + k);
 }
 
 void amsp_o_fill_grads(uint16_t* dst, uint64_t start, size_t n, uint64_t seed,

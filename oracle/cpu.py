@@ -17,6 +17,11 @@ class Scalars(C.Structure):
                                          "grad_scale")]
 
 
+class Accum(C.Structure):
+    _fields_ = [("micro_batches", C.c_int), ("staged", C.c_int), ("nblocks", C.c_int),
+                ("block_of", C.c_int * 16)]
+
+
 class Hyper(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("lr", "beta1", "beta2", "eps", "weight_decay")]
 
@@ -43,6 +48,17 @@ def lib() -> C.CDLL:
                                         C.POINTER(Hyper), fp, fp, fp, u16p]
         L.amsp_o_trajectory_range.argtypes = [C.c_uint64, C.c_size_t, C.c_uint64, C.c_int,
                                               C.c_int, C.POINTER(Hyper), fp, fp, fp, u16p]
+        L.amsp_o_trajectory_acc.argtypes = [u64p, C.c_size_t, C.c_uint64, C.c_int, C.c_int,
+                                            C.POINTER(Accum), C.POINTER(Hyper), fp, fp, fp,
+                                            u16p]
+        L.amsp_o_trajectory_range_acc.argtypes = [C.c_uint64, C.c_size_t, C.c_uint64, C.c_int,
+                                                  C.c_int, C.POINTER(Accum), C.POINTER(Hyper),
+                                                  fp, fp, fp, u16p]
+        L.amsp_o_fill_grads_mb.argtypes = [u16p, C.c_uint64, C.c_size_t, C.c_uint64,
+                                           C.c_uint32, C.c_uint32, C.c_uint32]
+        L.amsp_o_reduced_grad.restype = C.c_float
+        L.amsp_o_reduced_grad.argtypes = [C.c_uint64, C.c_int, C.c_uint64, C.c_int,
+                                          C.POINTER(Accum)]
         L.amsp_o_fill_grads.argtypes = [u16p, C.c_uint64, C.c_size_t, C.c_uint64, C.c_uint32,
                                         C.c_uint32]
         L.amsp_o_partition_greedy.argtypes = [u64p, C.c_int, C.c_int, C.POINTER(C.c_int),
@@ -70,23 +86,62 @@ def hyper(lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1) -> Hyper:
     return Hyper(lr, beta1, beta2, eps, weight_decay)
 
 
-def trajectory(index: np.ndarray, seed: int, steps: int, world: int, h: Hyper):
+def mesh_blocks(dp, mesh, world: int) -> list:
+    """block_of[rank] for the blocks of component `mesh` ((per_node, nodes))
+    tiling the DP mesh `dp`, ranks node-major (rank = node*per_node + local),
+    blocks numbered in order of their smallest rank. Restated from the
+    paper's 2-level device mesh for the checker."""
+    P, _ = dp
+    a, b = mesh
+    return [((r // P) // b) * (P // a) + (r % P) // a for r in range(world)]
+
+
+def accum(micro_batches: int, sg: int, block_of) -> Accum:
+    """Accumulation recipe: M micro-batches; s_g = 1 accumulates in place,
+    s_g > 1 through the bf16 G shards of the blocks in `block_of`."""
+    a = Accum()
+    a.micro_batches = micro_batches
+    a.staged = int(sg > 1)
+    a.nblocks = max(block_of) + 1
+    for r, blk in enumerate(block_of):
+        a.block_of[r] = blk
+    return a
+
+
+def trajectory(index: np.ndarray, seed: int, steps: int, world: int, h: Hyper,
+               acc: Accum | None = None):
     """(master, m, v, bf16 param) of the given flat indices after `steps`."""
     index = np.ascontiguousarray(index, dtype=np.uint64)
     n = index.size
     out = [np.empty(n, np.float32) for _ in range(3)] + [np.empty(n, np.uint16)]
-    lib().amsp_o_trajectory(_p(index, C.c_uint64), n, seed, steps, world, C.byref(h),
-                            _p(out[0], C.c_float), _p(out[1], C.c_float),
-                            _p(out[2], C.c_float), _p(out[3], C.c_uint16))
+    lib().amsp_o_trajectory_acc(_p(index, C.c_uint64), n, seed, steps, world,
+                                C.byref(acc) if acc is not None else None, C.byref(h),
+                                _p(out[0], C.c_float), _p(out[1], C.c_float),
+                                _p(out[2], C.c_float), _p(out[3], C.c_uint16))
     return out
 
 
-def trajectory_range(start: int, n: int, seed: int, steps: int, world: int, h: Hyper):
+def trajectory_range(start: int, n: int, seed: int, steps: int, world: int, h: Hyper,
+                     acc: Accum | None = None):
     out = [np.empty(n, np.float32) for _ in range(3)] + [np.empty(n, np.uint16)]
-    lib().amsp_o_trajectory_range(start, n, seed, steps, world, C.byref(h),
-                                  _p(out[0], C.c_float), _p(out[1], C.c_float),
-                                  _p(out[2], C.c_float), _p(out[3], C.c_uint16))
+    lib().amsp_o_trajectory_range_acc(start, n, seed, steps, world,
+                                      C.byref(acc) if acc is not None else None, C.byref(h),
+                                      _p(out[0], C.c_float), _p(out[1], C.c_float),
+                                      _p(out[2], C.c_float), _p(out[3], C.c_uint16))
     return out
+
+
+def grads_mb(start: int, n: int, seed: int, step: int, micro_batch: int,
+             rank: int) -> np.ndarray:
+    out = np.empty(n, np.uint16)
+    lib().amsp_o_fill_grads_mb(_p(out, C.c_uint16), start, n, seed, step, micro_batch, rank)
+    return out
+
+
+def reduced_grad(seed: int, step: int, index: int, world: int,
+                 acc: Accum | None = None) -> float:
+    return lib().amsp_o_reduced_grad(seed, step, index, world,
+                                     C.byref(acc) if acc is not None else None)
 
 
 def grads(start: int, n: int, seed: int, step: int, rank: int) -> np.ndarray:

@@ -269,3 +269,117 @@ def test_fullcheck_streams_every_element_and_catches_a_flip():
         bad = check_engine(Fake(), 2, 2, chunk=1 << 20, log=logs.append)
         assert len(bad) == 1 and bad[0].startswith(name), bad
         b.view(np.uint16 if name == "params" else np.uint32)[owned // 3] ^= 1
+
+
+# ---------------------------------------------------------------- micro-batches
+# Gradient accumulation over M micro-batches and gradient sharding (s_g > 1),
+# PAPER.md:316-326 / cost_model.cpp:119-126: an independent numpy restatement
+# of the recipe in the oracle's header (own splitmix64, own bf16 rounding).
+
+def _splitmix64(x: np.ndarray) -> np.ndarray:
+    z = (x + np.uint64(0x9E3779B97F4A7C15)).astype(np.uint64)
+    z = ((z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)).astype(np.uint64)
+    z = ((z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)).astype(np.uint64)
+    return z ^ (z >> np.uint64(31))
+
+
+def np_grad(idx, t, mb, r) -> np.ndarray:
+    key = (np.uint64(SEED) ^ np.uint64(t << 48) ^ np.uint64(mb << 44) ^ np.uint64(r << 40)
+           ^ idx.astype(np.uint64))
+    q = (_splitmix64(key) >> np.uint64(40)).astype(np.int64) - (1 << 23)
+    u = q.astype(np.float32) * np.float32(1.0 / 8388608.0)
+    return bf16_rne((u * np.float32(0.0078125)).astype(np.float32))
+
+
+def up(b: np.ndarray) -> np.ndarray:
+    return (b.astype(np.uint32) << 16).view(np.float32)
+
+
+def np_reduced(idx, t, world, M, staged, block_of):
+    f32 = np.float32
+    if M == 1:
+        g = up(np_grad(idx, t, 0, 0))
+        for r in range(1, world):
+            g = (g + up(np_grad(idx, t, 0, r))).astype(f32)
+        return g
+    if not staged:
+        g = None
+        for r in range(world):
+            acc = np_grad(idx, t, 0, r)
+            for mb in range(1, M):
+                acc = bf16_rne((up(acc) + up(np_grad(idx, t, mb, r))).astype(f32))
+            g = up(acc) if g is None else (g + up(acc)).astype(f32)
+        return g
+    g = None
+    for b in range(max(block_of) + 1):
+        members = [r for r in range(world) if block_of[r] == b]
+        acc = None
+        for mb in range(M - 1):
+            s = None
+            for r in members:
+                x = up(np_grad(idx, t, mb, r))
+                if s is None:
+                    s = x if mb == 0 else (up(acc) + x).astype(f32)
+                else:
+                    s = (s + x).astype(f32)
+            acc = bf16_rne(s)
+        g = up(acc) if g is None else (g + up(acc)).astype(f32)
+    for r in range(world):
+        g = (g + up(np_grad(idx, t, M - 1, r))).astype(f32)
+    return g
+
+
+ACCUM_CASES = [(2, 2, 0, [0, 1]), (4, 3, 0, [0, 1, 2, 3]),          # s_g = 1, in place
+               (2, 2, 1, [0, 0]), (4, 4, 1, [0, 0, 0, 0]),          # ZeRO-2/3, one block
+               (4, 2, 1, [0, 0, 1, 1]), (4, 3, 1, [0, 1, 0, 1]),    # replica blocks, 2-D mesh
+               (8, 2, 1, O.mesh_blocks((2, 4), (2, 4), 8)), (8, 4, 1, O.mesh_blocks((8, 1), (4, 1), 8))]
+
+
+@pytest.mark.parametrize("world,M,staged,block_of", ACCUM_CASES)
+def test_oracle_microbatch_recipe_matches_numpy(world, M, staged, block_of):
+    idx = np.concatenate([np.arange(0, 257), np.array([2**33 + 5, 13_015_864_319])]).astype(np.uint64)
+    acc = O.accum(M, 2 if staged else 1, block_of)
+    for t in (1, 3):
+        want = np_reduced(idx, t, world, M, staged, block_of)
+        got = np.array([O.reduced_grad(SEED, t, int(i), world, acc) for i in idx], np.float32)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    # micro-batch 0 is the single-micro-batch gradient (same key)
+    assert np.array_equal(O.grads_mb(10, 64, SEED, 2, 0, 1), O.grads(10, 64, SEED, 2, 1))
+    assert np.array_equal(O.grads_mb(10, 64, SEED, 2, 3, 1),
+                          np_grad(np.arange(10, 74, dtype=np.uint64), 2, 3, 1))
+
+
+def test_oracle_microbatch_one_is_flat_sum():
+    idx = np.arange(0, 500, dtype=np.uint64)
+    h = O.hyper()
+    flat = O.trajectory(idx, SEED, 3, 4, h)
+    for staged, blocks in ((0, [0, 1, 2, 3]), (1, [0, 1, 0, 1])):
+        got = O.trajectory(idx, SEED, 3, 4, h, O.accum(1, 2 if staged else 1, blocks))
+        for a, b in zip(got, flat):
+            assert np.array_equal(a, b)
+
+
+def test_oracle_microbatch_scale_and_mean():
+    """The step's gradient is the mean over W*M micro-batch gradients: with
+    M = 4 the Adam step sees scale 1/(W*M), and the staged sum is within bf16
+    accumulation error of the exact fp64 mean."""
+    idx = np.arange(0, 2000, dtype=np.uint64)
+    world, M = 2, 4
+    acc = O.accum(M, 2, [0, 0])
+    exact = sum(up(np_grad(idx, 1, mb, r)).astype(np.float64)
+                for mb in range(M) for r in range(world))
+    got = np.array([O.reduced_grad(SEED, 1, int(i), world, acc) for i in idx], np.float64)
+    assert np.max(np.abs(got - exact)) <= 2 ** -8 * np.max(np.abs(exact)) * M
+    s = O.scalars(1, world * M, O.hyper())
+    assert s.grad_scale == np.float32(1.0 / 8)
+
+
+def test_oracle_mesh_blocks_match_engine_groups():
+    """The checker's block map equals the engine's process groups."""
+    for dp, mesh in [((8, 1), (4, 1)), ((2, 4), (2, 4)), ((2, 4), (2, 2)), ((4, 2), (2, 1)),
+                     ((2, 2), (1, 2)), ((4, 1), (1, 1))]:
+        world = dp[0] * dp[1]
+        blocks = O.mesh_blocks(dp, mesh, world)
+        for r in range(world):
+            blk, _, _ = mesh_group(S.DeviceMesh(*dp), S.DeviceMesh(*mesh), r)
+            assert blk == blocks[r]
