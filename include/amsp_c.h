@@ -38,7 +38,7 @@ extern "C" {
 #define AMSP_EINFEASIBLE 2
 #define AMSP_ECUDA 3
 
-#define AMSP_ABI_VERSION 1
+#define AMSP_ABI_VERSION 2
 
 int amsp_abi_version(void);
 const char* amsp_last_error(void);
@@ -264,6 +264,15 @@ typedef struct {
                                    forward + backward parameter all-gathers
                                    itself; 1 = the caller schedules
                                    amsp_engine_gather (overlap scheduler) */
+  int micro_batches;            /* M per step (0 = 1; at most 16). With M > 1
+                                   and s_g > 1 the engine keeps the bf16 G
+                                   shard accumulator of D_g = 2*Phi/s_g bytes
+                                   (cost_model.cpp:151): micro-batches
+                                   0..M-2 go through amsp_engine_accumulate
+                                   (the T_g collectives, cost_model.cpp:
+                                   119-126), the last one through
+                                   amsp_engine_step. With s_g = 1 the
+                                   gradient buffer accumulates in place. */
 } amsp_engine_config_t;
 
 typedef struct {
@@ -284,6 +293,14 @@ typedef struct {
   int n_units;                  /* all-gather units (s_p > 1) */
   uint64_t slot_elems;          /* gathered-unit slot capacity */
   int variant;                  /* fused-kernel variant in use (see amsp_engine_tune) */
+  int micro_batches;            /* M */
+  int grad_shards;              /* s_g */
+  uint64_t acc_elems;           /* bf16 G-shard accumulator elements (0 when
+                                   M = 1 or s_g = 1): Phi/s_p when s_g = s_p,
+                                   else the OS shard (s_g = s_os) */
+  int acc_sources;              /* ranks pulled per accumulation (|G block|) */
+  int acc_holders;              /* accumulators summed by the last micro-batch */
+  uint64_t grad_elems;          /* elements of the local gradient buffer */
 } amsp_engine_info_t;
 
 #define AMSP_IPC_HANDLE_BYTES 64
@@ -311,8 +328,20 @@ int amsp_engine_link_local(amsp_engine_t* const* engines, int n);
 int amsp_engine_init_state(amsp_engine_t* e, void* stream);
 /* Synthetic bf16 gradients for this rank and step (oracle definition). */
 int amsp_engine_synth_grads(amsp_engine_t* e, int step, void* stream);
-/* One AMSP optimizer step (1-based step index) with device-resident grads:
- * cross-GPU barrier, fused reduce+AdamW+gather kernel, cross-GPU barrier. */
+/* Same for micro-batch mb of the step: written into the gradient buffer, or
+ * with s_g = 1 and mb > 0 accumulated into it in place (bf16). */
+int amsp_engine_synth_grads_mb(amsp_engine_t* e, int step, int mb, void* stream);
+/* Micro-batch mb < M-1 of the step is complete in every rank's gradient
+ * buffer: with s_g > 1, cross-GPU barrier, fold it into the G shard
+ * accumulators (each holder pulls its accumulation block's bf16 gradients
+ * over NVLink: the reduce-scatter / AllReduce + select & drop of
+ * PAPER.md:320-326 as one pass), barrier (the buffer may be overwritten).
+ * With s_g = 1 a no-op (the producer accumulates in place). */
+int amsp_engine_accumulate(amsp_engine_t* e, int step, int mb, void* stream);
+/* One AMSP optimizer step (1-based step index) with device-resident grads
+ * (the last micro-batch when M > 1): cross-GPU barrier, fused reduce (of the
+ * accumulators, then the raw gradients; scale 1/(W*M)) + AdamW + gather
+ * kernel, cross-GPU barrier. */
 int amsp_engine_step(amsp_engine_t* e, int step, void* stream);
 /* Same step through host buffers: H2D of this rank's bf16 gradients
  * (total_params elements; pinned for async), the step, and D2H of the step
@@ -324,7 +353,7 @@ int amsp_engine_step_host(amsp_engine_t* e, int step, const void* host_grads,
 int amsp_engine_stats(amsp_engine_t* e, float* stats2);
 /* Copy `count` elements at `offset` of a buffer to host (synchronous).
  * which: 0 grads(bf16) 1 params(bf16, the P shard) 2 master 3 exp_avg
- * 4 exp_avg_sq 5/6 gathered slot 0/1 (bf16). */
+ * 4 exp_avg_sq 5/6 gathered slot 0/1 (bf16) 7 G-shard accumulator (bf16). */
 int amsp_engine_read(amsp_engine_t* e, int which, uint64_t offset, uint64_t count,
                      void* host_dst);
 int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t count,
@@ -349,6 +378,8 @@ int amsp_engine_time_kernel(amsp_engine_t* e, int enable);
 int amsp_engine_kernel_ms(amsp_engine_t* e, double* total_ms, int* launches);
 /* Same for the all-gather phase of each step (s_p > 1). */
 int amsp_engine_gather_ms(amsp_engine_t* e, double* total_ms, int* steps);
+/* Same for the micro-batch accumulation kernels (amsp_engine_accumulate). */
+int amsp_engine_accum_ms(amsp_engine_t* e, double* total_ms, int* launches);
 /* Number of kernels this engine launched so far. */
 int amsp_engine_launch_count(const amsp_engine_t* e, uint64_t* n);
 void amsp_engine_destroy(amsp_engine_t* e);

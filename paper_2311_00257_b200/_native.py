@@ -105,7 +105,8 @@ class EngineConfig(C.Structure):
                 ("plan", Plan), ("dp_mesh", Mesh), ("rank", C.c_int), ("device", C.c_int),
                 ("layout", C.c_int), ("lr", C.c_double), ("beta1", C.c_double),
                 ("beta2", C.c_double), ("eps", C.c_double), ("weight_decay", C.c_double),
-                ("seed", C.c_uint64), ("skip_gathers", C.c_int)]
+                ("seed", C.c_uint64), ("skip_gathers", C.c_int),
+                ("micro_batches", C.c_int)]
 
 
 class EngineInfo(C.Structure):
@@ -118,7 +119,9 @@ class EngineInfo(C.Structure):
                 ("exp_avg_sq", C.c_void_p), ("device_bytes", C.c_uint64),
                 ("sp", C.c_int), ("p_position", C.c_int), ("param_elems", C.c_uint64),
                 ("n_units", C.c_int), ("slot_elems", C.c_uint64),
-                ("variant", C.c_int)]
+                ("variant", C.c_int), ("micro_batches", C.c_int), ("grad_shards", C.c_int),
+                ("acc_elems", C.c_uint64), ("acc_sources", C.c_int),
+                ("acc_holders", C.c_int), ("grad_elems", C.c_uint64)]
 
 
 class SchedConfig(C.Structure):
@@ -193,6 +196,9 @@ SIGNATURES = {
     "amsp_engine_link_local": (C.c_int, [P(vp), C.c_int]),
     "amsp_engine_init_state": (C.c_int, [vp, vp]),
     "amsp_engine_synth_grads": (C.c_int, [vp, C.c_int, vp]),
+    "amsp_engine_synth_grads_mb": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+    "amsp_engine_accumulate": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+    "amsp_engine_accum_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
     "amsp_engine_step": (C.c_int, [vp, C.c_int, vp]),
     "amsp_engine_step_host": (C.c_int, [vp, C.c_int, vp, P(C.c_float), vp]),
     "amsp_engine_stats": (C.c_int, [vp, P(C.c_float)]),
@@ -239,7 +245,7 @@ def lib() -> C.CDLL:
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
-    if L.amsp_abi_version() != 1:
+    if L.amsp_abi_version() != 2:
         raise ImportError("libamsp.so ABI version mismatch")
     _lib = L
     return L

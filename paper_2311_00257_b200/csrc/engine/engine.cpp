@@ -13,6 +13,7 @@
 //     params bf16 [Phi/s_p]  this rank's P shard (= all params when s_p = 1),
 //                            written by the OS owners of its elements
 //     flags  u32 [8192 x 8]  cross-GPU barrier words ([id][r] written by rank r)
+//     acc    bf16 [Phi/s_g]  G-shard micro-batch accumulator (M > 1, s_g > 1)
 //   private allocation:
 //     master, exp_avg, exp_avg_sq fp32 [owned]  the rank's OS shard
 //     segment tables, 2 gathered-unit slots (s_p > 1), stats, error flag
@@ -39,6 +40,31 @@ void plan_groups(amsp_engine* e, const DeviceMesh& dp, const shardplan::Sharding
   e->layout = amsp::pshard_layout(e->tensor_sizes, e->sp, e->p_group.position,
                                   static_cast<int>(e->dst_members.size()), my_k,
                                   e->cfg.layout);
+}
+
+// Gradient accumulation over micro-batches. s_g = 1:
+// every rank's full gradient buffer accumulates in place, nothing moves
+// until the last micro-batch. s_g > 1 and M > 1 ("staged"): the ranks of a
+// G-mesh block jointly accumulate, each holding the bf16 G shard of its
+// elements; the last micro-batch sums the holders of every G block (block
+// order) before the raw gradients.
+void plan_accumulation(amsp_engine* e, const DeviceMesh& dp,
+                       const shardplan::ShardingPlan& plan) {
+  e->staged = e->sg > 1 && e->micro > 1;
+  e->acc_by_dst = e->sg == e->sp;
+  if (!e->staged) return;
+  const amsp::MeshGroup mine = amsp::mesh_group(dp, plan.g, e->rank);
+  e->acc_sources = mine.members;
+  std::sort(e->acc_sources.begin(), e->acc_sources.end());
+  e->acc_holders.assign(static_cast<std::size_t>(e->world / e->sg), -1);
+  for (int r = 0; r < e->world; ++r) {
+    const amsp::MeshGroup g = amsp::mesh_group(dp, plan.g, r);
+    if (g.position == mine.position) e->acc_holders[static_cast<std::size_t>(g.block)] = r;
+  }
+  for (int h : e->acc_holders)
+    if (h < 0) throw Error("engine: G mesh blocks do not tile the DP mesh");
+  // s_g = s_p: the G shard is the P shard; s_g = s_os > s_p: the OS shard
+  e->acc_elems = e->acc_by_dst ? e->param_elems : e->layout.owned;
 }
 
 // Gather units: consecutive tensors up to max(largest tensor, 2^27 elems).
@@ -119,6 +145,10 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   if (cfg->plan.has_secondary)
     throw Error("engine: ZeRO++ secondary parameter meshes are not supported");
   plan_groups(e.get(), dp, plan);
+  e->micro = cfg->micro_batches > 0 ? cfg->micro_batches : 1;
+  if (e->micro > 16) throw Error("engine: at most 16 micro-batches per step");
+  e->sg = plan.sg();
+  plan_accumulation(e.get(), dp, plan);
   std::vector<amsp::CopySeg> copy;
   plan_units(e.get(), copy);
   // In-step all-gathers default to the TMA bulk-copy kernel when every P
@@ -134,7 +164,8 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   e->off_grads = 0;
   e->off_params = align_up(e->phi * 2);
   e->off_flags = e->off_params + align_up(e->param_elems * 2);
-  e->shared_bytes = e->off_flags + align_up(kFlagBytes);
+  e->off_acc = e->off_flags + align_up(kFlagBytes);  // last: its size may differ per rank
+  e->shared_bytes = e->off_acc + align_up(e->acc_elems * 2);
   ck(cudaMalloc(&e->shared, e->shared_bytes), "cudaMalloc shared");
   ck(cudaMemset(e->shared + e->off_flags, 0, kFlagBytes), "zero flags");
   for (int r = 0; r < e->world; ++r) e->peer_base[r] = e->shared;
@@ -149,6 +180,16 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
     psegs.push_back({s.flat, s.os, s.dst, s.len, 0});
   e->nptiles = tile_prefix(psegs);
   e->npseg = static_cast<int>(psegs.size());
+  // Accumulation table: Seg::os = offset in the bf16 G-shard accumulator.
+  std::vector<amsp::Seg> asegs;
+  if (e->staged) {
+    if (e->acc_by_dst)
+      for (const auto& s : psegs) asegs.push_back({s.flat, s.dst, s.dst, s.len, 0});
+    else
+      asegs = segs;
+    e->nacc_tiles = tile_prefix(asegs);
+    e->nacc_seg = static_cast<int>(asegs.size());
+  }
 
   // Private region.
   const std::size_t n = e->layout.owned;
@@ -162,6 +203,7 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   const std::size_t o_seg = carve(segs.size() * sizeof(amsp::Seg));
   const std::size_t o_pseg = carve(psegs.size() * sizeof(amsp::Seg));
   const std::size_t o_copy = carve(copy.size() * sizeof(amsp::CopySeg));
+  const std::size_t o_aseg = carve(asegs.size() * sizeof(amsp::Seg));
   const std::size_t o_slot0 = carve(e->slot_elems * 2), o_slot1 = carve(e->slot_elems * 2);
   const std::size_t o_stats = carve(kAlign), o_err = carve(kAlign), o_tab = carve(kAlign);
   ck(cudaMalloc(&e->priv, off), "cudaMalloc optimizer state");
@@ -171,6 +213,7 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   e->d_segs = reinterpret_cast<amsp::Seg*>(e->priv + o_seg);
   e->d_psegs = reinterpret_cast<amsp::Seg*>(e->priv + o_pseg);
   e->d_copy = reinterpret_cast<amsp::CopySeg*>(e->priv + o_copy);
+  e->d_acc_segs = reinterpret_cast<amsp::Seg*>(e->priv + o_aseg);
   e->slots[0] = reinterpret_cast<uint16_t*>(e->priv + o_slot0);
   e->slots[1] = reinterpret_cast<uint16_t*>(e->priv + o_slot1);
   e->stats = reinterpret_cast<float*>(e->priv + o_stats);
@@ -182,6 +225,7 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   upload(e->d_segs, segs.data(), segs.size() * sizeof(amsp::Seg), "copy segments");
   upload(e->d_psegs, psegs.data(), psegs.size() * sizeof(amsp::Seg), "copy P segments");
   upload(e->d_copy, copy.data(), copy.size() * sizeof(amsp::CopySeg), "copy gather table");
+  upload(e->d_acc_segs, asegs.data(), asegs.size() * sizeof(amsp::Seg), "copy accumulation table");
   ck(cudaMemset(e->priv + o_stats, 0, 2 * kAlign), "zero stats/err");
   e->publish_peer_flags();
   e->device_bytes = e->shared_bytes + off;
@@ -202,6 +246,7 @@ void* buffer_ptr(amsp_engine_t* e, int which, std::size_t* elem, std::uint64_t* 
     case 4: *elem = 4; *count = e->layout.owned; return e->exp_avg_sq;
     case 5: *elem = 2; *count = e->slot_elems; return e->slots[0];
     case 6: *elem = 2; *count = e->slot_elems; return e->slots[1];
+    case 7: *elem = 2; *count = e->acc_elems; return e->acc_of(e->rank);
     default: throw Error("engine: unknown buffer id " + std::to_string(which));
   }
 }
@@ -240,6 +285,12 @@ int amsp_engine_info(const amsp_engine_t* e, amsp_engine_info_t* info) {
     info->n_units = static_cast<int>(e->units.size());
     info->slot_elems = e->slot_elems;
     info->variant = e->variant;
+    info->micro_batches = e->micro;
+    info->grad_shards = e->sg;
+    info->acc_elems = e->acc_elems;
+    info->acc_sources = static_cast<int>(e->acc_sources.size());
+    info->acc_holders = static_cast<int>(e->acc_holders.size());
+    info->grad_elems = e->phi;
   });
 }
 
@@ -342,6 +393,29 @@ int amsp_engine_synth_grads(amsp_engine_t* e, int step, void* stream) {
   });
 }
 
+int amsp_engine_synth_grads_mb(amsp_engine_t* e, int step, int mb, void* stream) {
+  return amsp::guarded([&] {
+    if (!e) throw Error("engine: null argument");
+    e->check_micro_batch(mb);
+    e->use_device();
+    // s_g = 1 accumulates micro-batches in the gradient buffer itself
+    const bool in_place = e->sg == 1 && mb > 0;
+    ck(amsp::launch_synth_grad(e->grads_of(e->rank), 0, e->phi, e->cfg.seed, step, e->rank,
+                               e->pick(stream), mb, in_place),
+       "synth grads");
+    ++e->launches;
+  });
+}
+
+int amsp_engine_accumulate(amsp_engine_t* e, int step, int mb, void* stream) {
+  return amsp::guarded([&] {
+    if (!e) throw Error("engine: null argument");
+    if (step < 1) throw Error("engine: step index must be >= 1");
+    e->use_device();
+    e->accumulate(mb, e->pick(stream));
+  });
+}
+
 int amsp_engine_step(amsp_engine_t* e, int step, void* stream) {
   return amsp::guarded([&] {
     if (!e) throw Error("engine: null argument");
@@ -357,6 +431,12 @@ int amsp_engine_step_host(amsp_engine_t* e, int step, const void* host_grads,
     e->use_device();
     cudaStream_t s = e->pick(stream);
     if (step < 1) throw Error("engine: step index must be >= 1");
+    // Linked (emulated) engines upload on their own copy streams and skip the
+    // per-chunk barriers, so a rank could update chunk c before a peer's
+    // chunk c has landed: the host-buffer step needs real peers.
+    if (e->local_linked && e->world > 1)
+      throw Error("engine: step_host needs real peers (not link_local emulation)");
+    if (e->micro > 1) throw Error("engine: step_host runs one micro-batch per step (M = 1)");
     if (e->sp == 1) {
       e->step_host_pipelined(step, host_grads, s);
     } else {
@@ -447,6 +527,7 @@ int amsp_engine_time_kernel(amsp_engine_t* e, int enable) {
     e->time_kernel = enable != 0;
     e->kernel_events_used = 0;
     e->gather_events_used = 0;
+    e->accum_events_used = 0;
   });
 }
 
@@ -470,6 +551,16 @@ int amsp_engine_gather_ms(amsp_engine_t* e, double* total_ms, int* steps) {
   });
 }
 
+int amsp_engine_accum_ms(amsp_engine_t* e, double* total_ms, int* launches) {
+  return amsp::guarded([&] {
+    if (!e || !total_ms) throw Error("engine: null argument");
+    e->use_device();
+    *total_ms = amsp_engine::sum_ms(e->accum_events, e->accum_events_used);
+    if (launches) *launches = static_cast<int>(e->accum_events_used);
+    e->accum_events_used = 0;
+  });
+}
+
 int amsp_engine_launch_count(const amsp_engine_t* e, uint64_t* n) {
   return amsp::guarded([&] {
     if (!e || !n) throw Error("engine: null argument");
@@ -490,7 +581,7 @@ void amsp_engine_destroy(amsp_engine_t* e) {
   for (auto ev : e->chunk_events) cudaEventDestroy(ev);
   if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
   if (e->own_stream) cudaStreamDestroy(e->own_stream);
-  for (auto* pairs : {&e->kernel_events, &e->gather_events})
+  for (auto* pairs : {&e->kernel_events, &e->gather_events, &e->accum_events})
     for (auto& ev : *pairs) {
       cudaEventDestroy(ev.first);
       cudaEventDestroy(ev.second);

@@ -66,6 +66,20 @@ struct amsp_engine {
   std::vector<int> dst_members;  // OS-block ranks holding my P position
   int replicas = 1;
 
+  // Micro-batches and gradient sharding. With M > 1 and
+  // s_g > 1 ("staged") every rank holds a bf16 accumulator of its G shard:
+  // the P shard (indexed by Seg::dst) when s_g = s_p, the OS shard (Seg::os)
+  // when s_g = s_os > s_p. It sits at the end of the shared region (its size
+  // may differ per rank; every other offset is identical on all ranks).
+  int micro = 1, sg = 1;
+  bool staged = false, acc_by_dst = false;
+  std::size_t off_acc = 0;
+  std::uint64_t acc_elems = 0;
+  std::vector<int> acc_sources;  // my accumulation block, ascending rank
+  std::vector<int> acc_holders;  // holder of my elements in every block, block order
+  amsp::Seg* d_acc_segs = nullptr;
+  int nacc_seg = 0, nacc_tiles = 0;
+
   // Shared region and its offsets (identical on every rank).
   char* shared = nullptr;
   std::size_t shared_bytes = 0, off_grads = 0, off_params = 0, off_flags = 0;
@@ -110,8 +124,8 @@ struct amsp_engine {
   // Optional CUDA-event bracketing of every fused launch (bench roofline).
   bool time_kernel = false;
   using EventPairs = std::vector<std::pair<cudaEvent_t, cudaEvent_t>>;
-  EventPairs kernel_events, gather_events;
-  std::size_t kernel_events_used = 0, gather_events_used = 0;
+  EventPairs kernel_events, gather_events, accum_events;
+  std::size_t kernel_events_used = 0, gather_events_used = 0, accum_events_used = 0;
   std::uint64_t launches = 0;
 
   // When timing is on, records the start event of the next pair and returns
@@ -145,6 +159,9 @@ struct amsp_engine {
   }
   uint16_t* params_of(int r) const {
     return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_params);
+  }
+  uint16_t* acc_of(int r) const {
+    return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_acc);
   }
   uint32_t* flags_of(int r) const {
     return reinterpret_cast<uint32_t*>(static_cast<char*>(peer_base[r]) + off_flags);
@@ -275,7 +292,7 @@ struct amsp_engine {
     a.exp_avg = exp_avg;
     a.exp_avg_sq = exp_avg_sq;
     a.s = amsp::make_adam_scalars(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, t,
-                                  1.0 / world);
+                                  grad_scale());
     a.stats = stats;
     a.fence_peers = (world > 1 && !local_linked) ? 1 : 0;
     for (std::size_t c = 0; c < chunk_begin.size(); ++c) {
@@ -341,6 +358,48 @@ struct amsp_engine {
     ++launches;
   }
 
+  // The step's gradient is the mean over W ranks x M micro-batches.
+  double grad_scale() const { return 1.0 / (static_cast<double>(world) * micro); }
+
+  template <class P>
+  void set_acc(P* acc, int* nacc, int* by_dst) const {
+    *nacc = static_cast<int>(acc_holders.size());
+    for (int j = 0; j < *nacc; ++j) acc[j] = acc_of(acc_holders[j]);
+    *by_dst = acc_by_dst ? 1 : 0;
+  }
+
+  void check_micro_batch(int mb) const {
+    if (mb < 0 || mb >= micro)
+      throw Error("engine: micro-batch " + std::to_string(mb) + " outside 0.." +
+                  std::to_string(micro - 1));
+  }
+
+  // Micro-batch mb (< M-1) of every rank is in the gradient buffers: fold it
+  // into the G-shard accumulators (s_g > 1; with s_g = 1 the producer has
+  // accumulated in place and there is nothing to move).
+  void accumulate(int mb, cudaStream_t s) {
+    check_micro_batch(mb);
+    if (mb == micro - 1) throw Error("engine: the last micro-batch goes through the step");
+    require_peers();
+    if (!staged) return;
+    amsp::AccumArgs a{};
+    a.segs = d_acc_segs;
+    a.nseg = nacc_seg;
+    a.ntiles = nacc_tiles;
+    a.nsrc = static_cast<int>(acc_sources.size());
+    for (int q = 0; q < a.nsrc; ++q) a.grads[q] = grads_of(acc_sources[q]);
+    a.acc = acc_of(rank);
+    a.first = mb == 0 ? 1 : 0;
+    a.fence_peers = 0;  // local stores only; the trailing barrier orders them
+    barrier(s);  // micro-batch mb is complete on every rank
+    cudaEvent_t t_end =
+        nacc_tiles > 0 ? record_begin(accum_events, accum_events_used, s) : nullptr;
+    ck(amsp::launch_accumulate(a, sms * 4, s), "accumulate launch");
+    if (t_end) ck(cudaEventRecord(t_end, s), "event record");
+    if (nacc_tiles > 0) ++launches;
+    barrier(s);  // every holder has pulled: the gradient buffers may be rewritten
+  }
+
   void step(int t, cudaStream_t s) {
     if (t < 1) throw Error("engine: step index must be >= 1");
     require_peers();
@@ -364,14 +423,23 @@ struct amsp_engine {
     a.exp_avg = exp_avg;
     a.exp_avg_sq = exp_avg_sq;
     a.s = amsp::make_adam_scalars(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
-                                  cfg.weight_decay, t, 1.0 / world);
+                                  cfg.weight_decay, t, grad_scale());
     a.stats = stats;
     a.fence_peers = (world > 1 && !local_linked) ? 1 : 0;
+    int v = variant, g = grid;
+    if (staged) {
+      // the holders' accumulators first, then the raw last micro-batch
+      set_acc(a.acc, &a.nacc, &a.acc_by_dst);
+      if (v >= 5) {  // the accumulator sources are on the LDG kernels only
+        v = world <= 4 ? 2 : 1;
+        g = std::max(1, std::min(ntiles, sms * amsp::fused_blocks_per_sm(world, v)));
+      }
+    }
     ck(cudaMemsetAsync(stats, 0, 2 * sizeof(float), s), "reset stats");
     barrier(s);  // every rank's gradients are complete
     cudaEvent_t t_end =
         ntiles > 0 ? record_begin(kernel_events, kernel_events_used, s) : nullptr;
-    ck(amsp::launch_fused_step(a, world, grid, variant, s), "fused step launch");
+    ck(amsp::launch_fused_step(a, world, g, v, s), "fused step launch");
     if (t_end) ck(cudaEventRecord(t_end, s), "event record");
     if (ntiles > 0) ++launches;
     barrier(s);  // every owner's parameter stores have landed

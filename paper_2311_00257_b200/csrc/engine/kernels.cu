@@ -109,13 +109,45 @@ struct SegCursor {
 constexpr int kSegCap = 384;    // 15 KB of Seg in shared memory
 constexpr int kCopyCap = 256;   // 10 KB of CopySeg
 
-template <int W>
-__device__ __forceinline__ float reduce_scalar(const FusedArgs& a,
-                                               unsigned long long idx) {
-  float g = bf16_at(a.grads[0][idx]);
+// Unscaled gradient of one element: the micro-batch accumulators (if any)
+// in holder order, then the raw gradients in rank order (oracle recipe).
+template <int W, class Args>
+__device__ __forceinline__ float reduce_scalar(const Args& a, unsigned long long idx,
+                                               unsigned long long acc_idx) {
+  float g;
+  int r0 = 0;
+  if (a.nacc > 0) {
+    g = bf16_at(a.acc[0][acc_idx]);
+    for (int j = 1; j < a.nacc; ++j) g = __fadd_rn(g, bf16_at(a.acc[j][acc_idx]));
+  } else {
+    g = bf16_at(a.grads[0][idx]);
+    r0 = 1;
+  }
 #pragma unroll
-  for (int r = 1; r < W; ++r) g = __fadd_rn(g, bf16_at(a.grads[r][idx]));
-  return __fmul_rn(g, a.s.grad_scale);
+  for (int r = 0; r < W; ++r)
+    if (r >= r0) g = __fadd_rn(g, bf16_at(a.grads[r][idx]));
+  return g;
+}
+
+// Sum of the accumulators of 8 consecutive elements (vector path).
+template <class Args>
+__device__ __forceinline__ void acc_vec(const Args& a, unsigned long long acc_idx, float* out) {
+  const uint4 w0 = ld_ro_v4(a.acc[0] + acc_idx);
+  const uint32_t* u0 = reinterpret_cast<const uint32_t*>(&w0);
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    out[2 * w] = bf16_lo(u0[w]);
+    out[2 * w + 1] = bf16_hi(u0[w]);
+  }
+  for (int j = 1; j < a.nacc; ++j) {
+    const uint4 wj = ld_ro_v4(a.acc[j] + acc_idx);
+    const uint32_t* uj = reinterpret_cast<const uint32_t*>(&wj);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      out[2 * w] = __fadd_rn(out[2 * w], bf16_lo(uj[w]));
+      out[2 * w + 1] = __fadd_rn(out[2 * w + 1], bf16_hi(uj[w]));
+    }
+  }
 }
 
 // Element-wise path for ragged tails and unaligned segments.
@@ -125,7 +157,8 @@ __device__ void scalar_elems(const FusedArgs& a, const Seg& sg,
   const unsigned long long end = e + 8 < sg.len ? e + 8 : sg.len;
   for (; e < end; ++e) {
     const unsigned long long f = sg.flat + e, o = sg.os + e;
-    const float g = reduce_scalar<W>(a, f);
+    const float g = __fmul_rn(reduce_scalar<W>(a, f, (a.acc_by_dst ? sg.dst : sg.os) + e),
+                              a.s.grad_scale);
     float p = a.master[o], m = a.exp_avg[o], v = a.exp_avg_sq[o];
     adamw(a.s, g, p, m, v);
     a.master[o] = p;
@@ -180,10 +213,16 @@ fused_step_kernel(const FusedArgs a) {
           float* mf = reinterpret_cast<float*>(&m[u][0]);
           float* vf = reinterpret_cast<float*>(&v[u][0]);
           uint32_t packed[4];
+          float accs[8];
+          if (a.nacc > 0) acc_vec(a, (a.acc_by_dst ? sg.dst : sg.os) + e[u], accs);
 #pragma unroll
           for (int w = 0; w < 4; ++w) {
             const uint32_t* g0 = reinterpret_cast<const uint32_t*>(&graw[u][0]);
             float glo = bf16_lo(g0[w]), ghi = bf16_hi(g0[w]);
+            if (a.nacc > 0) {
+              glo = __fadd_rn(accs[2 * w], glo);
+              ghi = __fadd_rn(accs[2 * w + 1], ghi);
+            }
 #pragma unroll
             for (int r = 1; r < W; ++r) {
               const uint32_t* gr = reinterpret_cast<const uint32_t*>(&graw[u][r]);
@@ -342,23 +381,39 @@ __global__ void init_state_kernel(const Seg* segs, int nseg, int ntiles,
   }
 }
 
+// Synthetic gradient of micro-batch `mb` (the backward stand-in): written,
+// or with `accumulate` folded into the bf16 buffer in place, dst = bf16(dst
+// + g) -- the s_g = 1 gradient accumulation of the oracle recipe.
+template <bool kAccumulate>
 __global__ void synth_grad_kernel(uint16_t* __restrict__ dst, unsigned long long start,
                                   unsigned long long n, uint64_t seed, uint32_t step,
-                                  uint32_t rank) {
+                                  uint32_t mb, uint32_t rank) {
   const unsigned long long stride = 8ull * gridDim.x * blockDim.x;
   for (unsigned long long i = 8ull * (blockIdx.x * blockDim.x + threadIdx.x); i < n;
        i += stride) {
     if (i + 8 <= n && ((reinterpret_cast<uintptr_t>(dst + i) & 15) == 0)) {
+      float x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = grad_value(seed, step, mb, rank, start + i + k);
+      if (kAccumulate) {
+        const uint4 old = *reinterpret_cast<const uint4*>(dst + i);
+        const uint32_t* o = reinterpret_cast<const uint32_t*>(&old);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          x[2 * k] = __fadd_rn(bf16_lo(o[k]), x[2 * k]);
+          x[2 * k + 1] = __fadd_rn(bf16_hi(o[k]), x[2 * k + 1]);
+        }
+      }
       uint32_t w[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        w[k] = pack_bf16x2(grad_value(seed, step, rank, start + i + 2 * k),
-                           grad_value(seed, step, rank, start + i + 2 * k + 1));
+      for (int k = 0; k < 4; ++k) w[k] = pack_bf16x2(x[2 * k], x[2 * k + 1]);
       st_v4(dst + i, make_uint4(w[0], w[1], w[2], w[3]));
     } else {
       const unsigned long long end = i + 8 < n ? i + 8 : n;
-      for (unsigned long long k = i; k < end; ++k)
-        dst[k] = to_bf16(grad_value(seed, step, rank, start + k));
+      for (unsigned long long k = i; k < end; ++k) {
+        const float g = grad_value(seed, step, mb, rank, start + k);
+        dst[k] = to_bf16(kAccumulate ? __fadd_rn(bf16_at(dst[k]), g) : g);
+      }
     }
   }
 }
@@ -437,7 +492,7 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const ReduceArgs a) {
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
     const Seg sg = cursor.at(tile);
     const unsigned long long base = (static_cast<unsigned long long>(tile) - sg.tile0) * kTile;
-    const bool aligned = ((sg.flat | sg.os) & 7ull) == 0;
+    const bool aligned = ((sg.flat | sg.os | (a.nacc ? sg.dst : 0ull)) & 7ull) == 0;
 #pragma unroll 1
     for (int it = 0; it < kVecPerThread; ++it) {
       const unsigned long long e = base + (static_cast<unsigned long long>(it) * kBlock +
@@ -447,11 +502,16 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const ReduceArgs a) {
         uint4 g[W];
 #pragma unroll
         for (int r = 0; r < W; ++r) g[r] = ld_ro_v4(a.grads[r] + sg.flat + e);
-        float out[8];
+        float out[8], accs[8];
+        if (a.nacc > 0) acc_vec(a, (a.acc_by_dst ? sg.dst : sg.os) + e, accs);
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           const uint32_t* g0 = reinterpret_cast<const uint32_t*>(&g[0]);
           float lo = bf16_lo(g0[w]), hi = bf16_hi(g0[w]);
+          if (a.nacc > 0) {
+            lo = __fadd_rn(accs[2 * w], lo);
+            hi = __fadd_rn(accs[2 * w + 1], hi);
+          }
 #pragma unroll
           for (int r = 1; r < W; ++r) {
             const uint32_t* gr = reinterpret_cast<const uint32_t*>(&g[r]);
@@ -465,12 +525,9 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const ReduceArgs a) {
         st_stream_v4(a.red + sg.os + e + 4, make_float4(out[4], out[5], out[6], out[7]));
       } else {
         const unsigned long long end = e + 8 < sg.len ? e + 8 : sg.len;
-        for (unsigned long long k = e; k < end; ++k) {
-          float g = bf16_at(a.grads[0][sg.flat + k]);
-#pragma unroll
-          for (int r = 1; r < W; ++r) g = __fadd_rn(g, bf16_at(a.grads[r][sg.flat + k]));
-          a.red[sg.os + k] = __fmul_rn(g, a.scale);
-        }
+        for (unsigned long long k = e; k < end; ++k)
+          a.red[sg.os + k] = __fmul_rn(
+              reduce_scalar<W>(a, sg.flat + k, (a.acc_by_dst ? sg.dst : sg.os) + k), a.scale);
       }
     }
   }
@@ -523,6 +580,67 @@ __global__ void __launch_bounds__(kBlock) adam_push_kernel(const AdamPushArgs a)
           a.exp_avg_sq[sg.os + k] = v;
           const uint16_t b = to_bf16(p);
           for (int d = 0; d < a.ndst; ++d) a.dsts[d][sg.dst + k] = b;
+        }
+      }
+    }
+  }
+  if (a.fence_peers) __threadfence_system();
+}
+
+// Micro-batch accumulation into the local bf16 G shard (AccumArgs). NS =
+// block size; both vectors of a thread's tile are loaded (NS x 2 loads in
+// flight) before any math, like the fused kernel.
+template <int NS, bool kFirst>
+__global__ void __launch_bounds__(kBlock) accumulate_kernel(const AccumArgs a) {
+  __shared__ Seg s_segs[kSegCap];
+  SegCursor<Seg, kSegCap> cursor;
+  cursor.init(s_segs, a.segs, a.nseg);
+  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    const Seg sg = cursor.at(tile);
+    const unsigned long long base = (static_cast<unsigned long long>(tile) - sg.tile0) * kTile;
+    const bool aligned = ((sg.flat | sg.os) & 7ull) == 0;
+    unsigned long long e[kVecPerThread];
+    uint4 g[kVecPerThread][NS], old[kVecPerThread];
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+      e[u] = base + (static_cast<unsigned long long>(u) * kBlock + threadIdx.x) * 8ull;
+      if (aligned && e[u] + 8 <= sg.len) {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) g[u][q] = ld_ro_v4(a.grads[q] + sg.flat + e[u]);
+        if (!kFirst) old[u] = *reinterpret_cast<const uint4*>(a.acc + sg.os + e[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+      if (e[u] >= sg.len) continue;
+      if (aligned && e[u] + 8 <= sg.len) {
+        uint32_t packed[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t* g0 = reinterpret_cast<const uint32_t*>(&g[u][0]);
+          float lo = bf16_lo(g0[w]), hi = bf16_hi(g0[w]);
+          if (!kFirst) {
+            const uint32_t* o = reinterpret_cast<const uint32_t*>(&old[u]);
+            lo = __fadd_rn(bf16_lo(o[w]), lo);
+            hi = __fadd_rn(bf16_hi(o[w]), hi);
+          }
+#pragma unroll
+          for (int q = 1; q < NS; ++q) {
+            const uint32_t* gq = reinterpret_cast<const uint32_t*>(&g[u][q]);
+            lo = __fadd_rn(lo, bf16_lo(gq[w]));
+            hi = __fadd_rn(hi, bf16_hi(gq[w]));
+          }
+          packed[w] = pack_bf16x2(lo, hi);
+        }
+        st_v4(a.acc + sg.os + e[u], make_uint4(packed[0], packed[1], packed[2], packed[3]));
+      } else {
+        const unsigned long long end = e[u] + 8 < sg.len ? e[u] + 8 : sg.len;
+        for (unsigned long long k = e[u]; k < end; ++k) {
+          float s = bf16_at(a.grads[0][sg.flat + k]);
+          if (!kFirst) s = __fadd_rn(bf16_at(a.acc[sg.os + k]), s);
+#pragma unroll
+          for (int q = 1; q < NS; ++q) s = __fadd_rn(s, bf16_at(a.grads[q][sg.flat + k]));
+          a.acc[sg.os + k] = to_bf16(s);
         }
       }
     }
@@ -892,14 +1010,26 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(const GatherArgs a) {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Per-device caches: the attribute and SM count belong to the device (and
+// its context), not the process, so an engine on a second GPU in the same
+// process must not reuse the first device's answer.
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
+}
+
 int sm_count() {
-  static int n = [] {
-    int dev = 0, c = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess)
-      cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
-    return c;
-  }();
-  return n;
+  static int cache[kMaxDevices] = {};
+  const int dev = current_device();
+  if (cache[dev] == 0) {
+    int c = 148;
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = c;
+  }
+  return cache[dev];
 }
 
 using FusedFn = void (*)(const FusedArgs);
@@ -941,9 +1071,14 @@ struct Tma {
   static constexpr int kStages = tma_stages(W, V);
   static constexpr int kSmem = tma_smem(W, kStages, kOut);
   static constexpr auto kFn = fused_step_tma_kernel<W, kStages, tma_two_ctas(V) ? 2 : 1, kOut>;
+  // The >48 KB dynamic shared-memory opt-in, once per device.
   static cudaError_t prepare() {
-    static const cudaError_t attr =
+    static bool done[kMaxDevices] = {};
+    const int dev = current_device();
+    if (done[dev]) return cudaSuccess;
+    const cudaError_t attr =
         cudaFuncSetAttribute(kFn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (attr == cudaSuccess) done[dev] = true;
     return attr;
   }
   static int blocks_per_sm() {
@@ -1008,6 +1143,7 @@ int fused_blocks_per_sm(int world, int variant) {
 cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int variant,
                               cudaStream_t stream) {
   if (a.ntiles == 0) return cudaSuccess;
+  if (a.nacc > 0 && variant >= 5) return cudaErrorInvalidValue;  // LDG kernels only
   if (variant == 5) return tma_launch<5>(a, world, grid, stream);  // 8-aligned segments only
   if (variant == 6) return tma_launch<6>(a, world, grid, stream);
   if (variant == 7) return tma_launch<7>(a, world, grid, stream);
@@ -1089,10 +1225,41 @@ cudaError_t launch_init_state(const Seg* segs, int nseg, int ntiles, float* mast
 
 cudaError_t launch_synth_grad(uint16_t* dst, unsigned long long start,
                               unsigned long long n, uint64_t seed, int step, int rank,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, int mb, bool accumulate) {
   if (n == 0) return cudaSuccess;
-  synth_grad_kernel<<<sm_count() * 8, 256, 0, stream>>>(
-      dst, start, n, seed, static_cast<uint32_t>(step), static_cast<uint32_t>(rank));
+  if (mb < 0 || mb > 15 || rank < 0 || rank > 15) return cudaErrorInvalidValue;
+  const int grid = sm_count() * 8;
+  const uint32_t t = static_cast<uint32_t>(step), m = static_cast<uint32_t>(mb),
+                 r = static_cast<uint32_t>(rank);
+  if (accumulate)
+    synth_grad_kernel<true><<<grid, 256, 0, stream>>>(dst, start, n, seed, t, m, r);
+  else
+    synth_grad_kernel<false><<<grid, 256, 0, stream>>>(dst, start, n, seed, t, m, r);
+  return cudaGetLastError();
+}
+
+template <int NS>
+void accumulate_launch(const AccumArgs& a, int grid, cudaStream_t stream) {
+  if (a.first)
+    accumulate_kernel<NS, true><<<grid, kBlock, 0, stream>>>(a);
+  else
+    accumulate_kernel<NS, false><<<grid, kBlock, 0, stream>>>(a);
+}
+
+cudaError_t launch_accumulate(const AccumArgs& a, int grid, cudaStream_t stream) {
+  if (a.ntiles == 0) return cudaSuccess;
+  grid = std::max(1, std::min(a.ntiles, grid > 0 ? grid : sm_count() * 4));
+  switch (a.nsrc) {
+    case 1: accumulate_launch<1>(a, grid, stream); break;
+    case 2: accumulate_launch<2>(a, grid, stream); break;
+    case 3: accumulate_launch<3>(a, grid, stream); break;
+    case 4: accumulate_launch<4>(a, grid, stream); break;
+    case 5: accumulate_launch<5>(a, grid, stream); break;
+    case 6: accumulate_launch<6>(a, grid, stream); break;
+    case 7: accumulate_launch<7>(a, grid, stream); break;
+    case 8: accumulate_launch<8>(a, grid, stream); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

@@ -29,15 +29,16 @@ __device__ __forceinline__ float unit_from_key(uint64_t key) {
   return __fmul_rn(static_cast<float>(q), 1.0f / 8388608.0f);
 }
 
-__device__ __forceinline__ uint64_t grad_key(uint64_t seed, uint32_t step,
+// Micro-batch mu of step t (mu = 0 is the single-micro-batch key).
+__device__ __forceinline__ uint64_t grad_key(uint64_t seed, uint32_t step, uint32_t mb,
                                              uint32_t rank, uint64_t index) {
-  return seed ^ (static_cast<uint64_t>(step) << 48) ^
+  return seed ^ (static_cast<uint64_t>(step) << 48) ^ (static_cast<uint64_t>(mb) << 44) ^
          (static_cast<uint64_t>(rank) << 40) ^ index;
 }
 
-__device__ __forceinline__ float grad_value(uint64_t seed, uint32_t step,
+__device__ __forceinline__ float grad_value(uint64_t seed, uint32_t step, uint32_t mb,
                                             uint32_t rank, uint64_t index) {
-  return __fmul_rn(unit_from_key(grad_key(seed, step, rank, index)), 0.0078125f);
+  return __fmul_rn(unit_from_key(grad_key(seed, step, mb, rank, index)), 0.0078125f);
 }
 
 __device__ __forceinline__ float master_init(uint64_t seed, uint64_t index) {

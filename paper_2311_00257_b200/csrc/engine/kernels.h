@@ -62,6 +62,13 @@ struct FusedArgs {
   AdamScalars s;
   float* stats;                      // += sum(g^2); may be null
   int fence_peers;                   // membar.sys before exit (peer stores)
+  // Micro-batch accumulators (M > 1, s_g > 1): the bf16 G shards of the
+  // accumulation-block holders of these elements, summed in this order
+  // BEFORE the raw gradients; indexed by Seg::dst (s_g = s_p) or Seg::os.
+  // LDG kernels only (nacc = 0 for the TMA variants).
+  const uint16_t* acc[kMaxRanks];
+  int nacc;
+  int acc_by_dst;
 };
 
 AdamScalars make_adam_scalars(double lr, double beta1, double beta2, double eps,
@@ -88,7 +95,27 @@ struct ReduceArgs {
   const uint16_t* grads[kMaxRanks];
   float* red;
   float scale;
+  const uint16_t* acc[kMaxRanks];  // as FusedArgs::acc
+  int nacc;
+  int acc_by_dst;
 };
+// Micro-batch gradient accumulation (non-last micro-batch, s_g > 1; PAPER.md:
+// 320-326): for every element of this rank's G shard, pull the bf16
+// gradients of the nsrc ranks of its accumulation block (ascending rank) and
+// fold them into the local bf16 accumulator: acc[os] = bf16((first ? 0 :
+// acc[os]) + sum_q grads_q[flat]) -- the reduce-scatter / AllReduce + select
+// & drop of the micro-batch in one pass. Seg::os = accumulator offset.
+struct AccumArgs {
+  const Seg* segs;
+  int nseg;
+  int ntiles;
+  const uint16_t* grads[kMaxRanks];
+  int nsrc;
+  uint16_t* acc;
+  int first;
+  int fence_peers;
+};
+cudaError_t launch_accumulate(const AccumArgs& a, int grid, cudaStream_t stream);
 struct AdamPushArgs {
   const Seg* segs;
   int nseg;
@@ -118,7 +145,8 @@ cudaError_t launch_init_state(const Seg* segs, int nseg, int ntiles, float* mast
                               cudaStream_t stream);
 cudaError_t launch_synth_grad(uint16_t* dst, unsigned long long start,
                               unsigned long long n, uint64_t seed, int step,
-                              int rank, cudaStream_t stream);
+                              int rank, cudaStream_t stream, int mb = 0,
+                              bool accumulate = false);
 cudaError_t launch_adamw_flat(const void* grad, bool bf16_grad, float* master,
                               float* m, float* v, uint16_t* param_out,
                               unsigned long long n, const AdamScalars& s,

@@ -19,7 +19,7 @@ from .shardplan import DeviceMesh, ModelSpec, ShardingPlan, llama_tensors
 LAYOUTS = {"greedy": 0, "contiguous": 1}
 BUFFERS = {"grads": (0, np.uint16), "params": (1, np.uint16), "master": (2, np.float32),
            "exp_avg": (3, np.float32), "exp_avg_sq": (4, np.float32),
-           "slot0": (5, np.uint16), "slot1": (6, np.uint16)}
+           "slot0": (5, np.uint16), "slot1": (6, np.uint16), "acc": (7, np.uint16)}
 DEFAULT_SEED = 0x414D5350  # "AMSP"
 
 
@@ -36,7 +36,7 @@ class Engine:
                  dp_mesh: DeviceMesh, rank: int = 0, device: int = 0,
                  layout: str = "greedy", lr: float = 1e-3, betas=(0.9, 0.95),
                  eps: float = 1e-8, weight_decay: float = 0.1, seed: int = DEFAULT_SEED,
-                 skip_gathers: bool = False):
+                 skip_gathers: bool = False, micro_batches: int = 1):
         if isinstance(tensors, ModelSpec):
             tensors = llama_tensors(tensors)
         self.tensor_sizes = [int(t) for t in tensors]
@@ -48,7 +48,8 @@ class Engine:
         arr = (C.c_uint64 * len(self.tensor_sizes))(*self.tensor_sizes)
         cfg = N.EngineConfig(C.cast(arr, C.POINTER(C.c_uint64)), len(self.tensor_sizes),
                              plan._c(), dp_mesh._c(), rank, device, LAYOUTS[layout], lr,
-                             betas[0], betas[1], eps, weight_decay, seed, int(skip_gathers))
+                             betas[0], betas[1], eps, weight_decay, seed, int(skip_gathers),
+                             int(micro_batches))
         self._h = C.c_void_p()
         N.check(N.lib().amsp_engine_create(C.byref(cfg), C.byref(self._h)))
         self.info = self._info()
@@ -82,8 +83,26 @@ class Engine:
     def init_state(self, stream=None) -> None:
         N.check(N.lib().amsp_engine_init_state(self._h, _stream_ptr(stream)))
 
-    def synth_grads(self, step: int, stream=None) -> None:
-        N.check(N.lib().amsp_engine_synth_grads(self._h, step, _stream_ptr(stream)))
+    def synth_grads(self, step: int, stream=None, mb: int = 0) -> None:
+        """Synthetic gradient of micro-batch `mb` of `step` (s_g = 1 and
+        mb > 0: accumulated into the gradient buffer in place)."""
+        N.check(N.lib().amsp_engine_synth_grads_mb(self._h, step, mb, _stream_ptr(stream)))
+
+    def accumulate(self, step: int, mb: int, stream=None) -> None:
+        """Micro-batch mb < M-1 is in every rank's gradient buffer: fold it
+        into the G-shard accumulators (s_g > 1; a no-op for s_g = 1)."""
+        N.check(N.lib().amsp_engine_accumulate(self._h, step, mb, _stream_ptr(stream)))
+
+    def micro_step(self, step: int, stream=None) -> None:
+        """One whole step of M micro-batches with synthetic gradients: for
+        every micro-batch, synthesize it, then accumulate (mb < M-1) or run
+        the optimizer step (the last)."""
+        M = self.info.micro_batches
+        for mb in range(M):
+            self.synth_grads(step, stream, mb)
+            if mb + 1 < M:
+                self.accumulate(step, mb, stream)
+        self.step(step, stream)
 
     def step(self, step: int, stream=None) -> None:
         N.check(N.lib().amsp_engine_step(self._h, step, _stream_ptr(stream)))
@@ -101,8 +120,9 @@ class Engine:
 
     def read(self, which: str, offset: int = 0, count: Optional[int] = None) -> np.ndarray:
         idx, dt = BUFFERS[which]
-        total = {0: self.info.total_params, 1: self.info.param_elems}.get(
-            idx, self.info.owned if idx < 5 else self.info.slot_elems)
+        total = {0: self.info.total_params, 1: self.info.param_elems,
+                 7: self.info.acc_elems}.get(idx, self.info.owned if idx < 5
+                                             else self.info.slot_elems)
         count = total - offset if count is None else count
         out = np.empty(count, dtype=dt)
         N.check(N.lib().amsp_engine_read(self._h, idx, offset, count,
@@ -147,6 +167,12 @@ class Engine:
         """(summed fused-kernel ms, launches) since time_kernel(True)."""
         ms, n = C.c_double(), C.c_int()
         N.check(N.lib().amsp_engine_kernel_ms(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def accum_ms(self):
+        """(summed micro-batch accumulation kernel ms, launches) since time_kernel(True)."""
+        ms, n = C.c_double(), C.c_int()
+        N.check(N.lib().amsp_engine_accum_ms(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
     def gather_ms(self):

@@ -423,3 +423,78 @@ def test_emulated_parameter_sharding_bit_exact(cuda, world, p, os_k, layout, gat
         assert np.array_equal(got, want[3][lo:lo + elems]), (u, int(np.sum(got != want[3][lo:lo + elems])))
     for e in engines:
         e.close()
+
+
+# ---------------------------------------------------------------- micro-batches
+# M > 1 micro-batches per step with gradient sharding (the
+# reference's T_g collectives, cost_model.cpp:119-126, overlap_sim.cpp:320-330,
+# and D_g = 2*Phi/s_g, cost_model.cpp:151): bit-exact against the oracle's
+# accumulation recipe (oracle/amsp_oracle.c header).
+MB_CASES = [
+    # world, dp, p, g, os, M
+    (1, (1, 1), (1, 1), (1, 1), (1, 1), 3),   # one rank, in-place accumulation
+    (2, (2, 1), (1, 1), (1, 1), (2, 1), 2),   # ZeRO-1 (s_g = 1): in place
+    (4, (4, 1), (1, 1), (1, 1), (4, 1), 3),
+    (2, (2, 1), (1, 1), (2, 1), (2, 1), 4),   # ZeRO-2 (g = os)
+    (4, (4, 1), (1, 1), (4, 1), (4, 1), 2),
+    (4, (4, 1), (1, 1), (2, 1), (2, 1), 3),   # g = os = 2: two replica blocks
+    (4, (4, 1), (4, 1), (4, 1), (4, 1), 2),   # ZeRO-3 (s_g = s_p)
+    (4, (4, 1), (2, 1), (2, 1), (4, 1), 3),   # s_g = s_p = 2 < s_os (AMSP-13B style)
+    (8, (8, 1), (2, 1), (4, 1), (4, 1), 2),   # s_p < s_g = s_os, replicas
+    (8, (2, 4), (1, 1), (2, 4), (2, 4), 2),   # BASELINE partial: G shard mesh 2x4
+    (4, (2, 2), (1, 1), (1, 2), (1, 2), 2),   # 2-D mesh: G blocks {0,2}, {1,3}
+]
+
+
+@pytest.mark.parametrize("world,dp,p,g,os_,mb", MB_CASES)
+def test_micro_batches_gradient_sharding_bit_exact(cuda, world, dp, p, g, os_, mb):
+    model = S.model("tiny")
+    plan = S.ShardingPlan(M(*p), M(*g), M(*os_))
+    engines = [Engine(model, plan, M(*dp), rank=r, micro_batches=mb) for r in range(world)]
+    if world > 1:
+        link_local(engines)
+    for e in engines:
+        e.init_state()
+    steps = 3
+    for t in range(1, steps + 1):
+        for k in range(mb):
+            for e in engines:
+                e.synth_grads(t, mb=k)
+            if k + 1 < mb:
+                for e in engines:
+                    e.accumulate(t, k)
+        for e in engines:
+            e.step(t)
+    sg = plan.sg()
+    acc = O.accum(mb, sg, O.mesh_blocks(dp, g, world))
+    phi = engines[0].info.total_params
+    want = O.trajectory_range(0, phi, DEFAULT_SEED, steps, world, H, acc)
+    for e in engines:
+        _check_rank(e, want, steps)
+        # the G-shard accumulator is the plan's D_g (cost_model.cpp:151)
+        info = e.info
+        assert info.micro_batches == mb and info.grad_shards == sg
+        if sg == 1:
+            assert info.acc_elems == 0
+        elif sg == plan.sp():
+            assert info.acc_elems == phi // plan.sp()
+            assert info.acc_sources == sg and info.acc_holders == world // sg
+        else:
+            assert info.acc_elems == info.owned
+            assert info.acc_sources == sg and info.acc_holders == world // sg
+    for e in engines:
+        e.close()
+
+
+def test_micro_batch_api_errors(cuda):
+    model = S.model("tiny")
+    e = Engine(model, _plan(M(1, 1)), M(1, 1), micro_batches=2)
+    e.init_state()
+    with pytest.raises(Exception, match="last micro-batch"):
+        e.accumulate(1, 1)
+    with pytest.raises(Exception, match="micro-batch"):
+        e.synth_grads(1, mb=2)
+    e.accumulate(1, 0)  # s_g = 1: in place, nothing to move
+    with pytest.raises(Exception, match="micro-batches"):
+        Engine(model, _plan(M(1, 1)), M(1, 1), micro_batches=17)
+    e.close()
