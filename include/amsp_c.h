@@ -395,7 +395,7 @@ void amsp_engine_destroy(amsp_engine_t* e);
 typedef struct amsp_sched amsp_sched_t;
 
 typedef struct {
-  amsp_model_t model;           /* M must be 1 */
+  amsp_model_t model;           /* micro_batch_count = the engine's M */
   amsp_cost_config_t cost;      /* bucket size U */
   amsp_sim_config_t sim;        /* tier, recompute, streams, compute times */
   int comm_ctas;                /* CTAs per communication kernel (0 = 128) */
@@ -441,6 +441,13 @@ typedef struct {
                                    pieces into local HBM after the barrier,
                                    then the same kernels reduce locally (the
                                    NVLink traffic leaves the SMs to compute) */
+  int grad_source;              /* gradients of the stand-in backward: 0 = the
+                                   caller's (already in the gradient buffer;
+                                   M must be 1); 1 = every grad-weight event
+                                   writes its tensors' synthetic gradient of
+                                   its micro-batch (the oracle definition),
+                                   so gradients appear DURING the step and
+                                   the per-bucket barriers order real data */
 } amsp_sched_config_t;
 
 typedef struct {

@@ -129,7 +129,8 @@ class SchedConfig(C.Structure):
                 ("comm_ctas", C.c_int), ("compute_ctas", C.c_int), ("time_scale", C.c_double),
                 ("optimizer_overlap", C.c_int), ("compute_mode", C.c_int), ("tokens", C.c_int),
                 ("gemm_sm_margin", C.c_int), ("gather_mode", C.c_int), ("bc_mode", C.c_int),
-                ("optimizer_variant", C.c_int), ("reduce_mode", C.c_int)]
+                ("optimizer_variant", C.c_int), ("reduce_mode", C.c_int),
+                ("grad_source", C.c_int)]
 
 
 class SchedInfo(C.Structure):

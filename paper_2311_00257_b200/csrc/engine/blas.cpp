@@ -42,11 +42,12 @@ Blas::Blas() {
 }
 
 void Blas::gemm(cudaStream_t s, bool ta, bool tb, int m, int n, int k, const void* a, int lda,
-                const void* b, int ldb, void* c, int ldc) {
+                const void* b, int ldb, void* c, int ldc, bool accumulate) {
   const float one = 1.0f, zero = 0.0f;
   if (set_stream_(handle_, s) != 0) throw shardplan::Error("cublasSetStream failed");
   const int st = gemm_ex_(handle_, ta ? kOpT : kOpN, tb ? kOpT : kOpN, m, n, k, &one, a, kBf16,
-                          lda, b, kBf16, ldb, &zero, c, kBf16, ldc, kCompute32F, kAlgoDefault);
+                          lda, b, kBf16, ldb, accumulate ? &one : &zero, c, kBf16, ldc,
+                          kCompute32F, kAlgoDefault);
   if (st != 0) throw shardplan::Error("cublasGemmEx failed with status " + std::to_string(st));
 }
 
@@ -69,9 +70,9 @@ void Blas::linear_dgrad(cudaStream_t s, const void* dy, const void* w, void* dx,
 }
 
 void Blas::linear_wgrad(cudaStream_t s, const void* dy, const void* x, void* dw, int T, int in,
-                        int out) {
+                        int out, bool accumulate) {
   // dWc[in,out] = Xc[in,T] * dYc[out,T]^T
-  gemm(s, false, true, in, out, T, x, in, dy, out, dw, in);
+  gemm(s, false, true, in, out, T, x, in, dy, out, dw, in, accumulate);
 }
 
 }  // namespace amsp

@@ -18,9 +18,10 @@ class Blas {
   // dx[T,in] = dy[T,out] * w[out,in]
   void linear_dgrad(cudaStream_t s, const void* dy, const void* w, void* dx, int T, int in,
                     int out);
-  // dw[out,in] = dy[T,out]^T * x[T,in]
+  // dw[out,in] = dy[T,out]^T * x[T,in]  (+ dw when accumulate: gradient
+  // accumulation over micro-batches in the bf16 gradient buffer)
   void linear_wgrad(cudaStream_t s, const void* dy, const void* x, void* dw, int T, int in,
-                    int out);
+                    int out, bool accumulate = false);
   // Limit the SMs GEMM kernels are sized for (0 = all): leaves SMs free for
   // concurrently running communication / optimizer kernels.
   void set_sm_target(int sms);
@@ -28,7 +29,7 @@ class Blas {
  private:
   Blas();
   void gemm(cudaStream_t s, bool ta, bool tb, int m, int n, int k, const void* a, int lda,
-            const void* b, int ldb, void* c, int ldc);
+            const void* b, int ldb, void* c, int ldc, bool accumulate = false);
   void* lib_ = nullptr;
   void* handle_ = nullptr;
   int (*create_)(void**) = nullptr;

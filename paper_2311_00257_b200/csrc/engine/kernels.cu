@@ -396,6 +396,9 @@ __global__ void synth_grad_kernel(uint16_t* __restrict__ dst, unsigned long long
 #pragma unroll
       for (int k = 0; k < 8; ++k) x[k] = grad_value(seed, step, mb, rank, start + i + k);
       if (kAccumulate) {
+        // the micro-batch gradient is a bf16 value before it is accumulated
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = bf16_at(to_bf16(x[k]));
         const uint4 old = *reinterpret_cast<const uint4*>(dst + i);
         const uint32_t* o = reinterpret_cast<const uint32_t*>(&old);
 #pragma unroll
@@ -412,7 +415,7 @@ __global__ void synth_grad_kernel(uint16_t* __restrict__ dst, unsigned long long
       const unsigned long long end = i + 8 < n ? i + 8 : n;
       for (unsigned long long k = i; k < end; ++k) {
         const float g = grad_value(seed, step, mb, rank, start + k);
-        dst[k] = to_bf16(kAccumulate ? __fadd_rn(bf16_at(dst[k]), g) : g);
+        dst[k] = to_bf16(kAccumulate ? __fadd_rn(bf16_at(dst[k]), bf16_at(to_bf16(g))) : g);
       }
     }
   }

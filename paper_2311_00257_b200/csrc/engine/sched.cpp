@@ -53,7 +53,7 @@
 
 namespace {
 
-enum class Work { Compute, Gather, Reduce, ReduceAdam, Broadcast, Marker };
+enum class Work { Compute, Gather, Reduce, ReduceAdam, Accumulate, Broadcast, Marker };
 
 // One pull of the mirrored broadcast: params[dst, dst+len) from `owner`,
 // part of layer `layer` (the head tensors: layer = L).
@@ -86,10 +86,34 @@ struct EventWork {
   // bucket completed by this grad-input event, on the AR/BC stream.
   int post_begin = 0, post_nseg = 0, post_ntiles = 0;
   int bc = -1;  // Work::Broadcast: index into amsp_sched::bc_copies
+  // Micro-batches (M > 1). mb = the event's micro-batch. A grad-weight event
+  // may synthesize its tensors' gradients (grad_source = 1), accumulating in
+  // place when s_g = 1, and first waits until every rank has pulled the
+  // previous micro-batch's gradients of those tensors (release events of the
+  // accumulations that covered them).
+  int mb = 0;
+  std::vector<int> synth_tensors;
+  bool accum_in_place = false;
+  std::vector<int> wait_release;
+  // Work::Accumulate (non-last micro-batch, s_g > 1): barrier, fold the
+  // pieces [seg_begin, +nseg) of the accumulation table into the G shard,
+  // barrier `rel_barrier`, record this event's release event.
+  int rel_barrier = -1;
+  // s_g = s_p > 1: the head tensors have no ReduceScatter event in the graph
+  // (domain.hpp:69-71), so the head grad-weight event of a non-last
+  // micro-batch accumulates them on the AG/RS stream (index into
+  // amsp_sched::head_acc, -1 = none).
+  int head_acc = -1;
 };
 
 struct Table {
   int begin = 0, nseg = 0, ntiles = 0;
+};
+
+struct HeadAccum {
+  Table t;
+  int barrier = -1, rel_barrier = -1;
+  int rel = -1;  // index of its release event in amsp_sched::rel_events
 };
 
 constexpr int kFirstSchedBarrier = 16;  // ids 0..15 stay with the engine
@@ -139,6 +163,37 @@ struct amsp_sched {
   }
   amsp::Seg* d_rsegs = nullptr;
   amsp::CopySeg* d_tcopy = nullptr;
+  // Micro-batch accumulation tables (Seg::os = G-shard accumulator offset),
+  // the release event of every Work::Accumulate event, and the head pieces.
+  amsp::Seg* d_asegs = nullptr;
+  std::vector<cudaEvent_t> rel_events;
+  std::vector<HeadAccum> head_acc;
+  std::vector<cudaEvent_t> head_done;  // head grad-weight finished (per head_acc)
+  int grad_source = 0, micro = 1;
+
+  void accumulate(const Table& t, bool first, cudaStream_t s) {
+    if (t.ntiles == 0) return;
+    amsp::AccumArgs a{};
+    a.segs = d_asegs + t.begin;
+    a.nseg = t.nseg;
+    a.ntiles = t.ntiles;
+    a.nsrc = static_cast<int>(e->acc_sources.size());
+    for (int q = 0; q < a.nsrc; ++q) a.grads[q] = e->grads_of(e->acc_sources[q]);
+    a.acc = e->acc_of(e->rank);
+    a.first = first ? 1 : 0;
+    ck(amsp::launch_accumulate(a, comm_ctas, s), "sched accumulate");
+    ++e->launches;
+  }
+
+  // Backward stand-in's gradient output: micro-batch mb of tensor t.
+  void synth(int t, int mb, bool in_place, cudaStream_t s) {
+    const std::uint64_t a = e->pmap.tensor_offset[static_cast<std::size_t>(t)];
+    ck(amsp::launch_synth_grad(e->grads_of(e->rank) + a, a, e->tensor_sizes[t], e->cfg.seed,
+                               cur_step, e->rank, s, mb, in_place),
+       "synth grads");
+    ++e->launches;
+  }
+  int cur_step = 1;
   // Copy-engine staged reduce (reduce_mode 1): after the barrier, every
   // rank's bf16 gradients of the event's owned pieces are DMA'd (peer ->
   // local, rotated start) into stage[r * stage_slot + ...]; the reduce /
@@ -216,7 +271,7 @@ struct amsp_sched {
       case Gemm::WGrad: {
         const std::size_t ti = t < 0 ? e->tensor_sizes.size() - 1 : static_cast<std::size_t>(t);
         blas.linear_wgrad(st, dout, act, e->grads_of(e->rank) + e->pmap.tensor_offset[ti],
-                          tokens, w.g_in, w.g_out);
+                          tokens, w.g_in, w.g_out, w.accum_in_place);
         break;
       }
       case Gemm::None:
@@ -287,12 +342,14 @@ struct amsp_sched {
     if (start_ev) cudaEventDestroy(start_ev);
     for (auto ev : join_ev)
       if (ev) cudaEventDestroy(ev);
-    for (auto ev : layer_ev)
-      if (ev) cudaEventDestroy(ev);
+    for (auto* v : {&layer_ev, &rel_events, &head_done})
+      for (auto ev : *v)
+        if (ev) cudaEventDestroy(ev);
     for (auto s : comm)
       if (s) cudaStreamDestroy(s);
     cudaFree(d_rsegs);
     cudaFree(d_tcopy);
+    cudaFree(d_asegs);
     cudaFree(d_ssegs);
     cudaFree(stage);
     cudaFree(red);
@@ -324,7 +381,8 @@ struct amsp_sched {
       a.grads[r] = reduce_dma ? stage + static_cast<std::uint64_t>(r) * stage_slot
                               : e->grads_of(r);
     a.red = red;
-    a.scale = static_cast<float>(1.0 / e->world);
+    a.scale = static_cast<float>(e->grad_scale());
+    if (e->staged) e->set_acc(a.acc, &a.nacc, &a.acc_by_dst);
     ck(amsp::launch_reduce(a, e->world, grid, s), "sched reduce");
     ++e->launches;
   }
@@ -363,6 +421,7 @@ struct amsp_sched {
     a.s = scalars;
     a.stats = nullptr;
     a.fence_peers = (e->world > 1 && !e->local_linked) ? 1 : 0;
+    if (e->staged) e->set_acc(a.acc, &a.nacc, &a.acc_by_dst);
     ck(amsp::launch_fused_step(a, e->world, std::max(1, std::min(t.ntiles, grid)), variant, s),
        "sched fused");
     ++e->launches;
@@ -405,8 +464,9 @@ struct amsp_sched {
     // are reused by every scheduler created on this engine: the epoch must
     // keep growing across schedulers, so it is the engine's counter.
     epoch = ++e->sched_epoch;
+    cur_step = step;
     scalars = amsp::make_adam_scalars(e->cfg.lr, e->cfg.beta1, e->cfg.beta2, e->cfg.eps,
-                                      e->cfg.weight_decay, step, 1.0 / e->world);
+                                      e->cfg.weight_decay, step, e->grad_scale());
     ck(cudaEventRecord(start_ev, main), "event record");
     if (tracing) ck(cudaEventRecord(trace_origin, main), "event record");
     for (auto s : comm) ck(cudaStreamWaitEvent(s, start_ev, 0), "stream wait");
@@ -425,11 +485,22 @@ struct amsp_sched {
           ck(cudaStreamWaitEvent(st, events[d], 0), "stream wait");
         }
       }
+      if (with_comm)
+        for (int j : w.wait_release) ck(cudaStreamWaitEvent(st, rel_events[j], 0), "stream wait");
       if (tracing) ck(cudaEventRecord(t_begin[i], st), "event record");
       const Table t{w.seg_begin, w.nseg, w.ntiles};
       switch (w.kind) {
         case Work::Compute:
           compute(w, st);
+          for (int tt : w.synth_tensors) synth(tt, w.mb, w.accum_in_place, st);
+          break;
+        case Work::Accumulate:
+          if (with_comm) {
+            barrier(w.barrier, st);  // micro-batch w.mb of these pieces is complete everywhere
+            accumulate(t, w.mb == 0, st);
+            barrier(w.rel_barrier, st);  // every holder has pulled them
+            ck(cudaEventRecord(rel_events[i], st), "event record");
+          }
           break;
         case Work::Gather:
           if (with_comm) gather_tensor(w.tensor, st);
@@ -459,6 +530,18 @@ struct amsp_sched {
       }
       if (tracing) ck(cudaEventRecord(t_end[i], st), "event record");
       if (w.record) ck(cudaEventRecord(events[i], st), "event record");
+      if (with_comm && w.head_acc >= 0) {
+        // s_g = s_p: the head's micro-batch gradient into the P-shard
+        // accumulator (no ReduceScatter event carries it)
+        const HeadAccum& h = head_acc[static_cast<std::size_t>(w.head_acc)];
+        cudaEvent_t done = head_done[static_cast<std::size_t>(w.head_acc)];
+        ck(cudaEventRecord(done, st), "event record");
+        ck(cudaStreamWaitEvent(comm[0], done, 0), "stream wait");
+        barrier(h.barrier, comm[0]);
+        accumulate(h.t, w.mb == 0, comm[0]);
+        barrier(h.rel_barrier, comm[0]);
+        ck(cudaEventRecord(rel_events[static_cast<std::size_t>(h.rel)], comm[0]), "event record");
+      }
       if (with_comm && w.post_ntiles > 0) {
         ck(cudaStreamWaitEvent(comm[1], events[i], 0), "stream wait");
         fused(Table{w.post_begin, w.post_nseg, w.post_ntiles}, comm_ctas, comm[1], opt_variant);
@@ -554,8 +637,18 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
   const shardplan::ModelSpec model = model_in(&cfg->model);
   model.check();
   const int L = model.layer_count, K = model.modules_per_layer;
-  if (model.micro_batch_count != 1)
-    throw Error("sched: the executor runs one micro-batch per step (M = 1)");
+  const int Mb = model.micro_batch_count;
+  if (Mb != e->micro)
+    throw Error("sched: the model's " + std::to_string(Mb) +
+                " micro-batches differ from the engine's " + std::to_string(e->micro));
+  s->micro = Mb;
+  if (cfg->grad_source < 0 || cfg->grad_source > 1) throw Error("sched: unknown grad_source");
+  s->grad_source = cfg->grad_source;
+  if (Mb > 1 && cfg->compute_mode == 0 && s->grad_source == 0)
+    throw Error("sched: M > 1 with stand-in compute needs grad_source = 1 (each grad-weight "
+                "event produces its micro-batch gradient)");
+  if (e->staged && cfg->optimizer_variant != 0)
+    throw Error("sched: accumulated micro-batches reduce on the LDG kernels (optimizer_variant 0)");
   // Tensor list = [embed] + L x K modules + [final norm, lm_head].
   const std::size_t n = e->tensor_sizes.size();
   if (n != static_cast<std::size_t>(L) * K + 3)
@@ -628,10 +721,27 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
   }
 
   const auto& evs = s->graph.events;
-  // Last grad-input event of each tensor (head tensors: the head's gi).
+  // Micro-batch of every event: build_schedule emits forward then backward
+  // per micro-batch (overlap_sim.cpp:161-164), and each forward pass has
+  // exactly one FwdCompute of layer 0 / module 0.
+  std::vector<int> ev_mb(evs.size(), 0);
+  {
+    int cur = -1;
+    for (std::size_t i = 0; i < evs.size(); ++i) {
+      if (evs[i].kind == shardplan::EventKind::FwdCompute && evs[i].layer == 0 &&
+          evs[i].module == 0)
+        ++cur;
+      ev_mb[i] = std::max(cur, 0);
+    }
+    if (cur != Mb - 1) throw Error("sched: graph has " + std::to_string(cur + 1) +
+                                   " forward passes for M = " + std::to_string(Mb));
+  }
+  auto last_mb = [&](std::size_t i) { return ev_mb[i] == Mb - 1; };
+  // Last grad-input event of each tensor in the last micro-batch (head
+  // tensors: the head's gi) -- the optimizer placement anchors.
   std::vector<int> gi_event(n, -1);
   for (std::size_t i = 0; i < evs.size(); ++i) {
-    if (evs[i].kind != shardplan::EventKind::BwdGradInput) continue;
+    if (evs[i].kind != shardplan::EventKind::BwdGradInput || !last_mb(i)) continue;
     if (evs[i].layer < 0) {
       gi_event[0] = gi_event[n - 2] = gi_event[n - 1] = static_cast<int>(i);
     } else {
@@ -692,7 +802,24 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     s->layer_ev.assign(static_cast<std::size_t>(L) + 1, nullptr);
   }
   std::uint64_t max_out = 0;
-  std::vector<amsp::Seg> rsegs;
+  std::vector<amsp::Seg> rsegs, asegs;
+  // Accumulation index map (Seg::os = G-shard accumulator offset): the P
+  // shard when s_g = s_p, the OS shard when s_g = s_os > s_p.
+  amsp::ShardLayout acc_layout;
+  if (e->staged) {
+    if (e->acc_by_dst) {
+      acc_layout = amsp::pshard_layout(e->tensor_sizes, e->sp, e->p_group.position, 1, 0,
+                                       amsp::kLayoutContiguous);
+      for (auto& sg : acc_layout.segs) sg.os = sg.dst;
+    } else {
+      acc_layout = e->layout;
+    }
+  }
+  // release[mb][t]: the Accumulate events (rel_events indices) that pulled
+  // tensor t's gradient of micro-batch mb.
+  std::vector<std::vector<std::vector<int>>> release(
+      static_cast<std::size_t>(Mb), std::vector<std::vector<int>>(n));
+  const std::vector<int> head_tensors = {static_cast<int>(n) - 1, static_cast<int>(n) - 2, 0};
   std::vector<char> covered(n, 0);  // reduced by some event
   std::vector<char> updated(n, 0);  // optimizer already applied by some event
   int next_barrier = kFirstSchedBarrier;
@@ -702,6 +829,66 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     const shardplan::Event& ev = evs[i];
     EventWork& w = s->work[i];
     w.stream = ev.stream;
+    w.mb = ev_mb[i];
+    const bool last = last_mb(i);
+    if (ev.kind == shardplan::EventKind::BwdGradWeight) {
+      const std::vector<int> ts =
+          ev.layer < 0 ? head_tensors : std::vector<int>{tensor_of(ev.layer, ev.module)};
+      if (!s->gemm_mode && s->grad_source == 1) w.synth_tensors = ts;
+      w.accum_in_place = e->sg == 1 && w.mb > 0;
+      if (w.mb > 0)
+        for (int tt : ts)
+          for (int j : release[static_cast<std::size_t>(w.mb - 1)][tt]) w.wait_release.push_back(j);
+      if (!last && e->staged && e->acc_by_dst && ev.layer < 0) {
+        std::vector<FlatRange> hr;
+        for (int tt : ts) hr.push_back(range_of(tt));
+        std::sort(hr.begin(), hr.end());
+        HeadAccum h;
+        h.t = owned_pieces(acc_layout, hr, asegs);
+        h.barrier = next_barrier++;
+        h.rel_barrier = next_barrier++;
+        h.rel = static_cast<int>(evs.size() + s->head_acc.size());
+        w.head_acc = static_cast<int>(s->head_acc.size());
+        s->head_acc.push_back(h);
+        for (int tt : ts) release[static_cast<std::size_t>(w.mb)][tt].push_back(h.rel);
+      }
+    }
+    if (!last && (ev.kind == shardplan::EventKind::ReduceScatter ||
+                  ev.kind == shardplan::EventKind::AllReduceBucket)) {
+      // A non-last micro-batch: s_g = s_p folds each
+      // module's reduce-scatter into the P-shard accumulator; s_g > s_p
+      // folds each AllReduce bucket over ratio(g, p) + select & drop into
+      // the OS-shard accumulator (overlap_sim.cpp:320-330). Both pull the
+      // raw bf16 gradients of the rank's G block. Otherwise a marker.
+      std::vector<FlatRange> ranges;
+      std::vector<int> ts;
+      if (ev.kind == shardplan::EventKind::ReduceScatter && e->staged && e->acc_by_dst) {
+        const int tt = tensor_of(ev.layer, ev.module);
+        ranges = {range_of(tt)};
+        ts = {tt};
+      } else if (ev.kind == shardplan::EventKind::AllReduceBucket) {
+        if (!e->staged || e->acc_by_dst)
+          throw Error("sched: AllReduce bucket in a non-last micro-batch without s_g > s_p");
+        if (ev.module >= static_cast<int>(buckets.size()))
+          throw Error("sched: bucket index beyond the gradient stream");
+        ranges = buckets[ev.module];
+        ts = bucket_tensors[ev.module];
+      }
+      if (ranges.empty()) {
+        w.kind = Work::Marker;
+        continue;
+      }
+      w.kind = Work::Accumulate;
+      const Table at = owned_pieces(acc_layout, ranges, asegs);
+      w.seg_begin = at.begin;
+      w.nseg = at.nseg;
+      w.ntiles = at.ntiles;
+      w.barrier = next_barrier++;
+      w.rel_barrier = next_barrier++;
+      for (int tt : ts) release[static_cast<std::size_t>(w.mb)][tt].push_back(static_cast<int>(i));
+      ++s->n_reduce;
+      continue;
+    }
     switch (ev.kind) {
       case shardplan::EventKind::FwdCompute:
       case shardplan::EventKind::BwdGradInput:
@@ -889,6 +1076,23 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     ck(cudaMalloc(&s->d_tcopy, n * sizeof(amsp::CopySeg)), "cudaMalloc tensor copies");
     ck(cudaMemcpy(s->d_tcopy, tc.data(), n * sizeof(amsp::CopySeg), cudaMemcpyHostToDevice),
        "copy tensor copies");
+  }
+  if (!asegs.empty()) {
+    ck(cudaMalloc(&s->d_asegs, asegs.size() * sizeof(amsp::Seg)), "cudaMalloc accumulation segs");
+    ck(cudaMemcpy(s->d_asegs, asegs.data(), asegs.size() * sizeof(amsp::Seg),
+                  cudaMemcpyHostToDevice),
+       "copy accumulation segs");
+  }
+  s->rel_events.assign(evs.size() + s->head_acc.size(), nullptr);
+  for (std::size_t i = 0; i < evs.size(); ++i)
+    if (s->work[i].kind == Work::Accumulate)
+      ck(cudaEventCreateWithFlags(&s->rel_events[i], cudaEventDisableTiming), "event");
+  for (const HeadAccum& h : s->head_acc) {
+    ck(cudaEventCreateWithFlags(&s->rel_events[static_cast<std::size_t>(h.rel)],
+                                cudaEventDisableTiming),
+       "event");
+    s->head_done.push_back(nullptr);
+    ck(cudaEventCreateWithFlags(&s->head_done.back(), cudaEventDisableTiming), "event");
   }
   const bool needs_red = s->pending.ntiles > 0 || (plan.sp() == 1 && ar_seen > 0);
   if (needs_red)

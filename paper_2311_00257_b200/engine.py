@@ -219,7 +219,7 @@ class Scheduler:
                  comm_ctas: int = 0, compute_ctas: int = 0, time_scale: float = 1.0,
                  optimizer_overlap: bool = True, compute: str = "standin", tokens: int = 0,
                  gemm_sm_margin: int = 0, gather: str = "sm", bc: str = "auto",
-                 optimizer_variant: int = 0, reduce: str = "sm"):
+                 optimizer_variant: int = 0, reduce: str = "sm", grad_source: str = "caller"):
         from .shardplan import CostConfig, SimConfig
         cost = cost or CostConfig()
         sim = sim or SimConfig()
@@ -243,7 +243,7 @@ class Scheduler:
                             int(optimizer_overlap), {"standin": 0, "gemm": 1}[compute], tokens,
                             gemm_sm_margin, {"sm": 0, "dma": 1, "tma": 2}[gather],
                             {"auto": 0, "push": 1}[bc], optimizer_variant,
-                            {"sm": 0, "dma": 1}[reduce])
+                            {"sm": 0, "dma": 1}[reduce], {"caller": 0, "synth": 1}[grad_source])
         self.engine = engine
         self._h = C.c_void_p()
         N.check(N.lib().amsp_sched_create(engine._h, C.byref(cfg), profile._h, C.byref(self._h)))

@@ -27,6 +27,15 @@ def main():
     ap.add_argument("--dp-mesh", default=None)
     ap.add_argument("--layout", default="greedy")
     ap.add_argument("--p-mesh", default=None)
+    ap.add_argument("--g-mesh", default=None,
+                    help="explicit G mesh (default: the P mesh when given, else 1x1)")
+    ap.add_argument("--micro-batches", type=int, default=1)
+    ap.add_argument("--synth", action="store_true",
+                    help="scheduler: every grad-weight event writes its micro-batch gradient "
+                         "during the step (grad_source=synth); no host barriers anywhere")
+    ap.add_argument("--two-scheds", action="store_true",
+                    help="run the steps through two schedulers created on the same engine, "
+                         "alternating, with no host synchronisation between steps")
     ap.add_argument("--sched", action="store_true")
     ap.add_argument("--gather", default="sm", choices=["sm", "tma", "dma"])
     ap.add_argument("--reduce", default="sm", choices=["sm", "dma"],
@@ -54,12 +63,15 @@ def main():
     os_mesh = mesh(args.os_mesh) if args.os_mesh else dp
     p_mesh = mesh(args.p_mesh) if args.p_mesh else M(1, 1)
     g_mesh = p_mesh if p_mesh == os_mesh or args.p_mesh else M(1, 1)
+    if args.g_mesh:
+        g_mesh = mesh(args.g_mesh)
+    MB = args.micro_batches
     plan = S.ShardingPlan(p_mesh, g_mesh, os_mesh)
     # "chunky": three raw tensors (300M params) so the host-buffer step spans
     # two 2^28-element upload chunks, with the chunk boundary inside a tensor.
     model = [200_000_000, 100_000_008, 64] if args.model == "chunky" else S.model(args.model)
     e = Engine(model, plan, dp, rank=rank, device=local, layout=args.layout,
-               skip_gathers=args.sched)
+               skip_gathers=args.sched, micro_batches=MB)
     e.connect()
     if args.variant:
         e.tune(args.variant)
@@ -67,29 +79,43 @@ def main():
         e.tune_gather(args.gather)
     e.init_state()
     sched = None
+    scheds = []
     if args.sched:  # overlap scheduler: real cross-GPU barriers per bucket / module
         from paper_2311_00257_b200.engine import Scheduler, b200_profile
-        sched = Scheduler(e, S.model(args.model), b200_profile(),
-                          S.CostConfig(bucket_size=1 << 20),
-                          S.SimConfig(overlap_tier="ag_rs_ar_bc", peak_flops_per_gpu=1e16),
-                          gather=args.gather, reduce=args.reduce)
+        for _ in range(2 if args.two_scheds else 1):
+            scheds.append(Scheduler(e, S.model(args.model, micro_batch_count=MB), b200_profile(),
+                                    S.CostConfig(bucket_size=1 << 20),
+                                    S.SimConfig(overlap_tier="ag_rs_ar_bc",
+                                                peak_flops_per_gpu=1e16),
+                                    gather=args.gather, reduce=args.reduce,
+                                    grad_source="synth" if args.synth else "caller"))
+        sched = scheds[0]
     for t in range(1, args.steps + 1):
-        e.synth_grads(t)
-        if sched:
+        if sched and args.synth:
+            # gradients appear inside the step (grad-weight events); the
+            # device barriers alone order every cross-GPU read
+            scheds[(t - 1) % len(scheds)].step(t)
+        elif sched:
+            e.synth_grads(t)
             dist.barrier()  # every rank's grads of step t exist before pulls
             sched.step(t)
             torch.cuda.synchronize()
             dist.barrier()
+        elif MB > 1:
+            e.micro_step(t)
         elif args.host:
+            e.synth_grads(t)
             g = e.read("grads")  # this rank's step-t gradients, staged through host memory
             host = torch.from_numpy(g.view(np.int16)).pin_memory()
             e.step_host(t, host.data_ptr())
         else:
+            e.synth_grads(t)
             e.step(t)
     if sched:
-        sched.flush()  # mirrored broadcast: the last step's shards
+        scheds[(args.steps - 1) % len(scheds)].flush()  # mirrored broadcast: the last shards
         torch.cuda.synchronize()
-        sched.close()
+        for s in scheds:
+            s.close()
     torch.cuda.synchronize()
     if args.full:
         from fullcheck import check_engine
@@ -110,14 +136,17 @@ def main():
     # a rank may own no tensor (greedy layout, fewer tensors than ranks)
     idx = np.concatenate([np.arange(f, f + ln, dtype=np.uint64) for f, _, ln in segs]
                          or [np.empty(0, np.uint64)])
-    want = O.trajectory(idx, DEFAULT_SEED, args.steps, world, O.hyper()) if owned else [[]] * 3
+    acc = O.accum(MB, plan.sg(), O.mesh_blocks((dp.per_node, dp.nodes),
+                                                (g_mesh.per_node, g_mesh.nodes), world))
+    want = (O.trajectory(idx, DEFAULT_SEED, args.steps, world, O.hyper(), acc) if owned
+            else [[]] * 3)
     for name, ref in zip(("master", "exp_avg", "exp_avg_sq") if owned else (), want[:3]):
         got = e.read(name)
         if not np.array_equal(got.view(np.uint32), ref.view(np.uint32)):
             print(f"RANK {rank} MISMATCH {name}: {int(np.sum(got != ref))}", flush=True)
             ok = False
     params = e.read("params")
-    full_all = O.trajectory_range(0, phi, DEFAULT_SEED, args.steps, world, O.hyper())[3]
+    full_all = O.trajectory_range(0, phi, DEFAULT_SEED, args.steps, world, O.hyper(), acc)[3]
     psegs, pn = pshard_layout(e.tensor_sizes, plan.sp(), e.info.p_position, 1, 0, "contiguous")
     full = np.empty(pn, np.uint16)
     for f, _, d, ln in psegs:
