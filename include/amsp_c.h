@@ -380,6 +380,13 @@ int amsp_engine_kernel_ms(amsp_engine_t* e, double* total_ms, int* launches);
 int amsp_engine_gather_ms(amsp_engine_t* e, double* total_ms, int* steps);
 /* Same for the micro-batch accumulation kernels (amsp_engine_accumulate). */
 int amsp_engine_accum_ms(amsp_engine_t* e, double* total_ms, int* launches);
+/* NVLink peer-read probe (bench): every rank pulls `bytes` from its peers'
+ * gradient buffers into local scratch, after a cross-GPU barrier, `iters`
+ * times; pattern 0 = ring (all from rank+1), 1 = all-to-all (an equal share
+ * from every peer, 512-byte warp chunks interleaved -- the fused reduce's
+ * pattern). *ms_per_iter = this rank's time per pull of `bytes`. */
+int amsp_engine_nvlink_probe(amsp_engine_t* e, uint64_t bytes, int pattern, int iters,
+                             double* ms_per_iter);
 /* Number of kernels this engine launched so far. */
 int amsp_engine_launch_count(const amsp_engine_t* e, uint64_t* n);
 void amsp_engine_destroy(amsp_engine_t* e);

@@ -200,6 +200,8 @@ SIGNATURES = {
     "amsp_engine_synth_grads_mb": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "amsp_engine_accumulate": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "amsp_engine_accum_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
+    "amsp_engine_nvlink_probe": (C.c_int, [vp, C.c_uint64, C.c_int, C.c_int,
+                                           C.POINTER(C.c_double)]),
     "amsp_engine_step": (C.c_int, [vp, C.c_int, vp]),
     "amsp_engine_step_host": (C.c_int, [vp, C.c_int, vp, P(C.c_float), vp]),
     "amsp_engine_stats": (C.c_int, [vp, P(C.c_float)]),

@@ -561,6 +561,59 @@ int amsp_engine_accum_ms(amsp_engine_t* e, double* total_ms, int* launches) {
   });
 }
 
+int amsp_engine_nvlink_probe(amsp_engine_t* e, uint64_t bytes, int pattern, int iters,
+                             double* ms_per_iter) {
+  return amsp::guarded([&] {
+    if (!e || !ms_per_iter) throw Error("engine: null argument");
+    if (e->world < 2) throw Error("engine: the NVLink probe needs peers");
+    if (pattern < 0 || pattern > 1 || iters < 1) throw Error("engine: bad probe arguments");
+    e->require_peers();
+    e->use_device();
+    amsp::PullArgs a{};
+    if (pattern == 0) {  // ring: pull everything from the next rank
+      a.nsrc = 1;
+      a.src[0] = reinterpret_cast<const uint4*>(e->grads_of((e->rank + 1) % e->world));
+    } else {  // all-to-all: an equal share from every peer
+      for (int j = 1; j < e->world; ++j)
+        a.src[a.nsrc++] = reinterpret_cast<const uint4*>(e->grads_of((e->rank + j) % e->world));
+    }
+    a.rot = 0;
+    const std::uint64_t per_src = std::min<std::uint64_t>(bytes / a.nsrc, e->phi * 2) / 16;
+    if (per_src == 0) throw Error("engine: probe size too small");
+    a.vecs_per_src = per_src;
+    const std::uint64_t total = per_src * 16 * a.nsrc;
+    void* dst = nullptr;
+    ck(cudaMalloc(&dst, total), "cudaMalloc probe buffer");
+    a.dst = static_cast<uint4*>(dst);
+    cudaStream_t s = e->own_stream;
+    cudaEvent_t x, y;
+    ck(cudaEventCreate(&x), "event");
+    ck(cudaEventCreate(&y), "event");
+    try {
+      ck(amsp::launch_p2p_pull(a, 0, s), "probe warm-up");
+      e->barrier(s);  // every rank pulls at the same time
+      ck(cudaEventRecord(x, s), "event record");
+      for (int i = 0; i < iters; ++i) ck(amsp::launch_p2p_pull(a, 0, s), "probe");
+      ck(cudaEventRecord(y, s), "event record");
+      e->barrier(s);
+      ck(cudaEventSynchronize(y), "event sync");
+      float ms = 0.0f;
+      ck(cudaEventElapsedTime(&ms, x, y), "event elapsed");
+      *ms_per_iter = ms / iters;
+      e->launches += static_cast<std::uint64_t>(iters) + 1;
+    } catch (...) {
+      cudaEventDestroy(x);
+      cudaEventDestroy(y);
+      cudaFree(dst);
+      throw;
+    }
+    cudaEventDestroy(x);
+    cudaEventDestroy(y);
+    cudaFree(dst);
+    e->check_err();
+  });
+}
+
 int amsp_engine_launch_count(const amsp_engine_t* e, uint64_t* n) {
   return amsp::guarded([&] {
     if (!e || !n) throw Error("engine: null argument");

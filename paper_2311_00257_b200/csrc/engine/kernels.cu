@@ -651,6 +651,31 @@ __global__ void __launch_bounds__(kBlock) accumulate_kernel(const AccumArgs a) {
   if (a.fence_peers) __threadfence_system();
 }
 
+__global__ void __launch_bounds__(256) p2p_pull_kernel(const PullArgs a) {
+  const unsigned long long total = a.vecs_per_src * static_cast<unsigned long long>(a.nsrc);
+  const unsigned long long stride = 2ull * gridDim.x * blockDim.x;
+  for (unsigned long long v0 = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x +
+                                threadIdx.x);
+       v0 < total; v0 += stride) {
+    uint4 x[2];
+    unsigned long long off[2];
+    int q[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const unsigned long long v = v0 + u * (stride / 2);
+      const unsigned long long chunk = v / 32;
+      q[u] = static_cast<int>((chunk % a.nsrc + a.rot) % a.nsrc);
+      off[u] = (chunk / a.nsrc) * 32 + v % 32;
+      if (v < total) x[u] = ld_ro_v4(a.src[q[u]] + off[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const unsigned long long v = v0 + u * (stride / 2);
+      if (v < total) st_v4(a.dst + v, x[u]);
+    }
+  }
+}
+
 // Compute stand-in for the overlap schedule: every CTA keeps its warps
 // issuing dependent FMAs for `ns` nanoseconds (timed per CTA, so CTAs that
 // wait for SM slots held by communication kernels finish later — the
@@ -1187,6 +1212,12 @@ cudaError_t launch_reduce(const ReduceArgs& a, int world, int grid, cudaStream_t
 cudaError_t launch_adam_push(const AdamPushArgs& a, int grid, cudaStream_t stream) {
   if (a.ntiles == 0) return cudaSuccess;
   adam_push_kernel<<<std::max(1, std::min(a.ntiles, grid)), kBlock, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_pull(const PullArgs& a, int grid, cudaStream_t stream) {
+  if (a.nsrc < 1 || a.nsrc > kMaxRanks || a.vecs_per_src == 0) return cudaErrorInvalidValue;
+  p2p_pull_kernel<<<grid > 0 ? grid : sm_count() * 4, 256, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

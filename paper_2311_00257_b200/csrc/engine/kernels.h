@@ -116,6 +116,18 @@ struct AccumArgs {
   int fence_peers;
 };
 cudaError_t launch_accumulate(const AccumArgs& a, int grid, cudaStream_t stream);
+// NVLink peer-read probe: pull vecs_per_src 16-byte vectors from each of
+// nsrc (peer) buffers into a local buffer, interleaved across the sources in
+// 512-byte warp chunks (rotated by `rot`) -- the all-to-all pull pattern of
+// the fused step's gradient reduce, with nothing else in the way.
+struct PullArgs {
+  const uint4* src[kMaxRanks];
+  int nsrc;
+  int rot;
+  uint4* dst;
+  unsigned long long vecs_per_src;
+};
+cudaError_t launch_p2p_pull(const PullArgs& a, int grid, cudaStream_t stream);
 struct AdamPushArgs {
   const Seg* segs;
   int nseg;

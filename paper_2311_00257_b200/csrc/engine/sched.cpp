@@ -427,6 +427,26 @@ struct amsp_sched {
     ++e->launches;
   }
 
+  // The optimizer work of a table without communication (mode 2 baseline):
+  // own gradients (W = 1 sum), own parameters only.
+  void local_fused(const Table& t, int grid, cudaStream_t s, int variant = 0) {
+    if (t.ntiles == 0) return;
+    amsp::FusedArgs a{};
+    a.segs = d_rsegs + t.begin;
+    a.nseg = t.nseg;
+    a.ntiles = t.ntiles;
+    a.grads[0] = e->grads_of(e->rank);
+    a.ndst = 1;
+    a.dsts[0] = e->params_of(e->rank);
+    a.master = e->master;
+    a.exp_avg = e->exp_avg;
+    a.exp_avg_sq = e->exp_avg_sq;
+    a.s = scalars;
+    ck(amsp::launch_fused_step(a, 1, std::max(1, std::min(t.ntiles, grid)), variant, s),
+       "local optimizer");
+    ++e->launches;
+  }
+
   void gather_tensor(int t, cudaStream_t s) {
     if (gather_dma) {
       // Copy-engine all-gather: one peer-to-local DMA per P-group member
@@ -514,12 +534,17 @@ struct amsp_sched {
               barrier(w.barrier2, st);
               adam_push(t, comm_ctas, st);
             }
+          } else if (local_optimizer && w.adam_after) {
+            ck(cudaStreamWaitEvent(st, events[w.after_event], 0), "stream wait");
+            local_fused(t, comm_ctas, st, opt_variant);
           }
           break;
         case Work::ReduceAdam:
           if (with_comm) {
             barrier(w.barrier, st);
             fused(t, comm_ctas, st, opt_variant, true);
+          } else if (local_optimizer) {
+            local_fused(t, comm_ctas, st, opt_variant);
           }
           break;
         case Work::Broadcast:
@@ -542,9 +567,13 @@ struct amsp_sched {
         barrier(h.rel_barrier, comm[0]);
         ck(cudaEventRecord(rel_events[static_cast<std::size_t>(h.rel)], comm[0]), "event record");
       }
-      if (with_comm && w.post_ntiles > 0) {
+      if ((with_comm || local_optimizer) && w.post_ntiles > 0) {
         ck(cudaStreamWaitEvent(comm[1], events[i], 0), "stream wait");
-        fused(Table{w.post_begin, w.post_nseg, w.post_ntiles}, comm_ctas, comm[1], opt_variant);
+        const Table pt{w.post_begin, w.post_nseg, w.post_ntiles};
+        if (with_comm)
+          fused(pt, comm_ctas, comm[1], opt_variant);
+        else
+          local_fused(pt, comm_ctas, comm[1], opt_variant);
       }
     }
     for (int k = 0; k < 2; ++k) {
@@ -552,27 +581,14 @@ struct amsp_sched {
       ck(cudaStreamWaitEvent(main, join_ev[k], 0), "stream wait");
     }
     if (local_optimizer) {
-      // Baseline "compute + optimizer, no communication": the fused update
-      // of this rank's shard from its OWN gradients only, written to its own
-      // parameters — the optimizer's HBM work without any NVLink traffic
-      // (a timing proxy; the values are not the step's).
-      amsp::FusedArgs a{};
-      a.segs = e->d_segs;
-      a.nseg = e->nseg;
-      a.ntiles = e->ntiles;
-      a.grads[0] = e->grads_of(e->rank);
-      a.ndst = 1;
-      a.dsts[0] = e->params_of(e->rank);
-      a.master = e->master;
-      a.exp_avg = e->exp_avg;
-      a.exp_avg_sq = e->exp_avg_sq;
-      a.s = scalars;
-      // the engine's single-rank choice (W = 1 auto): the 3-stage TMA ring,
-      // 1 CTA / SM, when aligned, else LDG
-      const bool tma = e->variant >= 5;
-      ck(amsp::launch_fused_step(a, 1, tma ? e->sms : e->sms * 2, tma ? 5 : 4, main),
-         "local optimizer");
-      ++e->launches;
+      // Baseline "compute + optimizer, no communication": every optimizer
+      // update at the SAME place as in the full step (in backward or after
+      // it), but from this rank's own gradients into its own parameters:
+      // the optimizer's HBM and SM work without any NVLink traffic or
+      // barrier (a timing proxy; the values are not the step's). So the
+      // exposed communication t(full) - t(this) compares like with like.
+      local_fused(resid, e->sms * amsp::fused_blocks_per_sm(1, 0), main);
+      local_fused(pending, e->sms * 2, main);
       return;
     }
     if (!with_comm) return;

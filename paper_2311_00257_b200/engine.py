@@ -175,6 +175,18 @@ class Engine:
         N.check(N.lib().amsp_engine_accum_ms(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    def nvlink_probe(self, nbytes: int = 1 << 32, pattern: str = "all", iters: int = 5):
+        """This rank's NVLink ingress in GB/s pulling `nbytes` from its peers
+        (pattern "ring": all from rank+1; "all": an equal share from every
+        peer). Collective: every rank must call it."""
+        ms = C.c_double()
+        N.check(N.lib().amsp_engine_nvlink_probe(self._h, nbytes, {"ring": 0, "all": 1}[pattern],
+                                                 iters, C.byref(ms)))
+        per = (nbytes // (1 if pattern == "ring" else self.world - 1)) // 16 * 16
+        moved = min(per, 2 * self.info.total_params // 16 * 16) * (
+            1 if pattern == "ring" else self.world - 1)
+        return moved / (ms.value * 1e-3) / 1e9
+
     def gather_ms(self):
         """(summed all-gather-phase ms, steps) since time_kernel(True)."""
         ms, n = C.c_double(), C.c_int()

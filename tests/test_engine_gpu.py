@@ -442,7 +442,7 @@ MB_CASES = [
     (4, (4, 1), (2, 1), (2, 1), (4, 1), 3),   # s_g = s_p = 2 < s_os (AMSP-13B style)
     (8, (8, 1), (2, 1), (4, 1), (4, 1), 2),   # s_p < s_g = s_os, replicas
     (8, (2, 4), (1, 1), (2, 4), (2, 4), 2),   # BASELINE partial: G shard mesh 2x4
-    (4, (2, 2), (1, 1), (1, 2), (1, 2), 2),   # 2-D mesh: G blocks {0,2}, {1,3}
+    (4, (2, 2), (1, 1), (2, 1), (2, 1), 2),   # 2-D mesh: G shard inside each virtual node
 ]
 
 
