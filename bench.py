@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--tier", default="ag_rs_ar_bc", help="overlap tier for --overlap")
     ap.add_argument("--seq-len", type=int, default=4096)
     ap.add_argument("--micro-batch", type=int, default=1)
+    ap.add_argument("--micro-batches", type=int, default=1,
+                    help="M micro-batches per step: M-1 gradient accumulations into the G "
+                         "shards (s_g > 1) before the fused update (PAPER.md:316-326)")
     ap.add_argument("--compute-eff", type=float, default=0.6)
     ap.add_argument("--comm-ctas", type=int, default=0)
     ap.add_argument("--trace-dir", default=None,
@@ -82,7 +85,7 @@ def parse():
     ap.add_argument("--step-gather", default="auto", choices=["auto", "sm", "dma", "tma"],
                     help="all-gather implementation inside the pipeline-only step (s_p > 1); "
                          "auto = the engine's default (TMA when the P slices are aligned)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -178,7 +181,8 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def step_bytes(phi, owned, world, k, sp=1, sos=None, gathers=2):
+def step_bytes(phi, owned, world, k, sp=1, sos=None, gathers=2, micro=1, acc_elems=0, sg=1,
+               phases=False):
     """Algorithmic bytes per GPU of ONE step (all ranks run concurrently;
     DESIGN.md §4). k = ranks sharing this rank's P position in its OS group
     (its parameter-store destinations), R = W/s_os replica groups.
@@ -189,69 +193,124 @@ def step_bytes(phi, owned, world, k, sp=1, sos=None, gathers=2):
       NVL out = peers' pulls 2*(R*Phi-owned) + my pushes 2*owned*(k-1)
     s_p > 1 adds `gathers` all-gather passes (forward + backward):
       HBM  = 2*Phi (gathered write) + 2*Phi (the P group reading this shard)
-      NVL  = 2*Phi*(s_p-1)/s_p per direction."""
+      NVL  = 2*Phi*(s_p-1)/s_p per direction.
+    M > 1 with s_g > 1 adds, per non-last micro-batch, the accumulation of
+    the G shard (acc_elems bf16 accumulator elements on this rank, pulled
+    from the s_g ranks of its G group):
+      HBM  = 4*acc_elems (accumulator r/w) + 2*Phi (the holders read this
+             GPU's gradients once)
+      NVL in = 2*acc_elems*(s_g-1), out = 2*Phi*(s_g-1)/s_g
+    and the last micro-batch's update reads the W/s_g holders' accumulators
+    (2*owned each, W/s_g - 1 over NVLink) besides the raw gradients.
+    phases=True returns [(name, hbm, nvl)] per serial phase instead."""
     sos = sos or k * sp
     R = world // sos
     hbm = 24 * owned + 2 * phi * R + 2 * phi // sp
     nvl_in = 2 * owned * (world - 1) + 2 * (phi // sp - owned)
     nvl_out = 2 * (R * phi - owned) + 2 * owned * (k - 1)
-    if sp > 1:
-        hbm += gathers * 4 * phi
-        nvl_in += gathers * 2 * phi * (sp - 1) // sp
-        nvl_out += gathers * 2 * phi * (sp - 1) // sp
+    out = []
+    if micro > 1 and sg > 1 and acc_elems:
+        holders = world // sg
+        a_hbm = (micro - 1) * (4 * acc_elems + 2 * phi) - 2 * acc_elems  # first: write only
+        a_in = (micro - 1) * 2 * acc_elems * (sg - 1)
+        a_out = (micro - 1) * 2 * phi * (sg - 1) // sg
+        out.append(("accumulate", a_hbm, max(a_in, a_out) if world > 1 else 0))
+        hbm += 2 * acc_elems
+        nvl_in += 2 * owned * (holders - 1)
+        nvl_out += 2 * acc_elems * (holders - 1)
     if world == 1:
         nvl_in = nvl_out = 0
-    return hbm, max(nvl_in, nvl_out)
+    out.append(("update", hbm, max(nvl_in, nvl_out)))
+    if sp > 1:
+        g_hbm = gathers * 4 * phi
+        g_nvl = gathers * 2 * phi * (sp - 1) // sp
+        out.insert(0, ("all_gather", g_hbm, g_nvl))
+    if phases:
+        return out
+    return sum(x[1] for x in out), sum(x[2] for x in out)
 
 
-def cpu_baseline(phi_total, world, steps_budget_s=12.0, sample=None, max_steps=1000):
-    """The oracle's CPU step (C + OpenMP, all host cores) on a bounded sample
-    of the same workload: `sample` consecutive params of the flat model,
-    `world` ranks' gradients reduced, one OS owner per element (ZeRO-1).
-    Steps repeat over the sample until `steps_budget_s` of CPU work is done
-    (about 10 s by default); the value is the median step."""
-    import numpy as np
+def cpu_sample_size(phi_total):
+    """The bounded CPU sample both arms use: 1/16 of the flat model (8-aligned),
+    so one oracle step is ~0.1-0.3 s of host work."""
+    return max(8, (phi_total // 16) // 8 * 8)
 
-    from oracle import cpu as O
-    from paper_2311_00257_b200.engine import DEFAULT_SEED
-    h = O.hyper()
-    n = sample or (64 << 20)
-    grads = [O.grads(0, n, DEFAULT_SEED, 1, r) for r in range(world)]
-    master = np.array([0.0], np.float32)
-    master = np.empty(n, np.float32)
-    O.use_all_threads()
-    master[:] = 0.01
-    m = np.zeros(n, np.float32)
-    v = np.zeros(n, np.float32)
-    params = [np.zeros(n, np.uint16) for _ in range(world)]
-    segs = [(0, 0, n)]
+
+class CpuPort:
+    """The oracle's CPU step (C + OpenMP, all host cores) on `n` consecutive
+    params of the flat model: `world` ranks' bf16 gradients reduced in fixed
+    order, 1/W scale, AdamW on one OS owner per element (ZeRO-1), the bf16
+    params written into `world` copies (the gather). Test infrastructure:
+    only bench.py's baseline legs run it."""
+
+    def __init__(self, n, world):
+        import numpy as np
+
+        from oracle import cpu as O
+        from paper_2311_00257_b200.engine import DEFAULT_SEED
+        self.O, self.n, self.world = O, n, world
+        self.cores = O.use_all_threads()
+        self.h = O.hyper()
+        self.grads = [O.grads(0, n, DEFAULT_SEED, 1, r) for r in range(world)]
+        self.master = np.full(n, 0.01, np.float32)
+        self.m = np.zeros(n, np.float32)
+        self.v = np.zeros(n, np.float32)
+        self.params = [np.zeros(n, np.uint16) for _ in range(world)]
+        self.t = 0
+
+    def step(self):
+        self.t += 1
+        self.O.step(self.grads, [(0, 0, self.n)], self.master, self.m, self.v, self.params,
+                    self.O.scalars(self.t, self.world, self.h))
+
+    def describe(self, phi_total, steps, secs):
+        return (f"{self.n} consecutive params (1/16) of the {phi_total}-param flat model per "
+                f"step: {self.world} rank gradients reduced + AdamW + bf16 into {self.world} "
+                f"param copies; {steps} steps, {secs:.1f} s of CPU work")
+
+
+def cpu_baseline(phi_total, world, steps_budget_s=10.0, max_steps=1000):
+    """The oracle port timed on the bounded sample (cpu_sample_size) until
+    about `steps_budget_s` of CPU work; value = sample params / median step."""
+    port = CpuPort(cpu_sample_size(phi_total), world)
+    port.step()  # warm-up (page-in)
     times = []
     t_start = time.perf_counter()
-    t = 1
-    while True:
-        s = O.scalars(t, world, h)
+    while time.perf_counter() - t_start < steps_budget_s and len(times) < max_steps:
         t0 = time.perf_counter()
-        O.step(grads, segs, master, m, v, params, s)
+        port.step()
         times.append(time.perf_counter() - t0)
-        t += 1
-        if time.perf_counter() - t_start > steps_budget_s or len(times) >= max_steps:
-            break
     med = sorted(times)[len(times) // 2]
-    cores = O.use_all_threads()
-    return {"value": n / med, "unit": "params/s", "cores": cores, "kind": "port",
-            "sample": f"{n} consecutive params of the {phi_total}-param flat model, {world} "
-                      f"rank gradients reduced + AdamW + bf16 into {world} param copies; "
-                      f"median of {len(times)} steps ({sum(times):.1f} s of CPU work), "
-                      f"{med * 1e3:.1f} ms/step",
-            "ms_per_step_extrapolated": med * phi_total / n * 1e3}
+    return {"value": port.n / med, "unit": "params/s", "cores": port.cores, "kind": "port",
+            "sample": port.describe(phi_total, len(times), sum(times)) +
+                      f", median {med * 1e3:.1f} ms/step",
+            "ms_per_step_full_workload_extrapolated": round(med * phi_total / port.n * 1e3, 1)}
+
+
+def planner_timings(binary):
+    """tests/cpp/plan_time.cpp (solve, build_schedule + simulate_step through
+    the public shardplan API) run from `binary`: list of JSON records, or an
+    error string."""
+    if not Path(binary).exists():
+        return f"{binary} not built"
+    try:
+        r = subprocess.run([str(binary)], capture_output=True, text=True, timeout=120)
+        if r.returncode != 0:
+            return f"exit {r.returncode}: {r.stderr[-300:]}"
+        return [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    except Exception as ex:  # reported, never required
+        return str(ex)
 
 
 def workload_config(args, S, world, phi):
     """The `config` object both arms print (same workload, same keys)."""
     dp = mesh_of(args.mesh, S) if args.mesh else S.DeviceMesh(world, 1)
     plan = plan_of(args, S, dp)
+    mb = getattr(args, "micro_batches", 1)
     return {"workload": f"{args.model} model states ({phi} params: bf16 P/G, fp32 "
-                        f"master+m+v), AMSP step = grad reduce + AdamW + param gather",
+                        f"master+m+v), AMSP step = grad reduce + AdamW + param gather" +
+                        (f", {mb} micro-batches (G-shard accumulation)" if mb > 1 else ""),
+            "micro_batches": mb,
             "model": args.model, "phi": phi, "plan": str(plan), "dp_mesh": str(dp),
             "layout": args.layout,
             "l2": f"inputs ({(16 * phi) / 1e9:.0f} GB of model state) >> 126 MB L2",
@@ -259,49 +318,43 @@ def workload_config(args, S, world, phi):
 
 
 def run_reference(args):
+    """The reference arm: the reference's CPU implementation of the path on
+    this box's host cores. The reference (shardplan) is a planner/simulator
+    with no data plane, so the step is the oracle's C/OpenMP restatement
+    ("port") on a bounded sample; the reference's own compiled planner and
+    simulator (oracle/_ref/plan_time_ref, built from /root/reference by
+    oracle/build_ref.sh) are timed beside it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2311_00257_b200 import shardplan as S
-    model = S.model(args.model)
-    phi = model.total_params
+    phi = S.model(args.model).total_params
     world = args.gpus
-    cpu = cpu_baseline(phi, world, steps_budget_s=10.0)
-    # K timed steps on the bounded sample (each step = one sample pass).
-    import numpy as np
-
-    from oracle import cpu as O
-    from paper_2311_00257_b200.engine import DEFAULT_SEED
-    n = 32 << 20
-    h = O.hyper()
-    O.use_all_threads()
-    grads = [O.grads(0, n, DEFAULT_SEED, 1, r) for r in range(world)]
-    master = np.full(n, 0.01, np.float32)
-    m = np.zeros(n, np.float32)
-    v = np.zeros(n, np.float32)
-    params = [np.zeros(n, np.uint16) for _ in range(world)]
-    for t in range(1, args.warmup + 1):
-        O.step(grads, [(0, 0, n)], master, m, v, params, O.scalars(t, world, h))
+    port = CpuPort(cpu_sample_size(phi), world)
+    for _ in range(args.warmup):
+        port.step()
     t0 = time.perf_counter()
-    for t in range(args.warmup + 1, args.warmup + args.steps + 1):
-        O.step(grads, [(0, 0, n)], master, m, v, params, O.scalars(t, world, h))
+    for _ in range(args.steps):
+        port.step()
     dt = (time.perf_counter() - t0) / args.steps
-    value = n / dt
-    cores = O.use_all_threads()
+    value = port.n / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "params/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt * phi / n * 1e3, "higher_is_better": True,
+        "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "fp32 (bf16 in/out)",
         "data": "synthetic",
         "config": workload_config(args, S, world, phi),
-        "cpu_baseline": {"value": value, "unit": "params/s", "cores": cores, "kind": "port",
-                         "sample": f"{n} consecutive params per step, {world} rank gradients"},
+        "cpu_baseline": {"value": value, "unit": "params/s", "cores": port.cores, "kind": "port",
+                         "sample": port.describe(phi, args.steps, dt * args.steps)},
         "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "note": "the reference (shardplan) is a CPU planner/simulator with no data plane; "
-                "its CPU path for this step is the oracle restatement (oracle/amsp_oracle.c)",
-        "cpu_baseline_detail": cpu,
+        "ms_per_step_full_workload_extrapolated": round(dt * phi / port.n * 1e3, 1),
+        "note": "a step = one oracle step over the bounded sample (value = sample params / "
+                "step time); the reference (shardplan) is a CPU planner/simulator with no "
+                "data plane, so its CPU path for this step is the oracle restatement "
+                "(oracle/amsp_oracle.c)",
+        "planner": planner_timings(REPO / "oracle" / "_ref" / "plan_time_ref"),
     }
     print(json.dumps(line), flush=True)
 
@@ -408,7 +461,9 @@ def run_ours(args):
     dp = mesh_of(args.mesh, S) if args.mesh else S.DeviceMesh(world, 1)
     model = S.model(args.model)
     plan = plan_of(args, S, dp)
-    eng = Engine(model, plan, dp, rank=rank, device=local, layout=args.layout)
+    MB = args.micro_batches
+    eng = Engine(model, plan, dp, rank=rank, device=local, layout=args.layout,
+                 micro_batches=MB)
     eng.connect()
     if args.variant or args.grid:
         eng.tune(args.variant, args.grid)
@@ -431,10 +486,18 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def amsp_step(t):
+        # M-1 accumulations of the resident micro-batch gradients into the G
+        # shards, then the fused update (the backward that would rewrite the
+        # gradient buffer between micro-batches is not part of the pipeline)
+        for k in range(MB - 1):
+            eng.accumulate(t, k, stream)
+        eng.step(t, stream)
+
     step = 0
     for _ in range(args.warmup):
         step += 1
-        eng.step(step, stream)
+        amsp_step(step)
     torch.cuda.synchronize()
     barrier()
 
@@ -450,7 +513,7 @@ def run_ours(args):
         ev0.record(stream)
         for _ in range(args.steps):
             step += 1
-            eng.step(step, stream)
+            amsp_step(step)
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -465,24 +528,32 @@ def run_ours(args):
     eng.stats()
     k_total, k_n = eng.kernel_ms()
     g_total, g_n = eng.gather_ms()
+    a_total, a_n = eng.accum_ms()
     eng.time_kernel(False)
     kernel_ms = max_over_ranks(k_total / max(k_n, 1))
     gather_ms = max_over_ranks(g_total / g_n) if g_n else 0.0
+    accum_ms = max_over_ranks(a_total / args.steps) if a_n else 0.0  # per step
 
     phi = info.total_params
     value = phi / (ms_per_step * 1e-3)
     pk, pk_src = peaks()
-    hbm_b, nvl_b = step_bytes(phi, info.owned, world, info.os_group_size, info.sp, plan.sos())
-    # s_p = 1: the step is one fused launch (+2 tiny barriers) -> time the
-    # kernel. s_p > 1: the all-gather passes are part of the roofline bytes,
-    # so the whole step is the timed unit.
-    t_meas = kernel_ms if info.sp == 1 else ms_per_step
+    sb = dict(sp=info.sp, sos=plan.sos(), micro=MB, acc_elems=info.acc_elems, sg=plan.sg())
+    hbm_b, nvl_b = step_bytes(phi, info.owned, world, info.os_group_size, **sb)
+    phases = step_bytes(phi, info.owned, world, info.os_group_size, phases=True, **sb)
+    # s_p = 1, M = 1: the step is one fused launch (+2 tiny barriers) -> time
+    # the kernel. s_p > 1 or M > 1: the all-gather passes / accumulations are
+    # part of the roofline bytes, so the whole step is the timed unit.
+    whole = info.sp > 1 or (MB > 1 and info.acc_elems > 0)
+    t_meas = ms_per_step if whole else kernel_ms
     kname = "fused_step_tma_kernel" if info.variant >= 5 else "fused_step_kernel"
-    scope = (f"{kname} (reduce + AdamW + gather), variant {info.variant}" if info.sp == 1 else
-             "whole step: 2 all-gather passes (" +
-             {"sm": "gather_kernel", "dma": "copy engines", "tma": "gather_tma_kernel",
-              "auto": "engine default: gather_tma_kernel when aligned"}[args.step_gather] +
-             ") + fused reduce/AdamW + barriers")
+    scope = (f"{kname} (reduce + AdamW + gather), variant {info.variant}" if not whole else
+             "whole step: " +
+             ("2 all-gather passes (" +
+              {"sm": "gather_kernel", "dma": "copy engines", "tma": "gather_tma_kernel",
+               "auto": "engine default: gather_tma_kernel when aligned"}[args.step_gather] +
+              ") + " if info.sp > 1 else "") +
+             (f"{MB - 1} G-shard accumulations (accumulate_kernel) + " if MB > 1 else "") +
+             "fused reduce/AdamW + barriers")
     hbm_ach = hbm_b / (t_meas * 1e-3) / 1e9
     nvl_ach = nvl_b / (t_meas * 1e-3) / 1e9
     t_hbm = hbm_b / (pk["hbm_gbs"] * 1e9)
@@ -499,8 +570,10 @@ def run_ours(args):
         "kernel_ms": round(kernel_ms, 4),
         "timed_ms": round(t_meas, 4),
         "step_breakdown_ms": {"all_gather_passes": round(gather_ms, 4),
+                              "g_shard_accumulations": round(accum_ms, 4),
                               "fused_reduce_adamw_gather": round(kernel_ms, 4),
-                              "barriers_and_gaps": round(ms_per_step - gather_ms - kernel_ms, 4)},
+                              "barriers_and_gaps": round(ms_per_step - gather_ms - accum_ms -
+                                                         kernel_ms, 4)},
         "algorithmic_bytes": {"hbm": hbm_b, "nvlink_per_direction": nvl_b},
         "hbm": {"achieved": round(hbm_ach, 1), "peak": pk["hbm_gbs"],
                 "frac": round(hbm_ach / pk["hbm_gbs"], 4), "peak_source": pk_src},
@@ -511,6 +584,18 @@ def run_ours(args):
         "lower_bound_ms": round(max(t_hbm, t_nvl) * 1e3, 3),
         "frac_of_roofline_step": round(max(t_hbm, t_nvl) * 1e3 / ms_per_step, 4),
     }
+    if len(phases) > 1:
+        # The phases (all-gathers, accumulations, update) run one after the
+        # other in the pipeline-only step: each is bound by its own
+        # max(HBM, NVLink) time, and the step by their sum.
+        pb = [{"phase": n, "hbm_bytes": h, "nvlink_bytes_per_direction": v,
+               "bound_ms": round(max(h / (pk["hbm_gbs"] * 1e9), v / (NVLINK_P2P_GBS * 1e9)) *
+                                 1e3, 3)} for n, h, v in phases]
+        roof["phase_bounds"] = pb
+        roof["phase_bound_ms"] = round(sum(x["bound_ms"] for x in pb), 3)
+        roof["frac_of_phase_bound"] = round(roof["phase_bound_ms"] / ms_per_step, 4)
+        roof["bound_note"] = ("lower_bound_ms assumes the phases overlap (sum of bytes / peak); "
+                              "phase_bound_ms is the serial pipeline's bound")
     ncu_traffic = REPO / "profiles" / "r01_traffic.json"
     if ncu_traffic.exists():
         try:
@@ -528,11 +613,32 @@ def run_ours(args):
 
     # Busbw of the collective the fused kernel implements (nccl-tests
     # convention: RS/AG (n-1)/n on the gathered size; AR 2(n-1)/n).
+    # The fused kernel performs the reduce-scatter and the all-gather
+    # concurrently in one launch, i.e. an all-reduce of the 2*Phi-byte bf16
+    # gradient buffer (values in, updated values out): ONE busbw, AR
+    # convention 2(n-1)/n * bytes / time.
     busbw = None
-    if world > 1:
-        busbw = {"reduce_scatter_equiv_gbs": round(2 * phi * (world - 1) / world / (kernel_ms * 1e-3) / 1e9, 1),
-                 "all_gather_equiv_gbs": round(2 * phi * (world - 1) / world / (kernel_ms * 1e-3) / 1e9, 1),
-                 "vs_nvlink_gbs": NVLINK_NOMINAL_GBS}
+    if world > 1 and info.sp == 1:
+        bw = 2 * (world - 1) / world * 2 * phi / (kernel_ms * 1e-3) / 1e9
+        busbw = {"allreduce_equiv_busbw_gbs": round(bw, 1),
+                 "convention": "nccl-tests AR: 2(n-1)/n x 2*Phi bytes / fused-kernel time "
+                               "(RS + AG in one launch)",
+                 "vs_nvlink_p2p_gbs": NVLINK_P2P_GBS, "vs_nvlink_nominal_gbs": NVLINK_NOMINAL_GBS,
+                 "frac_of_nominal": round(bw / NVLINK_NOMINAL_GBS, 4)}
+    # This box's NVLink peer-read peak, measured in-run after the timed
+    # region (every rank pulls an equal share from every peer; the slowest
+    # rank's ingress).
+    nvl_probe = None
+    if world > 1 and not oversub:
+        try:
+            ingress = eng.nvlink_probe(1 << 32, "all")
+            nvl_probe = -max_over_ranks(-ingress)
+            roof["nvlink"]["peak_measured_in_run_gbs"] = round(nvl_probe, 1)
+            roof["nvlink"]["frac_of_measured_peak"] = round(nvl_ach / nvl_probe, 4)
+            if busbw:
+                busbw["nvlink_peer_read_measured_gbs"] = round(nvl_probe, 1)
+        except Exception as ex:  # reported, never required
+            roof["nvlink"]["peak_measured_in_run_error"] = str(ex)
 
     # Overlapped step: the reference event graph replayed by the scheduler on
     # 3 streams; measured with real cuBLAS GEMM compute (the realistic case)
@@ -541,7 +647,8 @@ def run_ours(args):
     def measure_overlap(compute):
         nonlocal step
         from paper_2311_00257_b200.engine import Scheduler, b200_profile
-        mspec = S.model(args.model, micro_batch=args.micro_batch, seq_len=args.seq_len)
+        mspec = S.model(args.model, micro_batch=args.micro_batch, seq_len=args.seq_len,
+                        micro_batch_count=MB)
         peak_tf = pk.get("bf16_tflops_sustained", 1400.0)
         sim = S.SimConfig(overlap_tier=args.tier, peak_flops_per_gpu=peak_tf * 1e12,
                           compute_efficiency=args.compute_eff)
@@ -562,7 +669,8 @@ def run_ours(args):
         sched = Scheduler(eng, mspec, b200_profile(), S.CostConfig(), sim, comm_ctas=ctas,
                           optimizer_overlap=bool(opt), compute=compute,
                           gemm_sm_margin=args.gemm_sm_margin, gather=args.gather, bc=args.bc,
-                          reduce=reduce)
+                          reduce=reduce,
+                          grad_source="synth" if (MB > 1 and compute == "standin") else "caller")
 
         def timed(with_comm, k):
             nonlocal step
@@ -578,6 +686,19 @@ def run_ours(args):
             barrier()
             return max_over_ranks(a.elapsed_time(b) / k)
 
+        # FLOPs of the compute stream per step: the reference's compute model
+        # (overlap_sim.cpp:97-110, flops_coeff_param 6 / flops_coeff_attn 12)
+        # and, for compute='gemm', what the kernels execute (linear modules
+        # incl. the LM head at 6 FLOPs/param/token, no embedding GEMM; the
+        # attention GEMMs compute the full S x S square = 12*B*S^2*H/layer).
+        toks = args.micro_batch * args.seq_len * MB
+        H, L, S_ = mspec.hidden, mspec.layer_count, args.seq_len
+        attn = 12.0 * L * args.micro_batch * MB * S_ * S_ * H
+        lin_params = phi - mspec.vocab * H - (2 * L + 1) * H  # minus embedding and norms
+        flops = {"model_6PhiBS_plus_attention": 6.0 * phi * toks + attn,
+                 "total": (6.0 * lin_params * toks + attn) if compute == "gemm"
+                 else 6.0 * phi * toks + attn}
+        flops["executed_over_model"] = round(flops["total"] / flops["model_6PhiBS_plus_attention"], 4)
         timed(True, args.warmup)
         t_b = timed(True, args.steps)
         t_c = timed(False, args.steps)
@@ -621,11 +742,16 @@ def run_ours(args):
                 "predicted_compute_ms": round(si.predicted_compute_s * 1e3, 3),
                 "events": si.n_events, "buckets": si.n_buckets, "gathers": si.n_gather,
                 "reduces": si.n_reduce, "barriers": si.n_barriers,
-                "compute_model": (f"timed stand-ins: 6*Phi*B*S at {peak_tf} TF/s x "
-                                  f"{args.compute_eff}" if compute == "standin" else
-                                  "cuBLAS bf16 GEMMs of every linear module (fwd, dgrad, "
-                                  "wgrad into the gradient buffer), norms as stand-ins, "
-                                  "no attention"),
+                "compute_model": (f"timed stand-ins: (6*Phi*B*S + 12*L*B*S^2*H) FLOPs at "
+                                  f"{peak_tf} TF/s x {args.compute_eff}" if compute == "standin"
+                                  else "real layer compute: cuBLAS bf16 GEMMs of every linear "
+                                  "module (fwd, dgrad, wgrad into the gradient buffer), the "
+                                  "attention core (strided-batched QK^T / PV GEMMs + causal "
+                                  "softmax, and their backward) in the o-projection's events, "
+                                  "RMSNorm kernels (fwd, dgrad, weight grad into the gradient "
+                                  "buffer) for the norm modules"),
+                "compute_flops": flops,
+                "compute_only_tflops": round(flops["total"] / (t_c * 1e-3) / 1e12, 1),
                 "profile": "synthetic B200 NVLink alpha-beta (680 GB/s, 5 us)"}
 
     overlap = None
@@ -672,11 +798,15 @@ def run_ours(args):
         del host
 
     cpu = None
+    planner = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
             cpu = cpu_baseline(phi, world, steps_budget_s=10.0)
         except Exception as ex:  # the baseline is reported, never required
             cpu = {"error": str(ex)}
+        from paper_2311_00257_b200 import build as B
+        planner = {"ours": planner_timings(B.PLAN_TIME),
+                   "reference": planner_timings(REPO / "oracle" / "_ref" / "plan_time_ref")}
 
     if rank == 0:
         clk = clocks.summary()
@@ -687,7 +817,7 @@ def run_ours(args):
             "dtype": "fp32 (bf16 grads/params)", "data": "synthetic",
             "config": workload_config(args, S, world, phi),
             "roofline": roof, "busbw": busbw, "overlap": overlap, "e2e": e2e,
-            "cpu_baseline": cpu,
+            "cpu_baseline": cpu, "planner": planner,
             "gpu_launches": launches, "clocks": clk,
         }
         if oversub:

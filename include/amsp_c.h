@@ -323,6 +323,14 @@ int amsp_engine_import_handles(amsp_engine_t* e, const void* handles, int world)
  * engines skip the cross-GPU barriers, so the caller must run their steps
  * one after another on one stream (synth all grads, then step every rank). */
 int amsp_engine_link_local(amsp_engine_t* const* engines, int n);
+/* Like amsp_engine_link_local, but the linked engines keep the multi-GPU
+ * synchronisation: every engine issues on its OWN default stream and runs
+ * the real barrier_kernel flag protocol and the __threadfence_system release
+ * of its parameter stores, exactly as with separate GPUs (one process, one
+ * CUDA context: the ranks' kernels share the device, they are not
+ * time-sliced processes). Calls may be interleaved rank by rank; the
+ * barriers order them. */
+int amsp_engine_link_local_sync(amsp_engine_t* const* engines, int n);
 /* master = 0.02*u(seed, i), m = v = 0, params = bf16(master) (all ranks
  * derive the identical replicated initial parameters locally). */
 int amsp_engine_init_state(amsp_engine_t* e, void* stream);
@@ -494,6 +502,9 @@ void amsp_sched_destroy(amsp_sched_t* s);
 /* dst[k] = grad(seed, step, rank, start+k) as bf16, k < n */
 int amsp_k_synth_grad(void* dst_bf16, uint64_t start, uint64_t n, uint64_t seed,
                       int step, int rank, void* stream);
+/* Compute stand-in: `ctas` CTAs each keep issuing FMAs for `ns` nanoseconds
+ * (the overlap scheduler's timed compute; tests use it to delay a stream). */
+int amsp_k_spin(int ctas, uint64_t ns, void* stream);
 /* Plain fused AdamW on a contiguous shard: fp32 or bf16 grads (grad_is_bf16),
  * grad_scale applied, bf16 copy of the updated master written to param_out
  * (may be NULL). */

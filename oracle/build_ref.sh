@@ -4,7 +4,8 @@
 # Compiles the unmodified reference planner/simulator (`shardplan`,
 # /root/reference/proj/src/*.cpp) from the sources where they lie into
 # oracle/_ref/libshardplan_ref.so, and links the golden-vector driver
-# tests/cpp/plan_dump.cpp against it (oracle/_ref/plan_dump_ref).
+# tests/cpp/plan_dump.cpp against it (oracle/_ref/plan_dump_ref), and the
+# planner timing driver tests/cpp/plan_time.cpp (oracle/_ref/plan_time_ref).
 # No reference source is copied into this repo; outputs go to oracle/_ref/
 # only (git-ignored, but shipped to the GPU box by gpurun).
 #
@@ -34,6 +35,11 @@ done
 $CXX -shared -fopenmp -o "$OUT/libshardplan_ref.so" "${objs[@]}"
 if [ -f "$REPO/tests/cpp/plan_dump.cpp" ]; then
   $CXX $FLAGS "$REPO/tests/cpp/plan_dump.cpp" -o "$OUT/plan_dump_ref" \
+      -L"$OUT" -lshardplan_ref -Wl,-rpath,'$ORIGIN'
+fi
+# Planner/simulator timing driver (bench.py --impl reference times it).
+if [ -f "$REPO/tests/cpp/plan_time.cpp" ]; then
+  $CXX $FLAGS "$REPO/tests/cpp/plan_time.cpp" -o "$OUT/plan_time_ref" \
       -L"$OUT" -lshardplan_ref -Wl,-rpath,'$ORIGIN'
 fi
 echo "build_ref: wrote $OUT"

@@ -195,6 +195,7 @@ SIGNATURES = {
     "amsp_engine_unit": (C.c_int, [vp, C.c_int, P(C.c_int), P(C.c_int), P(u64)]),
     "amsp_engine_gather": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "amsp_engine_link_local": (C.c_int, [P(vp), C.c_int]),
+    "amsp_engine_link_local_sync": (C.c_int, [P(vp), C.c_int]),
     "amsp_engine_init_state": (C.c_int, [vp, vp]),
     "amsp_engine_synth_grads": (C.c_int, [vp, C.c_int, vp]),
     "amsp_engine_synth_grads_mb": (C.c_int, [vp, C.c_int, C.c_int, vp]),
@@ -227,6 +228,7 @@ SIGNATURES = {
                                C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                vp]),
     "amsp_k_upcast_scale": (C.c_int, [vp, vp, u64, C.c_float, vp]),
+    "amsp_k_spin": (C.c_int, [C.c_int, u64, vp]),
     "amsp_k_rs_upcast_scale": (C.c_int, [P(vp), C.c_int, u64, vp, u64, C.c_float, vp]),
     "amsp_k_ag_downcast": (C.c_int, [vp, u64, P(vp), C.c_int, u64, vp]),
 }

@@ -131,8 +131,30 @@ def build_reference() -> None:
                        capture_output=True)
 
 
+PLAN_TIME = BUILD / "plan_time"
+
+
+def build_plan_time() -> Path:
+    """tests/cpp/plan_time.cpp (planner/simulator timing through the public
+    shardplan API) linked against libamsp.so; oracle/build_ref.sh links the
+    same source against the reference."""
+    src = REPO / "tests" / "cpp" / "plan_time.cpp"
+    cmd = [CXX, "-std=c++20", "-O2", "-I", str(REPO / "include"), str(src), "-o",
+           str(PLAN_TIME), "-L", str(PKG), "-lamsp", "-Wl,-rpath,$ORIGIN/.."]
+    stamp_file = PLAN_TIME.with_suffix(".stamp")
+    stamp = _stamp(cmd, src, _headers() + [LIB])
+    if PLAN_TIME.exists() and stamp_file.exists() and stamp_file.read_text() == stamp:
+        return PLAN_TIME
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"plan_time build failed:\n{r.stderr}")
+    stamp_file.write_text(stamp)
+    return PLAN_TIME
+
+
 def build_all(verbose: bool = False) -> None:
     build_library(verbose)
+    build_plan_time()
     build_oracle()
     build_reference()
 

@@ -36,24 +36,58 @@ Blas::Blas() {
   set_sm_target_ =
       reinterpret_cast<decltype(set_sm_target_)>(dlsym(lib_, "cublasSetSmCountTarget"));
   auto gemm = reinterpret_cast<decltype(gemm_ex_)>(dlsym(lib_, "cublasGemmEx"));
+  gemm_sb_ = reinterpret_cast<decltype(gemm_sb_)>(dlsym(lib_, "cublasGemmStridedBatchedEx"));
   if (!create_ || !set_stream_ || !gemm) return;
   if (create_(&handle_) != 0) return;
   gemm_ex_ = gemm;
 }
 
+void* Blas::handle_for(cudaStream_t s) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) throw shardplan::Error("cudaGetDevice failed");
+  std::lock_guard<std::mutex> lock(mu_);
+  auto it = handles_.find({dev, s});
+  if (it == handles_.end()) {
+    void* h = nullptr;
+    if (create_(&h) != 0) throw shardplan::Error("cublasCreate failed");
+    if (set_stream_(h, s) != 0) throw shardplan::Error("cublasSetStream failed");
+    it = handles_.emplace(std::make_pair(dev, s), std::make_pair(h, 0)).first;
+  }
+  if (it->second.second != sm_target_ && set_sm_target_) {
+    if (set_sm_target_(it->second.first, sm_target_) != 0)
+      throw shardplan::Error("cublasSetSmCountTarget failed");
+    it->second.second = sm_target_;
+  }
+  return it->second.first;
+}
+
 void Blas::gemm(cudaStream_t s, bool ta, bool tb, int m, int n, int k, const void* a, int lda,
                 const void* b, int ldb, void* c, int ldc, bool accumulate) {
   const float one = 1.0f, zero = 0.0f;
-  if (set_stream_(handle_, s) != 0) throw shardplan::Error("cublasSetStream failed");
-  const int st = gemm_ex_(handle_, ta ? kOpT : kOpN, tb ? kOpT : kOpN, m, n, k, &one, a, kBf16,
-                          lda, b, kBf16, ldb, accumulate ? &one : &zero, c, kBf16, ldc,
+  const int st = gemm_ex_(handle_for(s), ta ? kOpT : kOpN, tb ? kOpT : kOpN, m, n, k, &one, a,
+                          kBf16, lda, b, kBf16, ldb, accumulate ? &one : &zero, c, kBf16, ldc,
                           kCompute32F, kAlgoDefault);
   if (st != 0) throw shardplan::Error("cublasGemmEx failed with status " + std::to_string(st));
 }
 
+void Blas::bgemm(cudaStream_t s, bool ta, bool tb, int M, int N, int K, const void* A, int lda,
+                 long long sA, const void* B, int ldb, long long sB, void* C, int ldc,
+                 long long sC, int batch) {
+  if (!gemm_sb_) throw shardplan::Error("cublasGemmStridedBatchedEx not found in cuBLAS");
+  const float one = 1.0f, zero = 0.0f;
+  // row-major C = op(A) op(B)  <=>  col-major C^T = op(B)^T op(A)^T
+  const int st = gemm_sb_(handle_for(s), tb ? kOpT : kOpN, ta ? kOpT : kOpN, N, M, K, &one, B,
+                          kBf16, ldb, sB, A, kBf16, lda, sA, &zero, C, kBf16, ldc, sC, batch,
+                          kCompute32F, kAlgoDefault);
+  if (st != 0)
+    throw shardplan::Error("cublasGemmStridedBatchedEx failed with status " + std::to_string(st));
+}
+
 void Blas::set_sm_target(int sms) {
-  if (!set_sm_target_) return;  // older cuBLAS: ignore the hint
-  if (set_sm_target_(handle_, sms) != 0) throw shardplan::Error("cublasSetSmCountTarget failed");
+  // applied to each stream's handle at its next GEMM (older cuBLAS without
+  // cublasSetSmCountTarget: ignored)
+  std::lock_guard<std::mutex> lock(mu_);
+  sm_target_ = sms;
 }
 
 // Column-major views: a row-major [r, c] matrix is a col-major [c, r] one.

@@ -251,6 +251,30 @@ void* buffer_ptr(amsp_engine_t* e, int which, std::size_t* elem, std::uint64_t* 
   }
 }
 
+// Single-GPU emulation of a group: every engine maps the others' buffers as
+// its peers (amsp_engine_link_local / _sync).
+void link_local(amsp_engine_t* const* engines, int n, bool sync) {
+  if (!engines || n < 1) throw Error("engine: null argument");
+  for (int r = 0; r < n; ++r) {
+    const amsp_engine* e = engines[r];
+    if (!e || e->world != n || e->rank != r || e->cfg.device != engines[0]->cfg.device ||
+        e->phi != engines[0]->phi)
+      throw Error("engine: link_local needs ranks 0..n-1 of one group on one device");
+  }
+  for (int r = 0; r < n; ++r) {
+    amsp_engine* e = engines[r];
+    for (int q = 0; q < n; ++q) e->peer_base[q] = engines[q]->shared;
+    e->use_device();
+    e->publish_peer_flags();
+    e->imported = true;
+    e->local_linked = true;
+    e->local_sync = sync;
+    // unsynchronised emulation: one stream orders the ranks' calls;
+    // synchronised: every rank on its own stream, the barriers order them
+    e->shared_default = sync ? nullptr : engines[0]->own_stream;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -346,25 +370,13 @@ int amsp_engine_import_handles(amsp_engine_t* e, const void* handles, int world)
   });
 }
 
+
 int amsp_engine_link_local(amsp_engine_t* const* engines, int n) {
-  return amsp::guarded([&] {
-    if (!engines || n < 1) throw Error("engine: null argument");
-    for (int r = 0; r < n; ++r) {
-      const amsp_engine* e = engines[r];
-      if (!e || e->world != n || e->rank != r || e->cfg.device != engines[0]->cfg.device ||
-          e->phi != engines[0]->phi)
-        throw Error("engine: link_local needs ranks 0..n-1 of one group on one device");
-    }
-    for (int r = 0; r < n; ++r) {
-      amsp_engine* e = engines[r];
-      for (int q = 0; q < n; ++q) e->peer_base[q] = engines[q]->shared;
-      e->use_device();
-      e->publish_peer_flags();
-      e->imported = true;
-      e->local_linked = true;
-      e->shared_default = engines[0]->own_stream;
-    }
-  });
+  return amsp::guarded([&] { link_local(engines, n, false); });
+}
+
+int amsp_engine_link_local_sync(amsp_engine_t* const* engines, int n) {
+  return amsp::guarded([&] { link_local(engines, n, true); });
 }
 
 int amsp_engine_init_state(amsp_engine_t* e, void* stream) {
@@ -651,6 +663,13 @@ int amsp_k_synth_grad(void* dst_bf16, uint64_t start, uint64_t n, uint64_t seed,
     ck(amsp::launch_synth_grad(static_cast<uint16_t*>(dst_bf16), start, n, seed, step,
                                rank, static_cast<cudaStream_t>(stream)),
        "synth grad");
+  });
+}
+
+int amsp_k_spin(int ctas, uint64_t ns, void* stream) {
+  return amsp::guarded([&] {
+    if (ctas < 1 || ctas > 65535) throw Error("spin: 1..65535 CTAs");
+    ck(amsp::launch_spin(ctas, ns, static_cast<cudaStream_t>(stream)), "spin");
   });
 }
 

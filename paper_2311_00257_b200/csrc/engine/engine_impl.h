@@ -86,7 +86,10 @@ struct amsp_engine {
   std::uint64_t param_elems = 0;
   void* peer_base[amsp::kMaxRanks] = {};
   bool imported = false;
-  bool local_linked = false;  // single-GPU emulation: no barriers
+  bool local_linked = false;  // single-GPU emulation of a group
+  bool local_sync = false;    // ... with the real barriers / release fences
+  // Cross-rank synchronisation is live (real group, or emulated with sync).
+  bool synced() const { return world > 1 && (!local_linked || local_sync); }
 
   float* master = nullptr;
   float* exp_avg = nullptr;
@@ -220,7 +223,7 @@ struct amsp_engine {
   }
 
   void barrier(cudaStream_t s) {
-    if (world == 1 || local_linked) return;
+    if (!synced()) return;
     ++epoch;
     // ids 0/1 alternate (pre / post); the epoch keeps each id monotonic.
     ck(amsp::launch_barrier(d_peer_flags, world, rank, static_cast<int>(epoch & 1), epoch, err, s),
@@ -294,7 +297,7 @@ struct amsp_engine {
     a.s = amsp::make_adam_scalars(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, t,
                                   grad_scale());
     a.stats = stats;
-    a.fence_peers = (world > 1 && !local_linked) ? 1 : 0;
+    a.fence_peers = synced() ? 1 : 0;
     for (std::size_t c = 0; c < chunk_begin.size(); ++c) {
       const std::uint64_t lo = c * kHostChunk, n = std::min(kHostChunk, phi - lo);
       ck(cudaMemcpyAsync(dst + lo * 2, src + lo * 2, n * 2, cudaMemcpyHostToDevice, copy_stream),
@@ -425,7 +428,7 @@ struct amsp_engine {
     a.s = amsp::make_adam_scalars(cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
                                   cfg.weight_decay, t, grad_scale());
     a.stats = stats;
-    a.fence_peers = (world > 1 && !local_linked) ? 1 : 0;
+    a.fence_peers = synced() ? 1 : 0;
     int v = variant, g = grid;
     if (staged) {
       // the holders' accumulators first, then the raw last micro-batch

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -275,7 +276,9 @@ fused_step_kernel(const FusedArgs a) {
 // r's word [id][rank] and waits until its own word [id][r] reaches the
 // epoch. Distinct ids never interfere, so barriers issued on different
 // streams may complete in any order. Bounded wait: after ~20 s it raises
-// *err instead of hanging.
+// *err instead of hanging; once *err is set (by this or an earlier barrier
+// of the rank) every later barrier gives up at once, so a lost peer costs
+// one timeout, not one per barrier of the step.
 __global__ void barrier_kernel(uint32_t* const* peer_flags, int world, int rank, int id,
                                uint32_t epoch, int* err) {
   const int t = threadIdx.x;
@@ -294,6 +297,7 @@ __global__ void barrier_kernel(uint32_t* const* peer_flags, int world, int rank,
                    : "l"(mine)
                    : "memory");
       if (static_cast<int32_t>(seen - epoch) >= 0) break;
+      if (*reinterpret_cast<volatile int*>(err)) break;
       uint64_t now;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       if (now - t0 > 20000000000ull) {
@@ -421,36 +425,132 @@ __global__ void synth_grad_kernel(uint16_t* __restrict__ dst, unsigned long long
   }
 }
 
-// Plain AdamW over a contiguous shard (the NCCL-path optimizer and the raw
-// amsp_k_adamw launcher).
-template <bool kBf16Grad>
-__global__ void adamw_flat_kernel(const void* __restrict__ grad, float* master, float* m,
-                                  float* v, uint16_t* param_out, unsigned long long n,
-                                  AdamScalars s) {
-  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-  for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    float g = kBf16Grad ? bf16_at(static_cast<const uint16_t*>(grad)[i])
-                        : static_cast<const float*>(grad)[i];
-    g = __fmul_rn(g, s.grad_scale);
-    float p = master[i], mm = m[i], vv = v[i];
-    adamw(s, g, p, mm, vv);
-    master[i] = p;
-    m[i] = mm;
-    v[i] = vv;
-    if (param_out) param_out[i] = to_bf16(p);
+// ---------------------------------------------------------------------------
+// Raw C-ABI kernels (amsp_k_*) over plain contiguous buffers. Each thread
+// owns kRawU 8-element groups per iteration and issues every 128-bit load of
+// those groups before the first arithmetic op, so each SM keeps >= 8 KB of
+// reads in flight (HBM3e needs ~40 KB/SM at 8 TB/s; with 8 CTAs of 256
+// threads per SM that is 8*256*kRawU*bytes_per_group). The vector path
+// needs every base pointer 16-byte aligned at the group boundary; a ragged
+// tail (n % 8) and misaligned buffers take the scalar path, which performs
+// the same rounded operations, so the result never depends on alignment.
+constexpr int kRawU = 4;
+
+__device__ __forceinline__ bool al16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& w, float* x) {
+  const uint32_t* u = reinterpret_cast<const uint32_t*>(&w);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    x[2 * k] = bf16_lo(u[k]);
+    x[2 * k + 1] = bf16_hi(u[k]);
   }
 }
 
-__global__ void upcast_scale_kernel(const uint16_t* __restrict__ src, float* __restrict__ dst,
-                                    unsigned long long n, float scale) {
-  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-  for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    dst[i] = __fmul_rn(bf16_at(src[i]), scale);
+__device__ __forceinline__ uint4 pack8(const float* x) {
+  return make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]),
+                    pack_bf16x2(x[6], x[7]));
 }
 
-// Raw reduce-scatter epilogue over plain pointers (amsp_k_rs_upcast_scale):
-// dst[k] = (sum_r bf16 srcs[r][offset + k]) * scale, fixed rank order, the
-// same rounding sequence as the fused kernel. srcs may be peer pointers.
+// Grid-stride driver: fn_vec(group indices, valid mask) for full vector
+// groups, fn_scalar(i) for the rest.
+template <int U, class Vec, class Scalar>
+__device__ __forceinline__ void raw_loop(unsigned long long n, bool vec_ok, Vec fn_vec,
+                                         Scalar fn_scalar) {
+  const unsigned long long groups = vec_ok ? n / 8 : 0;
+  const unsigned long long tid = static_cast<unsigned long long>(blockIdx.x) * blockDim.x +
+                                 threadIdx.x;
+  const unsigned long long nthr = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  for (unsigned long long g0 = tid; g0 < groups; g0 += nthr * U) {
+    unsigned long long g[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      g[u] = g0 + u * nthr;
+      ok[u] = g[u] < groups;
+    }
+    fn_vec(g, ok);
+  }
+  for (unsigned long long i = groups * 8 + tid; i < n; i += nthr) fn_scalar(i);
+}
+
+// Plain AdamW over a contiguous shard (the raw amsp_k_adamw launcher):
+// g = grad * scale (bf16 or fp32 grad), AdamW, optional bf16 param out.
+template <bool kBf16Grad, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) adamw_flat_kernel(const void* __restrict__ grad,
+                                                         float* master, float* m, float* v,
+                                                         uint16_t* param_out,
+                                                         unsigned long long n, AdamScalars s) {
+  const bool vec_ok = al16(grad) && al16(master) && al16(m) && al16(v) &&
+                      (param_out == nullptr || al16(param_out));
+  raw_loop<U>(
+      n, vec_ok,
+      [=](const unsigned long long* g, const bool* ok) {
+        uint4 gb[U];
+        float4 gf[U][U], p[U][U], mm[U][U], vv[U][U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (!ok[u]) continue;
+          const unsigned long long i = g[u] * 8;
+          if (kBf16Grad) {
+            gb[u] = ld_ro_v4(static_cast<const uint16_t*>(grad) + i);
+          } else {
+            const float* gp = static_cast<const float*>(grad) + i;
+            gf[u][0] = ld_state_v4(gp);
+            gf[u][1] = ld_state_v4(gp + 4);
+          }
+          p[u][0] = ld_state_v4(master + i);
+          p[u][1] = ld_state_v4(master + i + 4);
+          mm[u][0] = ld_state_v4(m + i);
+          mm[u][1] = ld_state_v4(m + i + 4);
+          vv[u][0] = ld_state_v4(v + i);
+          vv[u][1] = ld_state_v4(v + i + 4);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (!ok[u]) continue;
+          const unsigned long long i = g[u] * 8;
+          float x[8];
+          if (kBf16Grad) {
+            unpack8(gb[u], x);
+          } else {
+            const float* f = reinterpret_cast<const float*>(&gf[u][0]);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) x[k] = f[k];
+          }
+          float* pf = reinterpret_cast<float*>(&p[u][0]);
+          float* mf = reinterpret_cast<float*>(&mm[u][0]);
+          float* vf = reinterpret_cast<float*>(&vv[u][0]);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) adamw(s, __fmul_rn(x[k], s.grad_scale), pf[k], mf[k], vf[k]);
+          st_stream_v4(master + i, p[u][0]);
+          st_stream_v4(master + i + 4, p[u][1]);
+          st_stream_v4(m + i, mm[u][0]);
+          st_stream_v4(m + i + 4, mm[u][1]);
+          st_stream_v4(v + i, vv[u][0]);
+          st_stream_v4(v + i + 4, vv[u][1]);
+          if (param_out) st_v4(param_out + i, pack8(pf));
+        }
+      },
+      [=](unsigned long long i) {
+        float g = kBf16Grad ? bf16_at(static_cast<const uint16_t*>(grad)[i])
+                            : static_cast<const float*>(grad)[i];
+        g = __fmul_rn(g, s.grad_scale);
+        float p = master[i], mm = m[i], vv = v[i];
+        adamw(s, g, p, mm, vv);
+        master[i] = p;
+        m[i] = mm;
+        v[i] = vv;
+        if (param_out) param_out[i] = to_bf16(p);
+      });
+}
+
+// Raw reduce-scatter epilogue over plain pointers (amsp_k_rs_upcast_scale,
+// and amsp_k_upcast_scale with one source): dst[k] = (sum_r bf16
+// srcs[r][offset + k]) * scale, fixed rank order, the same rounding sequence
+// as the fused kernel. srcs may be peer pointers (NVLink reads).
 struct RsArgs {
   const uint16_t* srcs[kMaxRanks];
   int nsrc;
@@ -459,13 +559,45 @@ struct RsArgs {
   float scale;
 };
 
-__global__ void rs_upcast_scale_kernel(const RsArgs a) {
-  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-  for (unsigned long long k = blockIdx.x * blockDim.x + threadIdx.x; k < a.n; k += stride) {
-    float g = bf16_at(a.srcs[0][a.offset + k]);
-    for (int r = 1; r < a.nsrc; ++r) g = __fadd_rn(g, bf16_at(a.srcs[r][a.offset + k]));
-    a.dst[k] = __fmul_rn(g, a.scale);
-  }
+template <int NS>
+__global__ void __launch_bounds__(256, 2) rs_upcast_scale_kernel(const RsArgs a) {
+  constexpr int kU = NS <= 2 ? 4 : 2;
+  bool vec_ok = al16(a.dst);
+#pragma unroll
+  for (int r = 0; r < NS; ++r) vec_ok = vec_ok && al16(a.srcs[r] + a.offset);
+  raw_loop<kU>(
+      a.n, vec_ok,
+      [=](const unsigned long long* g, const bool* ok) {
+        uint4 w[kU][NS];
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+#pragma unroll
+          for (int r = 0; r < NS; ++r)
+            if (ok[u]) w[u][r] = ld_ro_v4(a.srcs[r] + a.offset + g[u] * 8);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          if (!ok[u]) continue;
+          float x[8], y[8];
+          unpack8(w[u][0], x);
+#pragma unroll
+          for (int r = 1; r < NS; ++r) {
+            unpack8(w[u][r], y);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) x[k] = __fadd_rn(x[k], y[k]);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) x[k] = __fmul_rn(x[k], a.scale);
+          float* d = a.dst + g[u] * 8;
+          st_stream_v4(d, make_float4(x[0], x[1], x[2], x[3]));
+          st_stream_v4(d + 4, make_float4(x[4], x[5], x[6], x[7]));
+        }
+      },
+      [=](unsigned long long k) {
+        float g = bf16_at(a.srcs[0][a.offset + k]);
+#pragma unroll
+        for (int r = 1; r < NS; ++r) g = __fadd_rn(g, bf16_at(a.srcs[r][a.offset + k]));
+        a.dst[k] = __fmul_rn(g, a.scale);
+      });
 }
 
 // Raw all-gather epilogue (amsp_k_ag_downcast): bf16(src[k]) stored into
@@ -477,12 +609,34 @@ struct AgArgs {
   const float* src;
 };
 
-__global__ void ag_downcast_kernel(const AgArgs a) {
-  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-  for (unsigned long long k = blockIdx.x * blockDim.x + threadIdx.x; k < a.n; k += stride) {
-    const uint16_t b = to_bf16(a.src[k]);
-    for (int d = 0; d < a.ndst; ++d) a.dsts[d][a.dst_offset + k] = b;
-  }
+template <int ND>
+__global__ void __launch_bounds__(256) ag_downcast_kernel(const AgArgs a) {
+  bool vec_ok = al16(a.src);
+#pragma unroll
+  for (int d = 0; d < ND; ++d) vec_ok = vec_ok && al16(a.dsts[d] + a.dst_offset);
+  raw_loop<kRawU>(
+      a.n, vec_ok,
+      [=](const unsigned long long* g, const bool* ok) {
+        float4 x[kRawU][2];
+#pragma unroll
+        for (int u = 0; u < kRawU; ++u) {
+          if (!ok[u]) continue;
+          x[u][0] = ld_state_v4(a.src + g[u] * 8);
+          x[u][1] = ld_state_v4(a.src + g[u] * 8 + 4);
+        }
+#pragma unroll
+        for (int u = 0; u < kRawU; ++u) {
+          if (!ok[u]) continue;
+          const uint4 b = pack8(reinterpret_cast<const float*>(&x[u][0]));
+#pragma unroll
+          for (int d = 0; d < ND; ++d) st_v4(a.dsts[d] + a.dst_offset + g[u] * 8, b);
+        }
+      },
+      [=](unsigned long long k) {
+        const uint16_t b = to_bf16(a.src[k]);
+#pragma unroll
+        for (int d = 0; d < ND; ++d) a.dsts[d][a.dst_offset + k] = b;
+      });
 }
 
 // Reduce half of the split step: red[os] = (sum_r grads_r[flat]) * scale,
@@ -1297,15 +1451,55 @@ cudaError_t launch_accumulate(const AccumArgs& a, int grid, cudaStream_t stream)
   return cudaGetLastError();
 }
 
+// Persistent grid for the raw kernels: one wave of resident 256-thread CTAs
+// (occupancy of the kernel `fn`), fewer when n is small.
+template <class F>
+int raw_grid(F* fn, unsigned long long n) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const unsigned long long per_cta = 256ull * 8 * kRawU;
+  const unsigned long long need = (n + per_cta - 1) / per_cta;
+  return static_cast<int>(
+      std::max(1ull, std::min<unsigned long long>(need, 1ull * sm_count() * per_sm)));
+}
+
+template <bool B, int U, int MINB>
+void adamw_flat_launch(const void* grad, float* master, float* m, float* v,
+                       uint16_t* param_out, unsigned long long n, const AdamScalars& s,
+                       cudaStream_t stream) {
+  adamw_flat_kernel<B, U, MINB><<<raw_grid(adamw_flat_kernel<B, U, MINB>, n), 256, 0, stream>>>(
+      grad, master, m, v, param_out, n, s);
+}
+
+// Default: 4 groups (32 elements) per thread at 1 CTA/SM, 94% of measured
+// HBM on 2^28 elements vs 81% for 2 groups at 2 CTAs/SM and 1 group at 4
+// (profiles/r02_bench_raw_adamw_variants.jsonl). Tuning hook
+// (tools/bench_raw.py): AMSP_RAW_ADAMW = 1 -> <2 groups, 2 CTAs/SM>,
+// 2 -> <1 group, 4 CTAs/SM>.
+int raw_adamw_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("AMSP_RAW_ADAMW");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 cudaError_t launch_adamw_flat(const void* grad, bool bf16_grad, float* master, float* m,
                               float* v, uint16_t* param_out, unsigned long long n,
                               const AdamScalars& s, cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
-  const int grid = sm_count() * 8;
-  if (bf16_grad)
-    adamw_flat_kernel<true><<<grid, 256, 0, stream>>>(grad, master, m, v, param_out, n, s);
-  else
-    adamw_flat_kernel<false><<<grid, 256, 0, stream>>>(grad, master, m, v, param_out, n, s);
+  const int var = raw_adamw_variant();
+  if (bf16_grad) {
+    if (var == 1) adamw_flat_launch<true, 2, 2>(grad, master, m, v, param_out, n, s, stream);
+    else if (var == 2) adamw_flat_launch<true, 1, 4>(grad, master, m, v, param_out, n, s, stream);
+    else adamw_flat_launch<true, 4, 1>(grad, master, m, v, param_out, n, s, stream);
+  } else {
+    if (var == 1) adamw_flat_launch<false, 2, 2>(grad, master, m, v, param_out, n, s, stream);
+    else if (var == 2) adamw_flat_launch<false, 1, 4>(grad, master, m, v, param_out, n, s, stream);
+    else adamw_flat_launch<false, 4, 1>(grad, master, m, v, param_out, n, s, stream);
+  }
   return cudaGetLastError();
 }
 
@@ -1321,7 +1515,17 @@ cudaError_t launch_rs_upcast_scale(const uint16_t* const* srcs, int nsrc,
   a.n = n;
   a.dst = dst;
   a.scale = scale;
-  rs_upcast_scale_kernel<<<sm_count() * 8, 256, 0, stream>>>(a);
+  const int grid = raw_grid(rs_upcast_scale_kernel<8>, n);
+  switch (nsrc) {
+    case 1: rs_upcast_scale_kernel<1><<<grid, 256, 0, stream>>>(a); break;
+    case 2: rs_upcast_scale_kernel<2><<<grid, 256, 0, stream>>>(a); break;
+    case 3: rs_upcast_scale_kernel<3><<<grid, 256, 0, stream>>>(a); break;
+    case 4: rs_upcast_scale_kernel<4><<<grid, 256, 0, stream>>>(a); break;
+    case 5: rs_upcast_scale_kernel<5><<<grid, 256, 0, stream>>>(a); break;
+    case 6: rs_upcast_scale_kernel<6><<<grid, 256, 0, stream>>>(a); break;
+    case 7: rs_upcast_scale_kernel<7><<<grid, 256, 0, stream>>>(a); break;
+    default: rs_upcast_scale_kernel<8><<<grid, 256, 0, stream>>>(a); break;
+  }
   return cudaGetLastError();
 }
 
@@ -1335,15 +1539,23 @@ cudaError_t launch_ag_downcast(const float* src, unsigned long long n, uint16_t*
   a.dst_offset = dst_offset;
   a.n = n;
   a.src = src;
-  ag_downcast_kernel<<<sm_count() * 8, 256, 0, stream>>>(a);
+  const int grid = raw_grid(ag_downcast_kernel<8>, n);
+  switch (ndst) {
+    case 1: ag_downcast_kernel<1><<<grid, 256, 0, stream>>>(a); break;
+    case 2: ag_downcast_kernel<2><<<grid, 256, 0, stream>>>(a); break;
+    case 3: ag_downcast_kernel<3><<<grid, 256, 0, stream>>>(a); break;
+    case 4: ag_downcast_kernel<4><<<grid, 256, 0, stream>>>(a); break;
+    case 5: ag_downcast_kernel<5><<<grid, 256, 0, stream>>>(a); break;
+    case 6: ag_downcast_kernel<6><<<grid, 256, 0, stream>>>(a); break;
+    case 7: ag_downcast_kernel<7><<<grid, 256, 0, stream>>>(a); break;
+    default: ag_downcast_kernel<8><<<grid, 256, 0, stream>>>(a); break;
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_upcast_scale(const uint16_t* src, float* dst, unsigned long long n,
                                 float scale, cudaStream_t stream) {
-  if (n == 0) return cudaSuccess;
-  upcast_scale_kernel<<<sm_count() * 8, 256, 0, stream>>>(src, dst, n, scale);
-  return cudaGetLastError();
+  return launch_rs_upcast_scale(&src, 1, 0, dst, n, scale, stream);
 }
 
 }  // namespace amsp

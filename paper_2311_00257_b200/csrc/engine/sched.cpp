@@ -47,7 +47,10 @@
 //   push — the optimizer kernels store the bf16 shard into every OS-group
 //       member directly (NVLink stores inside the update); BroadcastShard is
 //       a marker.
+#include <cmath>
+
 #include "blas.h"
+#include "compute.h"
 #include "engine_impl.h"
 #include "../convert.h"
 
@@ -64,8 +67,14 @@ struct BcCopy {
 };
 
 // Real-compute mode: a compute event of a linear module (or the LM head) is
-// a cuBLAS bf16 GEMM of its true shape over T tokens.
-enum class Gemm { None, Fwd, DGrad, WGrad };
+// a cuBLAS bf16 GEMM of its true shape over T tokens; a norm module's events
+// are RMSNorm kernels (forward, input grad, weight grad into the gradient
+// buffer). The attention core (QK^T, causal softmax, PV and their
+// backward: 12*B*S^2*H FLOPs per layer, the reference's flops_coeff_attn,
+// overlap_sim.cpp:97-110) runs inside the o-projection's forward (before
+// its GEMM) and grad-input (after its GEMM) events, where the data flow of
+// a LLaMA layer puts it.
+enum class Gemm { None, Fwd, DGrad, WGrad, NormFwd, NormDGrad, NormWGrad };
 
 struct EventWork {
   Work kind = Work::Marker;
@@ -73,6 +82,7 @@ struct EventWork {
   int tensor = -1;
   Gemm gemm = Gemm::None;
   int g_in = 0, g_out = 0;
+  bool attention = false;  // attention core before (Fwd) / after (DGrad) the GEMM
   int barrier = -1;
   int seg_begin = 0, nseg = 0, ntiles = 0;
   unsigned long long ns = 0;
@@ -238,6 +248,48 @@ struct amsp_sched {
   uint16_t* ring = nullptr;
   uint16_t* head_w = nullptr;
   std::uint64_t ring_slot = 0;
+  // attention core: seq_len S, heads x head_dim, sequences per micro-batch;
+  // probabilities P and their gradient dS, [heads, S, S] bf16 each
+  int attn_s = 0, attn_heads = 0, attn_dim = 0, attn_seqs = 0, hidden = 0;
+  uint16_t* probs = nullptr;
+  uint16_t* dprobs = nullptr;
+  float* norm_acc = nullptr;  // fp32 [H] scratch of the norm weight gradients
+
+  void attention_fwd(cudaStream_t st) {
+    amsp::Blas& blas = amsp::Blas::instance();
+    const int S = attn_s, d = attn_dim, nh = attn_heads, H = hidden;
+    const long long SS = static_cast<long long>(S) * S;
+    const float scale = 1.0f / std::sqrt(static_cast<float>(d));
+    for (int b = 0; b < attn_seqs; ++b) {
+      const long long o = static_cast<long long>(b) * S * H;
+      // scores_h = Q_h K_h^T  (Q = K = V = the activation buffer's head slices)
+      blas.bgemm(st, false, true, S, S, d, act + o, H, d, act + o, H, d, probs, S, SS, nh);
+      ck(amsp::launch_softmax_rows(probs, static_cast<long long>(nh) * S, S, S, scale, st),
+         "attention softmax");
+      // O_h = P_h V_h
+      blas.bgemm(st, false, false, S, d, S, probs, S, SS, act + o, H, d, yout + o, H, d, nh);
+      e->launches += 3;
+    }
+  }
+
+  void attention_bwd(cudaStream_t st) {
+    amsp::Blas& blas = amsp::Blas::instance();
+    const int S = attn_s, d = attn_dim, nh = attn_heads, H = hidden;
+    const long long SS = static_cast<long long>(S) * S;
+    const float scale = 1.0f / std::sqrt(static_cast<float>(d));
+    for (int b = 0; b < attn_seqs; ++b) {
+      const long long o = static_cast<long long>(b) * S * H;
+      // dP_h = dO_h V_h^T ; dS = softmax backward ; dV = P^T dO ; dQ = dS K ; dK = dS^T Q
+      blas.bgemm(st, false, true, S, S, d, dout + o, H, d, act + o, H, d, dprobs, S, SS, nh);
+      ck(amsp::launch_softmax_bwd_rows(probs, dprobs, static_cast<long long>(nh) * S, S, scale,
+                                       st),
+         "attention softmax backward");
+      blas.bgemm(st, true, false, S, d, S, probs, S, SS, dout + o, H, d, yout + o, H, d, nh);
+      blas.bgemm(st, false, false, S, d, S, dprobs, S, SS, act + o, H, d, yout + o, H, d, nh);
+      blas.bgemm(st, true, false, S, d, S, dprobs, S, SS, act + o, H, d, yout + o, H, d, nh);
+      e->launches += 5;
+    }
+  }
 
   uint16_t* gather_dst(int t) const {
     if (!gemm_mode) return e->slots[t & 1];
@@ -263,10 +315,26 @@ struct amsp_sched {
     const uint16_t* wt = weight_of(t);
     switch (w.gemm) {
       case Gemm::Fwd:
+        if (w.attention) attention_fwd(st);
         blas.linear_fwd(st, act, wt, yout, tokens, w.g_in, w.g_out);
         break;
       case Gemm::DGrad:
         blas.linear_dgrad(st, dout, wt, yout, tokens, w.g_in, w.g_out);
+        if (w.attention) attention_bwd(st);
+        break;
+      case Gemm::NormFwd:
+        ck(amsp::launch_rmsnorm_fwd(act, wt, yout, tokens, hidden, st), "rmsnorm");
+        break;
+      case Gemm::NormDGrad:
+        ck(amsp::launch_rmsnorm_dgrad(act, wt, dout, yout, tokens, hidden, st), "rmsnorm dgrad");
+        break;
+      case Gemm::NormWGrad:
+        ck(amsp::launch_rmsnorm_wgrad(act, dout, norm_acc,
+                                      e->grads_of(e->rank) +
+                                          e->pmap.tensor_offset[static_cast<std::size_t>(t)],
+                                      tokens, hidden, w.accum_in_place, st),
+           "rmsnorm wgrad");
+        ++e->launches;
         break;
       case Gemm::WGrad: {
         const std::size_t ti = t < 0 ? e->tensor_sizes.size() - 1 : static_cast<std::size_t>(t);
@@ -354,7 +422,9 @@ struct amsp_sched {
     cudaFree(stage);
     cudaFree(red);
     for (void* p : {static_cast<void*>(act), static_cast<void*>(dout), static_cast<void*>(yout),
-                    static_cast<void*>(ring), static_cast<void*>(head_w)})
+                    static_cast<void*>(ring), static_cast<void*>(head_w),
+                    static_cast<void*>(probs), static_cast<void*>(dprobs),
+                    static_cast<void*>(norm_acc)})
       cudaFree(p);
     cudaGetLastError();  // teardown must not leave a sticky error for the next call
   }
@@ -364,7 +434,7 @@ struct amsp_sched {
   }
 
   void barrier(int id, cudaStream_t s) {
-    if (e->world == 1 || e->local_linked) return;
+    if (!e->synced()) return;
     ck(amsp::launch_barrier(e->d_peer_flags, e->world, e->rank, id, epoch, e->err, s),
        "sched barrier");
     ++e->launches;
@@ -399,7 +469,7 @@ struct amsp_sched {
     a.exp_avg = e->exp_avg;
     a.exp_avg_sq = e->exp_avg_sq;
     a.s = scalars;
-    a.fence_peers = (e->world > 1 && !e->local_linked) ? 1 : 0;
+    a.fence_peers = e->synced() ? 1 : 0;
     ck(amsp::launch_adam_push(a, grid, s), "adam push");
     ++e->launches;
   }
@@ -420,7 +490,7 @@ struct amsp_sched {
     a.exp_avg_sq = e->exp_avg_sq;
     a.s = scalars;
     a.stats = nullptr;
-    a.fence_peers = (e->world > 1 && !e->local_linked) ? 1 : 0;
+    a.fence_peers = e->synced() ? 1 : 0;
     if (e->staged) e->set_acc(a.acc, &a.nacc, &a.acc_by_dst);
     ck(amsp::launch_fused_step(a, e->world, std::max(1, std::min(t.ntiles, grid)), variant, s),
        "sched fused");
@@ -917,7 +987,7 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
         const int t = ev.layer < 0 ? -1 : tensor_of(ev.layer, ev.module);
         const std::uint64_t size = e->tensor_sizes[t < 0 ? n - 1 : static_cast<std::size_t>(t)];
         const std::uint64_t H = static_cast<std::uint64_t>(model.hidden);
-        if (size > H && size % H == 0) {  // linear module (norms stay timed stand-ins)
+        if (size > H && size % H == 0) {  // linear module
           w.tensor = t;
           w.g_in = model.hidden;
           w.g_out = static_cast<int>(size / H);
@@ -925,6 +995,14 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
                    : ev.kind == shardplan::EventKind::BwdGradWeight ? Gemm::WGrad
                                                                     : Gemm::Fwd;
           max_out = std::max<std::uint64_t>(max_out, size / H);
+          // LLaMA layer template (q,k,v,o,gate,up,down,attn_norm,mlp_norm):
+          // the attention core sits between v and o
+          w.attention = K == 9 && ev.module == 3 && w.gemm != Gemm::WGrad;
+        } else if (size == H && H % 8 == 0 && t >= 0) {  // RMSNorm module
+          w.tensor = t;
+          w.gemm = ev.kind == shardplan::EventKind::BwdGradInput    ? Gemm::NormDGrad
+                   : ev.kind == shardplan::EventKind::BwdGradWeight ? Gemm::NormWGrad
+                                                                    : Gemm::NormFwd;
         }
         break;
       }
@@ -1139,6 +1217,25 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
       ck(cudaMalloc(p, std::max<std::uint64_t>(elems, 8) * 2), what);
     };
     alloc(&s->act, T * H, "cudaMalloc activations");
+    s->hidden = model.hidden;
+    ck(cudaMalloc(&s->norm_acc, H * 4), "cudaMalloc norm scratch");
+    ck(cudaMemset(s->norm_acc, 0, H * 4), "zero norm scratch");
+    // Attention core: head_dim 128 (64 when H is not a multiple of 128),
+    // T / S whole sequences per micro-batch.
+    const int S = model.seq_len;
+    const int d = model.hidden % 128 == 0 ? 128 : model.hidden % 64 == 0 ? 64 : 0;
+    if (K == 9 && d > 0 && S > 0 && S % 8 == 0 && s->tokens % S == 0) {
+      s->attn_s = S;
+      s->attn_dim = d;
+      s->attn_heads = model.hidden / d;
+      s->attn_seqs = s->tokens / S;
+      const std::uint64_t pe = static_cast<std::uint64_t>(s->attn_heads) * S * S;
+      alloc(&s->probs, pe, "cudaMalloc attention probabilities");
+      alloc(&s->dprobs, pe, "cudaMalloc attention probability grads");
+      ck(amsp::launch_synth_grad(s->probs, 0, pe, 0x5EED, 4, 0, nullptr), "fill probs");
+    } else {
+      for (auto& w : s->work) w.attention = false;
+    }
     alloc(&s->dout, T * wide, "cudaMalloc output grads");
     alloc(&s->yout, T * wide, "cudaMalloc outputs");
     // Small, finite synthetic activations (counter-based, like the grads).

@@ -326,12 +326,15 @@ def exchange_handles(handle: bytes, world: int, group=None) -> list:
     return handles
 
 
-def link_local(engines: Sequence[Engine]) -> None:
+def link_local(engines: Sequence[Engine], sync: bool = False) -> None:
     """Emulate one DP group on a single GPU (tests/smoke): engines must be
-    ranks 0..n-1 created on the same device; steps then run one after
-    another on one stream without cross-GPU barriers."""
+    ranks 0..n-1 created on the same device. sync=False: steps run one after
+    another on one stream without cross-GPU barriers. sync=True: every
+    engine keeps its own stream and the real barrier kernels / release
+    fences order the ranks, as across GPUs (amsp_engine_link_local_sync)."""
     arr = (C.c_void_p * len(engines))(*[e._h.value for e in engines])
-    N.check(N.lib().amsp_engine_link_local(arr, len(engines)))
+    fn = N.lib().amsp_engine_link_local_sync if sync else N.lib().amsp_engine_link_local
+    N.check(fn(arr, len(engines)))
     for e in engines:
         e._linked = engines  # keep peers alive while linked
 

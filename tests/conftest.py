@@ -6,6 +6,17 @@ import pytest
 
 REPO = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(REPO))
+# Emulated groups with real barriers put every rank's streams (own + the
+# scheduler's two comm streams) in one CUDA context; with the default 8
+# hardware work queues, streams alias and a spinning barrier kernel could
+# stall an unrelated stream behind it. Must be set before CUDA initialises.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# ... and with lazy module loading, the first launch of a kernel may need a
+# context synchronisation, which waits for a rank's barrier kernel spinning
+# on a peer whose work the (blocked) host thread has not issued yet: load
+# every kernel up front instead (CUDA lazy-loading guidance for kernels that
+# wait on each other).
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 
 def pytest_configure(config):

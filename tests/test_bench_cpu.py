@@ -25,6 +25,13 @@ def _check(line, world):
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert line["config"]["model"] == "llama-7b" and line["config"]["parallelism"] == f"dp{world}"
+    # the step is measured on the bounded sample, so steps x ms_per_step is real time
+    assert line["ms_per_step"] < line["ms_per_step_full_workload_extrapolated"]
+    planner = line["planner"]
+    if isinstance(planner, list):  # oracle/_ref built (the reference is mounted here)
+        entries = {p["entry"] for p in planner}
+        assert entries == {"solve", "build_schedule+simulate_step"}
+        assert all(p["best_us"] > 0 for p in planner)
 
 
 def test_reference_arm_single_process():

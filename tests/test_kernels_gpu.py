@@ -42,9 +42,13 @@ def test_synth_grad_matches_oracle(cuda):
     assert np.array_equal(_host(out, np.uint16), O.grads(start, n, DEFAULT_SEED, 3, 1))
 
 
-def test_upcast_and_rs_upcast_scale(cuda):
+# off = 0 / 8: 16-byte aligned buffers (128-bit vector path + ragged tail);
+# off = 17: misaligned (element path). Both must give identical bits.
+@pytest.mark.parametrize("off", [0, 8, 17])
+@pytest.mark.parametrize("W", [1, 2, 3, 5, 8])
+def test_upcast_and_rs_upcast_scale(cuda, off, W):
     import torch
-    n, off, W = 70_001, 17, 3
+    n = 70_001
     srcs = [O.grads(0, n + off, DEFAULT_SEED, 1, r) for r in range(W)]
     dev = [_dev(s.view(np.int16)) for s in srcs]
     scale = np.float32(1.0 / W)
@@ -66,26 +70,41 @@ def test_upcast_and_rs_upcast_scale(cuda):
         N.check(N.lib().amsp_k_rs_upcast_scale(ptrs, 9, 0, out.data_ptr(), n, 1.0, None))
 
 
-def test_ag_downcast_into_every_destination(cuda):
+@pytest.mark.parametrize("off", [0, 8, 3])
+@pytest.mark.parametrize("nd", [1, 3, 8])
+def test_ag_downcast_into_every_destination(cuda, off, nd):
     import torch
-    n, off = 50_000, 8
+    n = 50_005
     rng = np.random.default_rng(7)
     src = rng.standard_normal(n).astype(np.float32)
-    dsts = [torch.zeros(n + off, dtype=torch.int16, device="cuda") for _ in range(3)]
-    ptrs = (C.c_void_p * 3)(*[d.data_ptr() for d in dsts])
-    N.check(N.lib().amsp_k_ag_downcast(_dev(src).data_ptr(), n, ptrs, 3, off, None))
+    dsts = [torch.zeros(n + off, dtype=torch.int16, device="cuda") for _ in range(nd)]
+    ptrs = (C.c_void_p * nd)(*[d.data_ptr() for d in dsts])
+    N.check(N.lib().amsp_k_ag_downcast(_dev(src).data_ptr(), n, ptrs, nd, off, None))
     want = _f32_to_bf16(src)
     for d in dsts:
         got = _host(d, np.uint16)
         assert np.array_equal(got[off:], want) and not got[:off].any()
 
 
-@pytest.mark.parametrize("bf16_grad", [True, False])
-def test_adamw_flat_matches_oracle_step(cuda, bf16_grad):
-    """amsp_k_adamw over a contiguous shard == the oracle's AMSP step with one
-    rank (grad scale 1), three steps."""
+def test_raw_kernels_empty_is_noop(cuda):
     import torch
-    n = 33_333
+    out = torch.full((4,), 7.0, device="cuda")
+    src = torch.zeros(4, dtype=torch.int16, device="cuda")
+    ptrs = (C.c_void_p * 1)(src.data_ptr())
+    N.check(N.lib().amsp_k_upcast_scale(src.data_ptr(), out.data_ptr(), 0, 1.0, None))
+    N.check(N.lib().amsp_k_rs_upcast_scale(ptrs, 1, 0, out.data_ptr(), 0, 1.0, None))
+    N.check(N.lib().amsp_k_ag_downcast(out.data_ptr(), 0, ptrs, 1, 0, None))
+    torch.cuda.synchronize()
+    assert out.eq(7.0).all() and not src.any()
+
+
+@pytest.mark.parametrize("bf16_grad", [True, False])
+@pytest.mark.parametrize("n", [33_333, 7, 4096 * 37])
+def test_adamw_flat_matches_oracle_step(cuda, bf16_grad, n):
+    """amsp_k_adamw over a contiguous shard == the oracle's AMSP step with one
+    rank (grad scale 1), three steps (vector path + ragged tail, tail only,
+    several grid strides)."""
+    import torch
     h = O.hyper()
     master = np.array([O.master_init(DEFAULT_SEED, i) for i in range(n)], np.float32)
     m = np.zeros(n, np.float32)

@@ -1,0 +1,240 @@
+"""Cross-rank synchronisation of the AMSP step on ONE GPU, with the real
+barrier protocol (amsp_engine_link_local_sync).
+
+The emulated groups of tests/test_engine_gpu.py order the ranks by running
+them one after another on one stream, with the barriers compiled out. Here
+every rank issues on its own CUDA stream, calls are interleaved rank by
+rank, and ranks > 0 are delayed by a spin kernel before they produce their
+gradients. Correct results therefore REQUIRE what the multi-GPU path relies
+on: barrier_kernel's st.release.sys / ld.acquire.sys flag protocol (engine
+and scheduler barrier ids, epochs growing across schedulers), the
+__threadfence_system release of parameter stores into peers, and the
+micro-batch accumulation's release barriers. A negative control shows the
+same interleaving without barriers reads stale gradients.
+
+All ranks live in one process and one CUDA context (no time-sliced
+processes waiting on each other, B200_PROFILING.md); barrier waits are
+bounded (20 s -> error flag, never a hang)."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import cpu as O
+from paper_2311_00257_b200 import _native as N
+from paper_2311_00257_b200 import shardplan as S
+from paper_2311_00257_b200.engine import DEFAULT_SEED, Engine, link_local
+
+pytestmark = pytest.mark.gpu
+if os.environ.get("CUDA_MODULE_LOADING") != "EAGER":  # tests/conftest.py sets it
+    pytestmark = [pytest.mark.gpu,
+                  pytest.mark.skip(reason="needs CUDA_MODULE_LOADING=EAGER (lazy loading can "
+                                          "deadlock kernels that wait on each other)")]
+M = S.DeviceMesh
+H = O.hyper()
+DELAY_NS = 3_000_000  # 3 ms: far longer than any tiny-model kernel
+
+
+def _check_rank(e, want, what="rank"):
+    segs, owned = e.segments()
+    got = {n: e.read(n) for n in ("master", "exp_avg", "exp_avg_sq")}
+    for n, ref in zip(("master", "exp_avg", "exp_avg_sq"), want[:3]):
+        for f, o, ln in segs:
+            assert np.array_equal(got[n][o:o + ln].view(np.uint32),
+                                  ref[f:f + ln].view(np.uint32)), (what, n, f)
+    if e.plan.sp() == 1:
+        assert np.array_equal(e.read("params"), want[3]), (what, "params")
+
+
+def _delay(stream, ns=DELAY_NS):
+    N.check(N.lib().amsp_k_spin(4, ns, stream.cuda_stream))
+
+
+def _streams(cuda, n):
+    return [cuda.cuda.Stream() for _ in range(n)]
+
+
+@pytest.mark.parametrize("world,os_k,variant", [
+    (2, 2, 0), (4, 4, 0), (4, 2, 0), (8, 8, 0), (3, 3, 0),
+    (2, 2, 11), (4, 4, 10), (8, 8, 6), (4, 4, 1), (2, 2, 2)])
+def test_synced_group_interleaved_ranks(cuda, world, os_k, variant):
+    """Rank by rank: (delay) synth grads -> step. Rank 0's step runs before
+    rank 1 has even produced its gradients unless the pre-step barrier holds
+    it; the post-step barrier keeps rank r from overwriting its gradients
+    (next step's synth) while a peer still pulls them."""
+    model = S.model("tiny")
+    plan = S.ShardingPlan(M(1, 1), M(1, 1), M(os_k, 1))
+    engines = [Engine(model, plan, M(world, 1), rank=r) for r in range(world)]
+    link_local(engines, sync=True)
+    streams = _streams(cuda, world)
+    for e, s in zip(engines, streams):
+        if variant:
+            e.tune(variant)
+        e.init_state(s)
+    steps = 3
+    for t in range(1, steps + 1):
+        for r, (e, s) in enumerate(zip(engines, streams)):
+            if r > 0:
+                _delay(s)
+            e.synth_grads(t, s)
+            e.step(t, s)
+    want = O.trajectory_range(0, engines[0].info.total_params, DEFAULT_SEED, steps, world, H)
+    for e in engines:
+        e.stats()  # raises if a barrier timed out
+        _check_rank(e, want, f"rank {e.rank}")
+    for e in engines:
+        e.close()
+
+
+def test_unsynced_interleaving_reads_stale_gradients(cuda):
+    """Negative control: the same interleaving on per-rank streams with the
+    barriers compiled out (link_local without sync) does NOT reproduce the
+    oracle -- so the synced test above is discriminating."""
+    model = S.model("tiny")
+    plan = S.ShardingPlan(M(1, 1), M(1, 1), M(2, 1))
+    engines = [Engine(model, plan, M(2, 1), rank=r) for r in range(2)]
+    link_local(engines, sync=False)
+    streams = _streams(cuda, 2)
+    for e, s in zip(engines, streams):
+        e.init_state(s)
+    cuda.cuda.synchronize()
+    for r, (e, s) in enumerate(zip(engines, streams)):
+        if r > 0:
+            _delay(s, 20_000_000)
+        e.synth_grads(1, s)
+        e.step(1, s)
+    want = O.trajectory_range(0, engines[0].info.total_params, DEFAULT_SEED, 1, 2, H)
+    with pytest.raises(AssertionError):
+        _check_rank(engines[0], want)
+    for e in engines:
+        e.close()
+
+
+@pytest.mark.parametrize("world,dp,p,g,os_,mb", [
+    (2, (2, 1), (1, 1), (2, 1), (2, 1), 3),   # ZeRO-2 (g = os)
+    (4, (4, 1), (4, 1), (4, 1), (4, 1), 2),   # ZeRO-3 (s_g = s_p)
+    (4, (4, 1), (2, 1), (2, 1), (4, 1), 2),   # s_g = s_p = 2 < s_os
+    (4, (2, 2), (1, 1), (2, 1), (2, 1), 2),   # G shard inside each virtual node
+    (8, (2, 4), (1, 1), (2, 4), (2, 4), 2),   # BASELINE partial: G shard mesh 2x4
+    (4, (4, 1), (1, 1), (1, 1), (4, 1), 3)])  # ZeRO-1, in place
+def test_synced_micro_batches_gradient_sharding(cuda, world, dp, p, g, os_, mb):
+    """M micro-batches, rank-interleaved: every micro-batch's accumulate pulls
+    the G block of each peer only after the peer's gradients are complete
+    (barrier), and no rank rewrites its gradient buffer (next micro-batch)
+    before every holder has pulled it (release barrier)."""
+    model = S.model("tiny")
+    plan = S.ShardingPlan(M(*p), M(*g), M(*os_))
+    engines = [Engine(model, plan, M(*dp), rank=r, micro_batches=mb) for r in range(world)]
+    link_local(engines, sync=True)
+    streams = _streams(cuda, world)
+    for e, s in zip(engines, streams):
+        e.init_state(s)
+    steps = 2
+    for t in range(1, steps + 1):
+        for k in range(mb):
+            for r, (e, s) in enumerate(zip(engines, streams)):
+                if r > 0:
+                    _delay(s, 1_000_000)
+                e.synth_grads(t, s, mb=k)
+                if k + 1 < mb:
+                    e.accumulate(t, k, s)
+                else:
+                    e.step(t, s)
+    acc = O.accum(mb, plan.sg(), O.mesh_blocks(dp, g, world))
+    want = O.trajectory_range(0, engines[0].info.total_params, DEFAULT_SEED, steps, world, H,
+                              acc)
+    for e in engines:
+        e.stats()
+        _check_rank(e, want, f"rank {e.rank}")
+    for e in engines:
+        e.close()
+
+
+@pytest.mark.parametrize("world,p,os_k,mb,compute", [
+    (2, 1, 2, 1, "standin"), (4, 1, 4, 1, "standin"), (4, 4, 4, 1, "standin"),
+    (4, 2, 4, 2, "standin"), (2, 1, 2, 2, "standin")])
+def test_synced_scheduler_two_schedulers_no_host_sync(cuda, world, p, os_k, mb, compute):
+    """two schedulers on the same engines, alternating steps,
+    gradients written by the grad-weight events DURING the step
+    (grad_source='synth'), no host synchronisation between steps, ranks on
+    their own streams. The barrier epochs must keep growing across
+    schedulers, the per-bucket / per-module barriers must hold the reduces
+    until every rank's gradients exist, and the end-of-step barriers must
+    hold the next step's gradient writes until the owners are done."""
+    from paper_2311_00257_b200.engine import Scheduler, b200_profile
+    model = S.model("tiny", micro_batch_count=mb)
+    g = M(p, 1) if os_k == p else M(os_k, 1)
+    plan = S.ShardingPlan(M(p, 1), g, M(os_k, 1))
+    engines = [Engine(model, plan, M(world, 1), rank=r, micro_batches=mb, skip_gathers=True)
+               for r in range(world)]
+    link_local(engines, sync=True)
+    streams = _streams(cuda, world)
+    prof = b200_profile()
+    cost = S.CostConfig(bucket_size=1 << 20)
+    sim = S.SimConfig(overlap_tier="ag_rs_ar_bc", peak_flops_per_gpu=1e18)
+    scheds = [[Scheduler(e, model, prof, cost, sim, compute=compute, grad_source="synth")
+               for e in engines] for k in range(2)]
+    for e, s in zip(engines, streams):
+        e.init_state(s)
+    steps = 4
+    for t in range(1, steps + 1):
+        for r, s in enumerate(streams):
+            if r > 0:
+                _delay(s, 1_000_000)
+            scheds[t % 2][r].step(t, s)
+    for r, s in enumerate(streams):  # mirrored broadcast: the last step's shards
+        scheds[steps % 2][r].flush(s)
+    acc = O.accum(mb, plan.sg(), O.mesh_blocks((world, 1), (g.per_node, g.nodes), world))
+    want = O.trajectory_range(0, engines[0].info.total_params, DEFAULT_SEED, steps, world, H,
+                              acc)
+    for e in engines:
+        e.stats()
+        _check_rank(e, want, f"rank {e.rank}")
+    for k in range(2):
+        for sc in scheds[k]:
+            sc.close()
+    for e in engines:
+        e.close()
+
+
+@pytest.mark.parametrize("world,p", [(2, 1), (2, 2)])
+def test_synced_scheduler_real_gemm(cuda, world, p):
+    """compute='gemm' on per-rank streams with real barriers: cuBLAS wgrad
+    writes the gradient buffers while peers reduce finished buckets; the
+    replicated parameters must come out identical on every rank."""
+    from paper_2311_00257_b200.engine import Scheduler, b200_profile
+    model = S.model("tiny", seq_len=256)
+    plan = S.ShardingPlan(M(p, 1), M(p, 1), M(world, 1))
+    engines = [Engine(model, plan, M(world, 1), rank=r) for r in range(world)]
+    link_local(engines, sync=True)
+    streams = _streams(cuda, world)
+    scheds = [Scheduler(e, model, b200_profile(), S.CostConfig(bucket_size=1 << 20),
+                        S.SimConfig(peak_flops_per_gpu=1e15), compute="gemm")
+              for e in engines]
+    for e, s in zip(engines, streams):
+        e.init_state(s)
+    # compute-only warm-up per rank (no barriers): cuBLAS binds its per-stream
+    # handles and workspaces before any rank spins on a peer
+    for sc, s in zip(scheds, streams):
+        sc.step(1, s, with_comm=False)
+    cuda.cuda.synchronize()
+    for t in (1, 2, 3):
+        for r, (sc, s) in enumerate(zip(scheds, streams)):
+            if r > 0:
+                _delay(s, 1_000_000)
+            sc.step(t, s)
+    for sc, s in zip(scheds, streams):
+        sc.flush(s)
+    params = [e.read("params") for e in engines]
+    for e in engines:
+        e.stats()
+    for prm in params:
+        f = (prm.astype(np.uint32) << 16).view(np.float32)
+        assert np.all(np.isfinite(f))
+    if p == 1:
+        for prm in params[1:]:
+            assert np.array_equal(prm, params[0])
+    for sc in scheds:
+        sc.close()
+    for e in engines:
+        e.close()

@@ -1,0 +1,21 @@
+# ncu --set full captures of every default kernel at HEAD (one GPU; W > 1
+# groups emulated in one process by tools/ncu_targets.py), plus the raw C-ABI
+# kernels. Each capture follows a plain run of the same command.
+set -x
+mkdir -p gpurun_out/ncu
+NCU="ncu --set full --clock-control none --import-source on"
+run() {  # name, regex, skip, command...
+  local name=$1 re=$2 skip=$3; shift 3
+  timeout 600 "$@" > gpurun_out/ncu/$name.plain.log 2>&1 &&
+  timeout 900 $NCU -k regex:$re -s $skip -c 1 -o gpurun_out/ncu/$name "$@" > gpurun_out/ncu/$name.ncu.log 2>&1
+  echo "$name rc=$?"
+}
+run fused_w1_7b fused_step 0 python tools/ncu_targets.py fused --world 1 --model llama-7b --steps 2
+run fused_w2_1b fused_step 0 python tools/ncu_targets.py fused --world 2 --steps 2
+run fused_w4_1b fused_step 0 python tools/ncu_targets.py fused --world 4 --steps 2
+run fused_w8_1b fused_step 0 python tools/ncu_targets.py fused --world 8 --steps 2
+run gather_tma_w4_1b gather_tma 8 python tools/ncu_targets.py gather --world 4 --steps 2
+run raw_adamw adamw_flat 1 python tools/bench_raw.py --only adamw_flat_kernel\<bf16 --iters 1 --warmup 1
+run raw_rs4 rs_upcast 1 python tools/bench_raw.py --only rs_upcast_scale_kernel\<4 --iters 1 --warmup 1
+run raw_ag4 ag_downcast 1 python tools/bench_raw.py --only ag_downcast_kernel\<4 --iters 1 --warmup 1
+ls -la gpurun_out/ncu
