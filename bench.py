@@ -87,6 +87,9 @@ def parse():
                          "auto = the engine's default (TMA when the P slices are aligned)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--grad-ring", action=argparse.BooleanOptionalAction, default=True,
+                    help="s_g > 1: also time the overlapped step on a gradient-ring engine "
+                         "(gradient memory = G shard + ring)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -644,7 +647,7 @@ def run_ours(args):
     # 3 streams; measured with real cuBLAS GEMM compute (the realistic case)
     # and with the reference's timed stand-ins (6*Phi*B*S FLOPs at the
     # measured sustained bf16 peak x efficiency).
-    def measure_overlap(compute):
+    def measure_overlap(compute, eng=eng, ring=False):
         nonlocal step
         from paper_2311_00257_b200.engine import Scheduler, b200_profile
         mspec = S.model(args.model, micro_batch=args.micro_batch, seq_len=args.seq_len,
@@ -670,7 +673,8 @@ def run_ours(args):
                           optimizer_overlap=bool(opt), compute=compute,
                           gemm_sm_margin=args.gemm_sm_margin, gather=args.gather, bc=args.bc,
                           reduce=reduce,
-                          grad_source="synth" if (MB > 1 and compute == "standin") else "caller")
+                          grad_source=("synth" if ((MB > 1 or ring) and compute == "standin")
+                                       else "caller"))
 
         def timed(with_comm, k):
             nonlocal step
@@ -794,8 +798,56 @@ def run_ours(args):
                         "elements) on a copy stream, each chunk's fused update (W > 1: after a "
                         "cross-GPU barrier) behind it -> D2H stats"
                         if info.sp == 1 else
-                        "amsp_engine_step_host: pinned host bf16 grads -> H2D -> step -> D2H stats")}
+                        "amsp_engine_step_host: pinned host bf16 grads -> H2D -> step -> D2H stats"),
+               "direction": "host gradients in, updated parameters stay on the device (the "
+                            "D2H bytes are the step statistics)"}
         del host
+
+    # Memory: this rank's device allocation against the planner's model-state
+    # bytes (memory_breakdown, cost_model.cpp:140-160).
+    mbd = S.memory_breakdown(S.model(args.model, micro_batch_count=MB), plan)
+    memory = {"device_bytes": info.device_bytes, "grad_buffer_elems": info.grad_elems,
+              "g_shard_accumulator_elems": info.acc_elems,
+              "planner_d_modelstate": mbd.d_modelstate, "planner_d_grads": mbd.d_grads}
+
+    # Gradient ring (s_g > 1): the overlapped step once more on an engine
+    # whose gradient buffer is only the schedule's ring, so per-GPU gradient
+    # memory is the G shard (D_g = 2*Phi/s_g) plus that transient ring.
+    overlap_ring = None
+    if args.overlap and plan.sg() > 1 and args.grad_ring:
+        eng.close()
+        ring = max(info.owned, 1 << 26)
+        for _ in range(2):  # a ring too small for the schedule reports what it needs
+            eng = Engine(model, plan, dp, rank=rank, device=local, layout=args.layout,
+                         micro_batches=MB, skip_gathers=True, grad_ring=ring)
+            eng.connect()
+            try:
+                from paper_2311_00257_b200.engine import Scheduler, b200_profile
+                probe = Scheduler(eng, S.model(args.model, micro_batch=args.micro_batch,
+                                               seq_len=args.seq_len, micro_batch_count=MB),
+                                  b200_profile(), S.CostConfig(),
+                                  S.SimConfig(overlap_tier=args.tier), grad_source="synth")
+                need = probe.info.grad_ring_need
+                probe.close()
+                break
+            except Exception as ex:
+                import re
+                m = re.search(r"it needs (\d+)", str(ex))
+                if not m:
+                    raise
+                ring = int(m.group(1))
+                eng.close()
+        eng.init_state(stream)
+        torch.cuda.synchronize()
+        rinfo = eng._info()
+        modes = ["gemm", "standin"] if args.compute == "both" else [args.compute]
+        res = [measure_overlap(c, eng, ring=True) for c in modes]
+        overlap_ring = dict(res[0], standin=res[1]) if len(res) > 1 else res[0]
+        overlap_ring["memory"] = {"device_bytes": rinfo.device_bytes,
+                                  "grad_ring_elems": rinfo.grad_elems, "ring_need_elems": need,
+                                  "g_shard_accumulator_elems": rinfo.acc_elems,
+                                  "saved_vs_full_gradient_bytes":
+                                      info.device_bytes - rinfo.device_bytes}
 
     cpu = None
     planner = None
@@ -816,7 +868,8 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "fp32 (bf16 grads/params)", "data": "synthetic",
             "config": workload_config(args, S, world, phi),
-            "roofline": roof, "busbw": busbw, "overlap": overlap, "e2e": e2e,
+            "roofline": roof, "busbw": busbw, "overlap": overlap,
+            "overlap_grad_ring": overlap_ring, "memory": memory, "e2e": e2e,
             "cpu_baseline": cpu, "planner": planner,
             "gpu_launches": launches, "clocks": clk,
         }

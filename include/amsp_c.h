@@ -273,6 +273,18 @@ typedef struct {
                                    119-126), the last one through
                                    amsp_engine_step. With s_g = 1 the
                                    gradient buffer accumulates in place. */
+  uint64_t grad_ring_elems;     /* 0: the gradient buffer holds all Phi
+                                   bf16 gradients (the pipeline API:
+                                   synth_grads / accumulate / step /
+                                   step_host). > 0 (needs s_g > 1): a ring of
+                                   this many bf16 elements instead, written
+                                   and consumed only by the overlap
+                                   scheduler, which places every micro-
+                                   batch's tensor gradients in it as backward
+                                   produces them and frees them when every
+                                   rank has reduced them, so gradient memory
+                                   is D_g = 2*Phi/s_g (the accumulator) plus
+                                   this transient ring (cost_model.cpp:151). */
 } amsp_engine_config_t;
 
 typedef struct {
@@ -472,6 +484,8 @@ typedef struct {
   int mirrored_bc;              /* 1: parameters of other OS owners arrive in
                                    the next step's BC events (call
                                    amsp_sched_flush after the last step) */
+  uint64_t grad_ring_need;      /* gradient-ring engines: the smallest ring
+                                   (bf16 elements) this schedule runs in */
 } amsp_sched_info_t;
 
 int amsp_sched_create(amsp_engine_t* e, const amsp_sched_config_t* cfg,

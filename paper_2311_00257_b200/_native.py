@@ -106,7 +106,7 @@ class EngineConfig(C.Structure):
                 ("layout", C.c_int), ("lr", C.c_double), ("beta1", C.c_double),
                 ("beta2", C.c_double), ("eps", C.c_double), ("weight_decay", C.c_double),
                 ("seed", C.c_uint64), ("skip_gathers", C.c_int),
-                ("micro_batches", C.c_int)]
+                ("micro_batches", C.c_int), ("grad_ring_elems", C.c_uint64)]
 
 
 class EngineInfo(C.Structure):
@@ -137,7 +137,8 @@ class SchedInfo(C.Structure):
     _fields_ = [("n_events", C.c_int), ("n_compute", C.c_int), ("n_gather", C.c_int),
                 ("n_reduce", C.c_int), ("n_buckets", C.c_int), ("n_barriers", C.c_int),
                 ("stream_count", C.c_int), ("predicted_step_s", C.c_double),
-                ("predicted_compute_s", C.c_double), ("mirrored_bc", C.c_int)]
+                ("predicted_compute_s", C.c_double), ("mirrored_bc", C.c_int),
+                ("grad_ring_need", C.c_uint64)]
 
 
 P = C.POINTER

@@ -149,6 +149,11 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   if (e->micro > 16) throw Error("engine: at most 16 micro-batches per step");
   e->sg = plan.sg();
   plan_accumulation(e.get(), dp, plan);
+  e->ring = cfg->grad_ring_elems > 0;
+  if (e->ring && e->sg == 1)
+    throw Error("engine: a gradient ring needs s_g > 1 (s_g = 1 keeps the full gradient "
+                "replica, D_g = 2*Phi)");
+  e->grad_elems = e->ring ? (cfg->grad_ring_elems + 63) / 64 * 64 : e->phi;
   std::vector<amsp::CopySeg> copy;
   plan_units(e.get(), copy);
   // In-step all-gathers default to the TMA bulk-copy kernel when every P
@@ -162,12 +167,15 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
 
   // Shared region.
   e->off_grads = 0;
-  e->off_params = align_up(e->phi * 2);
+  e->off_params = align_up(e->grad_elems * 2);
   e->off_flags = e->off_params + align_up(e->param_elems * 2);
   e->off_acc = e->off_flags + align_up(kFlagBytes);  // last: its size may differ per rank
   e->shared_bytes = e->off_acc + align_up(e->acc_elems * 2);
   ck(cudaMalloc(&e->shared, e->shared_bytes), "cudaMalloc shared");
   ck(cudaMemset(e->shared + e->off_flags, 0, kFlagBytes), "zero flags");
+  // a ring's slots are read before the scheduler first writes some of them
+  // (tensors no backward event produces in compute='gemm' mode): keep them finite
+  if (e->ring) ck(cudaMemset(e->shared + e->off_grads, 0, e->grad_elems * 2), "zero ring");
   for (int r = 0; r < e->world; ++r) e->peer_base[r] = e->shared;
 
   // Segment tables: the OS shard, and the whole P shard (for init).
@@ -239,7 +247,7 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
 
 void* buffer_ptr(amsp_engine_t* e, int which, std::size_t* elem, std::uint64_t* count) {
   switch (which) {
-    case 0: *elem = 2; *count = e->phi; return e->grads_of(e->rank);
+    case 0: *elem = 2; *count = e->grad_elems; return e->grads_of(e->rank);
     case 1: *elem = 2; *count = e->param_elems; return e->params_of(e->rank);
     case 2: *elem = 4; *count = e->layout.owned; return e->master;
     case 3: *elem = 4; *count = e->layout.owned; return e->exp_avg;
@@ -314,7 +322,7 @@ int amsp_engine_info(const amsp_engine_t* e, amsp_engine_info_t* info) {
     info->acc_elems = e->acc_elems;
     info->acc_sources = static_cast<int>(e->acc_sources.size());
     info->acc_holders = static_cast<int>(e->acc_holders.size());
-    info->grad_elems = e->phi;
+    info->grad_elems = e->grad_elems;
   });
 }
 
@@ -397,6 +405,7 @@ int amsp_engine_init_state(amsp_engine_t* e, void* stream) {
 int amsp_engine_synth_grads(amsp_engine_t* e, int step, void* stream) {
   return amsp::guarded([&] {
     if (!e) throw Error("engine: null argument");
+    e->require_full_grads("synth_grads");
     e->use_device();
     ck(amsp::launch_synth_grad(e->grads_of(e->rank), 0, e->phi, e->cfg.seed, step,
                                e->rank, e->pick(stream)),
@@ -409,6 +418,7 @@ int amsp_engine_synth_grads_mb(amsp_engine_t* e, int step, int mb, void* stream)
   return amsp::guarded([&] {
     if (!e) throw Error("engine: null argument");
     e->check_micro_batch(mb);
+    e->require_full_grads("synth_grads");
     e->use_device();
     // s_g = 1 accumulates micro-batches in the gradient buffer itself
     const bool in_place = e->sg == 1 && mb > 0;
@@ -423,6 +433,7 @@ int amsp_engine_accumulate(amsp_engine_t* e, int step, int mb, void* stream) {
   return amsp::guarded([&] {
     if (!e) throw Error("engine: null argument");
     if (step < 1) throw Error("engine: step index must be >= 1");
+    e->require_full_grads("accumulate");
     e->use_device();
     e->accumulate(mb, e->pick(stream));
   });
@@ -431,6 +442,7 @@ int amsp_engine_accumulate(amsp_engine_t* e, int step, int mb, void* stream) {
 int amsp_engine_step(amsp_engine_t* e, int step, void* stream) {
   return amsp::guarded([&] {
     if (!e) throw Error("engine: null argument");
+    e->require_full_grads("step");
     e->use_device();
     e->step(step, e->pick(stream));
   });
@@ -440,6 +452,7 @@ int amsp_engine_step_host(amsp_engine_t* e, int step, const void* host_grads,
                           float* host_stats, void* stream) {
   return amsp::guarded([&] {
     if (!e || !host_grads) throw Error("engine: null argument");
+    e->require_full_grads("step_host");
     e->use_device();
     cudaStream_t s = e->pick(stream);
     if (step < 1) throw Error("engine: step index must be >= 1");
@@ -590,7 +603,7 @@ int amsp_engine_nvlink_probe(amsp_engine_t* e, uint64_t bytes, int pattern, int 
         a.src[a.nsrc++] = reinterpret_cast<const uint4*>(e->grads_of((e->rank + j) % e->world));
     }
     a.rot = 0;
-    const std::uint64_t per_src = std::min<std::uint64_t>(bytes / a.nsrc, e->phi * 2) / 16;
+    const std::uint64_t per_src = std::min<std::uint64_t>(bytes / a.nsrc, e->grad_elems * 2) / 16;
     if (per_src == 0) throw Error("engine: probe size too small");
     a.vecs_per_src = per_src;
     const std::uint64_t total = per_src * 16 * a.nsrc;

@@ -73,6 +73,17 @@ struct amsp_engine {
   // may differ per rank; every other offset is identical on all ranks).
   int micro = 1, sg = 1;
   bool staged = false, acc_by_dst = false;
+  // Gradient ring (cfg.grad_ring_elems > 0, s_g > 1): the gradient buffer is
+  // a ring of grad_elems bf16 elements that only the overlap scheduler
+  // addresses (sched.cpp, plan_grad_ring); otherwise grad_elems = Phi.
+  std::uint64_t grad_elems = 0;
+  bool ring = false;
+  void require_full_grads(const char* what) const {
+    if (ring)
+      throw Error(std::string("engine: ") + what +
+                  " needs the full gradient buffer; this engine keeps a gradient ring "
+                  "(grad_ring_elems) that only the overlap scheduler writes");
+  }
   std::size_t off_acc = 0;
   std::uint64_t acc_elems = 0;
   std::vector<int> acc_sources;  // my accumulation block, ascending rank

@@ -114,6 +114,11 @@ struct EventWork {
   // micro-batch accumulates them on the AG/RS stream (index into
   // amsp_sched::head_acc, -1 = none).
   int head_acc = -1;
+  // Tensors whose raw gradients this event's kernels read on some rank
+  // (Accumulate / Reduce / ReduceAdam), for the gradient ring's lifetimes;
+  // rel_barrier >= 0 on a Reduce / ReduceAdam: a release barrier + event
+  // after the reduce (ring mode), like the accumulations'.
+  std::vector<int> reads;
 };
 
 struct Table {
@@ -124,6 +129,8 @@ struct HeadAccum {
   Table t;
   int barrier = -1, rel_barrier = -1;
   int rel = -1;  // index of its release event in amsp_sched::rel_events
+  int mb = 0;
+  std::vector<int> reads;  // tensors whose gradients it pulls
 };
 
 constexpr int kFirstSchedBarrier = 16;  // ids 0..15 stay with the engine
@@ -196,10 +203,19 @@ struct amsp_sched {
   }
 
   // Backward stand-in's gradient output: micro-batch mb of tensor t.
+  // Where tensor t's gradient of micro-batch mb lives in the gradient
+  // buffer: its flat offset, or its slot in the gradient ring.
+  std::vector<std::vector<std::uint64_t>> ring_off;  // [mb][t] (ring mode)
+  std::uint64_t ring_need = 0;
+  std::uint64_t grad_offset(int t, int mb) const {
+    return e->ring ? ring_off[static_cast<std::size_t>(mb)][static_cast<std::size_t>(t)]
+                   : e->pmap.tensor_offset[static_cast<std::size_t>(t)];
+  }
+
   void synth(int t, int mb, bool in_place, cudaStream_t s) {
     const std::uint64_t a = e->pmap.tensor_offset[static_cast<std::size_t>(t)];
-    ck(amsp::launch_synth_grad(e->grads_of(e->rank) + a, a, e->tensor_sizes[t], e->cfg.seed,
-                               cur_step, e->rank, s, mb, in_place),
+    ck(amsp::launch_synth_grad(e->grads_of(e->rank) + grad_offset(t, mb), a, e->tensor_sizes[t],
+                               e->cfg.seed, cur_step, e->rank, s, mb, in_place),
        "synth grads");
     ++e->launches;
   }
@@ -330,16 +346,16 @@ struct amsp_sched {
         break;
       case Gemm::NormWGrad:
         ck(amsp::launch_rmsnorm_wgrad(act, dout, norm_acc,
-                                      e->grads_of(e->rank) +
-                                          e->pmap.tensor_offset[static_cast<std::size_t>(t)],
-                                      tokens, hidden, w.accum_in_place, st),
+                                      e->grads_of(e->rank) + grad_offset(t, w.mb), tokens,
+                                      hidden, w.accum_in_place, st),
            "rmsnorm wgrad");
         ++e->launches;
         break;
       case Gemm::WGrad: {
         const std::size_t ti = t < 0 ? e->tensor_sizes.size() - 1 : static_cast<std::size_t>(t);
-        blas.linear_wgrad(st, dout, act, e->grads_of(e->rank) + e->pmap.tensor_offset[ti],
-                          tokens, w.g_in, w.g_out, w.accum_in_place);
+        blas.linear_wgrad(st, dout, act,
+                          e->grads_of(e->rank) + grad_offset(static_cast<int>(ti), w.mb), tokens,
+                          w.g_in, w.g_out, w.accum_in_place);
         break;
       }
       case Gemm::None:
@@ -599,6 +615,10 @@ struct amsp_sched {
           if (with_comm) {
             barrier(w.barrier, st);
             reduce(t, comm_ctas, st);
+            if (w.rel_barrier >= 0) {  // gradient ring: every rank has pulled these
+              barrier(w.rel_barrier, st);
+              ck(cudaEventRecord(rel_events[i], st), "event record");
+            }
             if (w.adam_after) {
               ck(cudaStreamWaitEvent(st, events[w.after_event], 0), "stream wait");
               barrier(w.barrier2, st);
@@ -613,6 +633,10 @@ struct amsp_sched {
           if (with_comm) {
             barrier(w.barrier, st);
             fused(t, comm_ctas, st, opt_variant, true);
+            if (w.rel_barrier >= 0) {  // gradient ring: every rank has pulled these
+              barrier(w.rel_barrier, st);
+              ck(cudaEventRecord(rel_events[i], st), "event record");
+            }
           } else if (local_optimizer) {
             local_fused(t, comm_ctas, st, opt_variant);
           }
@@ -716,6 +740,202 @@ Table owned_pieces(const amsp::ShardLayout& L, const std::vector<FlatRange>& ran
   t.ntiles = static_cast<int>(tiles);
   return t;
 }
+
+// Gradient ring (engine grad_ring_elems > 0; PAPER.md:316-326 / D_g =
+// 2*Phi/s_g, cost_model.cpp:151). Every micro-batch's tensor gradients get a
+// slot in the ring when their grad-weight event produces them, and the slot
+// is reused once every rank has pulled it: the release barrier + event of
+// the accumulation (non-last micro-batch) or of the reduce (last one, ring
+// mode adds it) that read it. A producer whose slot overlaps older
+// gradients waits on those release events; gradients only the end-of-step
+// update reads (tensors without a reduce event, e.g. the head when s_p > 1)
+// hold their slot for the whole step (the step's end barrier releases
+// them). The placement is a deterministic simulation of the graph's issue
+// order, identical on every rank, so every rank's ring has the same layout
+// and peers address each other's slots directly. The tables' `flat` offsets
+// (used only to address gradients) are remapped into the ring, split at
+// tensor boundaries; slot starts keep flat's alignment mod 64 elements, so
+// every kernel takes the same vector / scalar paths as without the ring.
+namespace {
+
+struct RingPlan {
+  bool ok = true;
+  std::vector<std::vector<std::uint64_t>> off;           // [mb][t]
+  std::vector<std::vector<int>> waits;                    // per event: rel event ids
+};
+
+RingPlan simulate_ring(const amsp_sched* s, const std::vector<shardplan::Event>& evs,
+                       const std::vector<int>& ev_mb, const std::vector<char>& covered,
+                       std::uint64_t R) {
+  const amsp_engine* e = s->e;
+  const std::size_t n = e->tensor_sizes.size();
+  const int Mb = s->micro;
+  const int K = s->layers_k;
+  RingPlan p;
+  p.off.assign(static_cast<std::size_t>(Mb), std::vector<std::uint64_t>(n, ~0ull));
+  p.waits.assign(evs.size(), {});
+  // consumers still to come for every (mb, t)
+  std::vector<std::vector<int>> pending(static_cast<std::size_t>(Mb), std::vector<int>(n, 0));
+  for (std::size_t i = 0; i < evs.size(); ++i)
+    for (int t : s->work[i].reads) ++pending[static_cast<std::size_t>(ev_mb[i])][t];
+  for (const HeadAccum& h : s->head_acc)
+    for (int t : h.reads) ++pending[static_cast<std::size_t>(h.mb)][t];
+  for (std::size_t t = 0; t < n; ++t)
+    if (!covered[t]) ++pending[static_cast<std::size_t>(Mb - 1)][t];  // end-of-step update
+  struct Live {
+    std::uint64_t a, b;
+    int mb, t;
+    std::vector<int> rel;
+  };
+  std::vector<Live> live;
+  std::uint64_t cursor = 0;
+  auto consume = [&](int mb, int t, int rel) {
+    for (Live& L : live)
+      if (L.mb == mb && L.t == t) {
+        --pending[static_cast<std::size_t>(mb)][t];
+        L.rel.push_back(rel);
+        return;
+      }
+  };
+  const std::vector<int> head = {static_cast<int>(n) - 1, static_cast<int>(n) - 2, 0};
+  for (std::size_t i = 0; i < evs.size() && p.ok; ++i) {
+    const EventWork& w = s->work[i];
+    const int mb = ev_mb[i];
+    if (evs[i].kind == shardplan::EventKind::BwdGradWeight) {
+      const std::vector<int> ts =
+          evs[i].layer < 0 ? head : std::vector<int>{1 + evs[i].layer * K + evs[i].module};
+      for (int t : ts) {
+        const std::uint64_t size = e->tensor_sizes[static_cast<std::size_t>(t)];
+        const std::uint64_t phase = e->pmap.tensor_offset[static_cast<std::size_t>(t)] % 64;
+        auto place = [phase](std::uint64_t from) {
+          std::uint64_t st = from / 64 * 64 + phase;
+          return st < from ? st + 64 : st;
+        };
+        std::uint64_t a = place(cursor);
+        if (a + size > R) a = place(0);
+        if (a + size > R) {
+          p.ok = false;
+          break;
+        }
+        for (std::size_t k = 0; k < live.size();) {
+          const Live& L = live[k];
+          if (L.a < a + size && a < L.b) {
+            if (pending[static_cast<std::size_t>(L.mb)][L.t] > 0) {  // not yet consumed
+              p.ok = false;
+              break;
+            }
+            for (int r : L.rel) p.waits[i].push_back(r);
+            live.erase(live.begin() + static_cast<long>(k));
+          } else {
+            ++k;
+          }
+        }
+        if (!p.ok) break;
+        live.push_back({a, a + size, mb, t, {}});
+        p.off[static_cast<std::size_t>(mb)][static_cast<std::size_t>(t)] = a;
+        cursor = a + size;
+      }
+      if (w.head_acc >= 0) {  // the head's accumulation runs right behind it
+        const HeadAccum& h = s->head_acc[static_cast<std::size_t>(w.head_acc)];
+        for (int t : h.reads) consume(h.mb, t, h.rel);
+      }
+    }
+    if (w.kind == Work::Accumulate || w.kind == Work::Reduce || w.kind == Work::ReduceAdam)
+      for (int t : w.reads) consume(mb, t, static_cast<int>(i));
+  }
+  for (auto& v : p.waits) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  }
+  return p;
+}
+
+// A table of `src` re-emitted into `dst` with every piece split at tensor
+// boundaries and `flat` moved into micro-batch mb's ring slots.
+Table remap_table(const amsp_sched* s, const Table& t, const std::vector<amsp::Seg>& src,
+                  std::vector<amsp::Seg>& dst, int mb) {
+  const amsp_engine* e = s->e;
+  const auto& toff = e->pmap.tensor_offset;
+  Table out;
+  out.begin = static_cast<int>(dst.size());
+  for (int j = t.begin; j < t.begin + t.nseg; ++j) {
+    amsp::Seg sg = src[static_cast<std::size_t>(j)];
+    while (sg.len > 0) {
+      const std::size_t ti = static_cast<std::size_t>(
+          std::upper_bound(toff.begin(), toff.begin() + static_cast<long>(e->tensor_sizes.size()),
+                           sg.flat) - toff.begin() - 1);
+      const std::uint64_t in_t = sg.flat - toff[ti];
+      const std::uint64_t take = std::min<std::uint64_t>(sg.len, e->tensor_sizes[ti] - in_t);
+      const std::uint64_t slot = s->ring_off[static_cast<std::size_t>(mb)][ti];
+      if (slot == ~0ull) throw Error("sched: gradient ring has no slot for a reduced tensor");
+      dst.push_back({slot + in_t, sg.os, sg.dst, take, 0});
+      sg.flat += take;
+      sg.os += take;
+      sg.dst += take;
+      sg.len -= take;
+    }
+  }
+  long long tiles = 0;
+  for (std::size_t i = static_cast<std::size_t>(out.begin); i < dst.size(); ++i) {
+    dst[i].tile0 = static_cast<unsigned long long>(tiles);
+    tiles += static_cast<long long>((dst[i].len + amsp::kTile - 1) / amsp::kTile);
+  }
+  out.nseg = static_cast<int>(dst.size()) - out.begin;
+  out.ntiles = static_cast<int>(tiles);
+  return out;
+}
+
+void plan_grad_ring(amsp_sched* s, const std::vector<shardplan::Event>& evs,
+                    const std::vector<int>& ev_mb, const std::vector<char>& covered,
+                    std::vector<amsp::Seg>& rsegs, std::vector<amsp::Seg>& asegs,
+                    int& next_barrier) {
+  amsp_engine* e = s->e;
+  // smallest ring the schedule runs in (binary search over the simulation)
+  std::uint64_t lo = *std::max_element(e->tensor_sizes.begin(), e->tensor_sizes.end());
+  std::uint64_t hi = (e->phi + 64 * e->tensor_sizes.size()) * static_cast<std::uint64_t>(s->micro);
+  if (!simulate_ring(s, evs, ev_mb, covered, hi).ok)
+    throw Error("sched: the gradient ring cannot serve this schedule");
+  while (lo + 64 < hi) {
+    const std::uint64_t mid = (lo + hi) / 2;
+    if (simulate_ring(s, evs, ev_mb, covered, mid).ok) hi = mid; else lo = mid;
+  }
+  s->ring_need = (hi + 63) / 64 * 64;
+  if (e->grad_elems < s->ring_need)
+    throw Error("sched: gradient ring of " + std::to_string(e->grad_elems) +
+                " elements is too small for this schedule; it needs " +
+                std::to_string(s->ring_need));
+  RingPlan p = simulate_ring(s, evs, ev_mb, covered, e->grad_elems);
+  if (!p.ok)  // placement is not monotone in the ring size: the exact size can fail
+    throw Error("sched: gradient ring of " + std::to_string(e->grad_elems) +
+                " elements cannot place this schedule; use " + std::to_string(s->ring_need));
+  s->ring_off = std::move(p.off);
+  const int last = s->micro - 1;
+  std::vector<amsp::Seg> r2, a2;
+  for (std::size_t i = 0; i < evs.size(); ++i) {
+    EventWork& w = s->work[i];
+    for (int j : p.waits[i]) w.wait_release.push_back(j);
+    if (w.kind == Work::Reduce || w.kind == Work::ReduceAdam) {
+      const Table t = remap_table(s, {w.seg_begin, w.nseg, w.ntiles}, rsegs, r2, last);
+      w.seg_begin = t.begin;
+      w.nseg = t.nseg;
+      w.ntiles = t.ntiles;
+      w.rel_barrier = next_barrier++;
+    } else if (w.kind == Work::Accumulate) {
+      const Table t = remap_table(s, {w.seg_begin, w.nseg, w.ntiles}, asegs, a2, w.mb);
+      w.seg_begin = t.begin;
+      w.nseg = t.nseg;
+      w.ntiles = t.ntiles;
+    }
+    if (w.post_ntiles > 0) throw Error("sched: a gradient ring needs W > 1");
+  }
+  for (HeadAccum& h : s->head_acc) h.t = remap_table(s, h.t, asegs, a2, h.mb);
+  s->resid = remap_table(s, s->resid, rsegs, r2, last);
+  s->pending = remap_table(s, s->pending, rsegs, r2, last);
+  rsegs = std::move(r2);
+  asegs = std::move(a2);
+}
+
+}  // namespace
 
 void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* profile) {
   amsp_engine* e = s->e;
@@ -934,6 +1154,8 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
         h.barrier = next_barrier++;
         h.rel_barrier = next_barrier++;
         h.rel = static_cast<int>(evs.size() + s->head_acc.size());
+        h.mb = w.mb;
+        h.reads = ts;
         w.head_acc = static_cast<int>(s->head_acc.size());
         s->head_acc.push_back(h);
         for (int tt : ts) release[static_cast<std::size_t>(w.mb)][tt].push_back(h.rel);
@@ -965,6 +1187,7 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
         continue;
       }
       w.kind = Work::Accumulate;
+      w.reads = ts;
       const Table at = owned_pieces(acc_layout, ranges, asegs);
       w.seg_begin = at.begin;
       w.nseg = at.nseg;
@@ -1013,6 +1236,7 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
         break;
       case shardplan::EventKind::ReduceScatter: {
         w.tensor = tensor_of(ev.layer, ev.module);
+        w.reads = {w.tensor};
         covered[w.tensor] = 1;
         const Table t = owned_pieces(e->layout, {range_of(w.tensor)}, rsegs);
         w.seg_begin = t.begin;
@@ -1038,6 +1262,7 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
         if (ev.module >= static_cast<int>(buckets.size()))
           throw Error("sched: bucket index beyond the gradient stream");
         w.kind = Work::Reduce;
+        w.reads = bucket_tensors[ev.module];
         const Table t = owned_pieces(e->layout, buckets[ev.module], rsegs);
         w.seg_begin = t.begin;
         w.nseg = t.nseg;
@@ -1114,6 +1339,12 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
   }
   s->resid = owned_pieces(e->layout, rest, rsegs);
   s->pending = owned_pieces(e->layout, pend, rsegs);
+  if (e->ring) {
+    if (!s->gemm_mode && s->grad_source == 0)
+      throw Error("sched: a gradient ring is written by the step's own grad-weight events: use "
+                  "compute='gemm' or grad_source = 1");
+    plan_grad_ring(s, evs, ev_mb, covered, rsegs, asegs, next_barrier);
+  }
   s->end_a = next_barrier++;
   s->end_b = next_barrier++;
   s->flush_barrier = next_barrier++;
@@ -1179,7 +1410,7 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
   }
   s->rel_events.assign(evs.size() + s->head_acc.size(), nullptr);
   for (std::size_t i = 0; i < evs.size(); ++i)
-    if (s->work[i].kind == Work::Accumulate)
+    if (s->work[i].kind == Work::Accumulate || s->work[i].rel_barrier >= 0)
       ck(cudaEventCreateWithFlags(&s->rel_events[i], cudaEventDisableTiming), "event");
   for (const HeadAccum& h : s->head_acc) {
     ck(cudaEventCreateWithFlags(&s->rel_events[static_cast<std::size_t>(h.rel)],
@@ -1291,6 +1522,7 @@ int amsp_sched_info(const amsp_sched_t* s, amsp_sched_info_t* info) {
     info->predicted_step_s = s->predicted_step;
     info->predicted_compute_s = s->predicted_compute;
     info->mirrored_bc = s->mirror ? 1 : 0;
+    info->grad_ring_need = s->ring_need;
   });
 }
 

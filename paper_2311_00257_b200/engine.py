@@ -36,7 +36,7 @@ class Engine:
                  dp_mesh: DeviceMesh, rank: int = 0, device: int = 0,
                  layout: str = "greedy", lr: float = 1e-3, betas=(0.9, 0.95),
                  eps: float = 1e-8, weight_decay: float = 0.1, seed: int = DEFAULT_SEED,
-                 skip_gathers: bool = False, micro_batches: int = 1):
+                 skip_gathers: bool = False, micro_batches: int = 1, grad_ring: int = 0):
         if isinstance(tensors, ModelSpec):
             tensors = llama_tensors(tensors)
         self.tensor_sizes = [int(t) for t in tensors]
@@ -49,7 +49,7 @@ class Engine:
         cfg = N.EngineConfig(C.cast(arr, C.POINTER(C.c_uint64)), len(self.tensor_sizes),
                              plan._c(), dp_mesh._c(), rank, device, LAYOUTS[layout], lr,
                              betas[0], betas[1], eps, weight_decay, seed, int(skip_gathers),
-                             int(micro_batches))
+                             int(micro_batches), int(grad_ring))
         self._h = C.c_void_p()
         N.check(N.lib().amsp_engine_create(C.byref(cfg), C.byref(self._h)))
         self.info = self._info()
@@ -183,7 +183,7 @@ class Engine:
         N.check(N.lib().amsp_engine_nvlink_probe(self._h, nbytes, {"ring": 0, "all": 1}[pattern],
                                                  iters, C.byref(ms)))
         per = (nbytes // (1 if pattern == "ring" else self.world - 1)) // 16 * 16
-        moved = min(per, 2 * self.info.total_params // 16 * 16) * (
+        moved = min(per, 2 * self.info.grad_elems // 16 * 16) * (
             1 if pattern == "ring" else self.world - 1)
         return moved / (ms.value * 1e-3) / 1e9
 

@@ -65,3 +65,29 @@ def test_reference_arm_reports_the_roofline_solver_plan():
     line = _lines(r.stdout)[0]
     assert line["config"]["plan"] == "p=1x1,g=1x1,os=4x1"
     assert line["config"]["dp_mesh"] == "4x1"
+
+
+def test_step_bytes_phases_and_micro_batches():
+    """bench.step_bytes (DESIGN.md §4): ZeRO-1 moves 4*Phi*(W-1)/W per direction;
+    the phase split sums to the totals; M > 1 with s_g > 1 adds (M-1)
+    accumulation passes; s_p > 1 adds the two all-gather passes."""
+    sys.path.insert(0, str(REPO))
+    import bench
+    phi, W = 6_738_415_616, 4
+    hbm, nvl = bench.step_bytes(phi, phi // W, W, W)
+    assert abs(nvl - 4 * phi * (W - 1) / W) <= 8
+    assert hbm == 24 * (phi // W) + 2 * phi + 2 * phi
+    for kw in ({"micro": 4, "acc_elems": phi // 2, "sg": 2, "sos": 2},
+               {"sp": 4, "sos": 4}, {}):
+        k = 2 if kw.get("sos") == 2 else (1 if kw.get("sp") == 4 else W)
+        owned = phi // kw.get("sos", W)
+        phases = bench.step_bytes(phi, owned, W, k, phases=True, **kw)
+        tot = bench.step_bytes(phi, owned, W, k, **kw)
+        assert (sum(p[1] for p in phases), sum(p[2] for p in phases)) == tot
+    acc = bench.step_bytes(phi, phi // 2, W, 2, sos=2, micro=4, acc_elems=phi // 2, sg=2,
+                           phases=True)
+    assert [p[0] for p in acc] == ["accumulate", "update"]
+    # 3 accumulations: each pulls the (s_g-1)/s_g remote half of the G block
+    assert acc[0][2] == 3 * 2 * (phi // 2) * 1
+    z3 = bench.step_bytes(13_015_864_320, 13_015_864_320 // 4, 4, 1, sp=4, sos=4, phases=True)
+    assert [p[0] for p in z3] == ["all_gather", "update"]

@@ -238,3 +238,107 @@ def test_synced_scheduler_real_gemm(cuda, world, p):
         sc.close()
     for e in engines:
         e.close()
+
+
+# ---------------------------------------------------------------- gradient ring
+# s_g > 1 with the gradient buffer cut to a ring (engine grad_ring): gradient
+# memory is the G-shard accumulator (D_g = 2*Phi/s_g, cost_model.cpp:151) plus
+# a transient ring the scheduler reuses once every rank has pulled a slot.
+RING_CASES = [
+    # world, dp, p, g, os, M
+    (2, (2, 1), (1, 1), (2, 1), (2, 1), 1),   # ZeRO-2
+    (2, (2, 1), (1, 1), (2, 1), (2, 1), 3),
+    (4, (4, 1), (4, 1), (4, 1), (4, 1), 1),   # ZeRO-3
+    (4, (4, 1), (4, 1), (4, 1), (4, 1), 2),
+    (4, (4, 1), (2, 1), (2, 1), (4, 1), 2),   # s_g = s_p = 2 < s_os
+    (4, (2, 2), (1, 1), (2, 1), (2, 1), 2),   # G shard inside each virtual node
+    (8, (2, 4), (1, 1), (2, 4), (2, 4), 2)]   # BASELINE partial: G shard mesh 2x4
+
+
+def _ring_group(cuda, world, dp, p, g, os_, mb, ring):
+    from paper_2311_00257_b200.engine import Scheduler, b200_profile
+    model = S.model("tiny", micro_batch_count=mb)
+    plan = S.ShardingPlan(M(*p), M(*g), M(*os_))
+    engines = [Engine(model, plan, M(*dp), rank=r, micro_batches=mb, skip_gathers=True,
+                      grad_ring=ring) for r in range(world)]
+    link_local(engines, sync=True)
+    cost = S.CostConfig(bucket_size=1 << 20)
+    sim = S.SimConfig(overlap_tier="ag_rs_ar_bc", peak_flops_per_gpu=1e18)
+    scheds = [Scheduler(e, model, b200_profile(), cost, sim, grad_source="synth")
+              for e in engines]
+    return model, plan, engines, scheds
+
+
+@pytest.mark.parametrize("world,dp,p,g,os_,mb", RING_CASES)
+def test_gradient_ring_bit_exact(cuda, world, dp, p, g, os_, mb):
+    """Pass 1 learns the schedule's smallest ring (info.grad_ring_need) with a
+    generous one; pass 2 runs 3 steps in exactly that ring -- maximal slot
+    reuse, so every producer's wait on the previous occupant's release is
+    exercised -- and must match the oracle bit for bit. Gradient memory drops
+    from 2*Phi to the ring (+ the accumulator)."""
+    phi = S.model("tiny").total_params
+    _, _, engines, scheds = _ring_group(cuda, world, dp, p, g, os_, mb, 2 * phi)
+    need = scheds[0].info.grad_ring_need
+    assert 0 < need < phi
+    for sc in scheds:
+        sc.close()
+    for e in engines:
+        e.close()
+    model, plan, engines, scheds = _ring_group(cuda, world, dp, p, g, os_, mb, need)
+    full = Engine(S.model("tiny", micro_batch_count=mb), plan, M(*dp), rank=0,
+                  micro_batches=mb, skip_gathers=True)
+    assert engines[0].info.grad_elems == need
+    assert full.info.device_bytes - engines[0].info.device_bytes >= 2 * (phi - need) - (1 << 20)
+    full.close()
+    # the allocation contract: the planner's model-state bytes (params/s_p +
+    # G shard/s_g + OS/s_os, memory_breakdown = cost_model.cpp:140-160) plus
+    # the transient ring and gather slots, nothing of size Phi beyond that
+    mbd = S.memory_breakdown(model, plan)
+    for e in engines:
+        # + the greedy OS map's imbalance over Phi/s_os (few tensors in the tiny model)
+        imbalance = 12 * max(0, e.info.owned - phi // plan.sos())
+        extra = 2 * need + 2 * 2 * e.info.slot_elems + imbalance + (1 << 20)
+        assert e.info.device_bytes <= mbd.d_modelstate + extra, (e.info.device_bytes,
+                                                                 mbd.d_modelstate)
+    streams = _streams(cuda, world)
+    for e, s in zip(engines, streams):
+        e.init_state(s)
+    steps = 3
+    for t in range(1, steps + 1):
+        for r, s in enumerate(streams):
+            if r > 0:
+                _delay(s, 500_000)
+            scheds[r].step(t, s)
+    for r, s in enumerate(streams):
+        scheds[r].flush(s)
+    acc = O.accum(mb, plan.sg(), O.mesh_blocks(dp, g, world))
+    want = O.trajectory_range(0, phi, DEFAULT_SEED, steps, world, H, acc)
+    for e in engines:
+        e.stats()
+        _check_rank(e, want, f"rank {e.rank}")
+    for sc in scheds:
+        sc.close()
+    for e in engines:
+        e.close()
+
+
+def test_gradient_ring_errors(cuda):
+    model = S.model("tiny")
+    with pytest.raises(N.InvalidConfig, match="s_g > 1"):
+        Engine(model, S.ShardingPlan(M(1, 1), M(1, 1), M(2, 1)), M(2, 1), grad_ring=1 << 20)
+    plan = S.ShardingPlan(M(1, 1), M(2, 1), M(2, 1))
+    engines = [Engine(model, plan, M(2, 1), rank=r, grad_ring=1 << 10) for r in range(2)]
+    link_local(engines, sync=True)
+    with pytest.raises(N.InvalidConfig, match="full gradient buffer"):
+        engines[0].synth_grads(1)
+    with pytest.raises(N.InvalidConfig, match="full gradient buffer"):
+        engines[0].step(1)
+    from paper_2311_00257_b200.engine import Scheduler, b200_profile
+    with pytest.raises(N.InvalidConfig, match="too small"):
+        Scheduler(engines[0], model, b200_profile(), S.CostConfig(bucket_size=1 << 20),
+                  S.SimConfig(peak_flops_per_gpu=1e18), grad_source="synth")
+    with pytest.raises(N.InvalidConfig, match="grad-weight events"):
+        Scheduler(engines[0], model, b200_profile(), S.CostConfig(bucket_size=1 << 20),
+                  S.SimConfig(peak_flops_per_gpu=1e18))
+    for e in engines:
+        e.close()

@@ -2,6 +2,7 @@
 
   python tools/ncu_summary.py full  <report.ncu-rep> [algorithmic_bytes]
   python tools/ncu_summary.py launches <launches.csv>
+  python tools/ncu_summary.py alg <plain run log>   (algorithmic bytes of one launch)
 """
 import csv
 import io
@@ -68,5 +69,18 @@ def launches(path):
     print(json.dumps(res, indent=1))
 
 
+def alg(plain_log):
+    """Per-launch algorithmic bytes from a tools/ncu_targets.py or
+    tools/bench_raw.py JSON line (prints nothing when absent)."""
+    for line in open(plain_log):
+        if line.startswith("{"):
+            d = json.loads(line)
+            for k in ("algorithmic_bytes_per_launch", "algorithmic_bytes_per_unit",
+                      "algorithmic_bytes"):
+                if k in d:
+                    print(int(d[k]))
+                    return
+
+
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](*sys.argv[2:])
+    {"full": full, "launches": launches, "alg": alg}[sys.argv[1]](*sys.argv[2:])

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--unit", type=int, default=8, help="gather: the unit ncu captures")
     args = ap.parse_args()
     M = S.DeviceMesh
     W = args.world
@@ -72,6 +73,9 @@ def main():
         elems = sum(e.unit(u)[2] for u in range(info.n_units))
         out["units"] = info.n_units
         out["algorithmic_bytes_per_pass"] = int(elems * 2 * (W - 1) / W + 2 * elems)
+        # the captured launch: unit `--unit` (ncu -s skips the earlier ones)
+        ue = e.unit(args.unit)[2]
+        out["algorithmic_bytes_per_unit"] = int(ue * 2 * (W - 1) / W + 2 * ue)
         for t in range(args.steps):
             torch.cuda.synchronize()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
