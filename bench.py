@@ -782,19 +782,42 @@ def run_ours(args):
         del grads_dev
         torch.cuda.synchronize()
         barrier()
-        eng.step_host(step + 1, host.data_ptr(), stream)
+        if MB > 1:
+            # M micro-batches: each one's host gradients are copied (pinned,
+            # async, on the engine stream) into the engine's gradient buffer,
+            # then accumulated (k < M-1) or stepped (the last); D2H = stats
+            class _Dev:  # the engine's gradient buffer as a torch tensor (no copy)
+                __cuda_array_interface__ = {"shape": (phi,), "typestr": "<i2",
+                                            "data": (info.grads, False), "version": 3}
+            grads_view = torch.as_tensor(_Dev(), device=f"cuda:{local}")
+
+            def host_step(t):
+                with torch.cuda.stream(stream):
+                    for k in range(MB):
+                        grads_view.copy_(host, non_blocking=True)
+                        if k + 1 < MB:
+                            eng.accumulate(t, k, stream)
+                    eng.step(t, stream)
+                eng.stats()
+        else:
+            def host_step(t):
+                eng.step_host(t, host.data_ptr(), stream)
+        host_step(step + 1)
         step += 1
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             step += 1
-            eng.step_host(step, host.data_ptr(), stream)
+            host_step(step)
         barrier()
         e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
         e2e = {"value": phi / e2e_s, "unit": "params/s", "ms_per_step": round(e2e_s * 1e3, 3),
-               "h2d_bytes_per_step": 2 * phi * world, "d2h_bytes_per_step": 8 * world,
+               "h2d_bytes_per_step": 2 * phi * world * MB, "d2h_bytes_per_step": 8 * world,
                "steps": args.e2e_steps,
-               "path": ("amsp_engine_step_host: pinned host bf16 grads -> chunked H2D (2^28 "
+               "path": (f"{MB} micro-batches: pinned host bf16 grads -> async H2D into the "
+                        "engine's gradient buffer -> amsp_engine_accumulate (k < M-1) / "
+                        "amsp_engine_step (last) -> D2H stats" if MB > 1 else
+                        "amsp_engine_step_host: pinned host bf16 grads -> chunked H2D (2^28 "
                         "elements) on a copy stream, each chunk's fused update (W > 1: after a "
                         "cross-GPU barrier) behind it -> D2H stats"
                         if info.sp == 1 else
