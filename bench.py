@@ -599,20 +599,25 @@ def run_ours(args):
         roof["frac_of_phase_bound"] = round(roof["phase_bound_ms"] / ms_per_step, 4)
         roof["bound_note"] = ("lower_bound_ms assumes the phases overlap (sum of bytes / peak); "
                               "phase_bound_ms is the serial pipeline's bound")
-    ncu_traffic = REPO / "profiles" / "r01_traffic.json"
-    if ncu_traffic.exists():
+    ncu_traffic = REPO / "profiles" / "r02_traffic.json"
+    if ncu_traffic.exists() and not whole:
         try:
             d = json.loads(ncu_traffic.read_text())
             key = f"{args.model}/{world}"
             if key in d:
                 roof["traffic"] = d[key]
+            elif str(world) in d.get("ratio_by_world", {}):
+                # ncu profiles one GPU per command, so a multi-rank step has no
+                # capture: report the DRAM-traffic / algorithmic-bytes ratio of
+                # the same default kernel with the W-rank group emulated on one
+                # GPU (re-reads would show there), not an absolute figure
+                rw = d["ratio_by_world"][str(world)]
+                roof["traffic_over_algorithmic_emulated"] = rw["traffic_over_algorithmic"]
+                roof["traffic_note"] = (f"{rw['kernel']}: ncu DRAM bytes / algorithmic bytes of "
+                                        f"one launch with W={world} emulated on one GPU "
+                                        f"({rw['source']})")
         except Exception:
             pass
-    if roof["traffic"] is None and world > 1:
-        roof["traffic_note"] = (
-            "ncu profiles one GPU per command, so a multi-rank step has no capture; "
-            "the same kernel with the W-rank group emulated on one GPU moves 0.997x its "
-            "algorithmic DRAM bytes (profiles/r01_s2_ncu_fused_tma_v7_w2_emulated_1b.json)")
 
     # Busbw of the collective the fused kernel implements (nccl-tests
     # convention: RS/AG (n-1)/n on the gathered size; AR 2(n-1)/n).

@@ -811,26 +811,39 @@ RingPlan simulate_ring(const amsp_sched* s, const std::vector<shardplan::Event>&
           std::uint64_t st = from / 64 * 64 + phase;
           return st < from ? st + 64 : st;
         };
+        // first fit from the cursor (wrapping once): skip slots still holding
+        // gradients whose readers have not all been issued; slots whose
+        // readers have been issued are reused behind their release events
         std::uint64_t a = place(cursor);
-        if (a + size > R) a = place(0);
-        if (a + size > R) {
-          p.ok = false;
-          break;
-        }
-        for (std::size_t k = 0; k < live.size();) {
-          const Live& L = live[k];
-          if (L.a < a + size && a < L.b) {
-            if (pending[static_cast<std::size_t>(L.mb)][L.t] > 0) {  // not yet consumed
+        bool wrapped = false;
+        while (p.ok) {
+          if (a + size > R) {
+            if (wrapped) {
               p.ok = false;
               break;
             }
+            wrapped = true;
+            a = place(0);
+            continue;
+          }
+          const Live* block = nullptr;
+          for (const Live& L : live)
+            if (L.a < a + size && a < L.b && pending[static_cast<std::size_t>(L.mb)][L.t] > 0 &&
+                (!block || L.b > block->b))
+              block = &L;
+          if (!block) break;
+          a = place(block->b);
+        }
+        if (!p.ok) break;
+        for (std::size_t k = 0; k < live.size();) {
+          const Live& L = live[k];
+          if (L.a < a + size && a < L.b) {
             for (int r : L.rel) p.waits[i].push_back(r);
             live.erase(live.begin() + static_cast<long>(k));
           } else {
             ++k;
           }
         }
-        if (!p.ok) break;
         live.push_back({a, a + size, mb, t, {}});
         p.off[static_cast<std::size_t>(mb)][static_cast<std::size_t>(t)] = a;
         cursor = a + size;

@@ -37,6 +37,9 @@ def main():
                     help="run the steps through two schedulers created on the same engine, "
                          "alternating, with no host synchronisation between steps")
     ap.add_argument("--sched", action="store_true")
+    ap.add_argument("--ring", action="store_true",
+                    help="scheduler + s_g > 1: the gradient buffer is the schedule's smallest "
+                         "ring (learned from a first engine with a generous ring)")
     ap.add_argument("--gather", default="sm", choices=["sm", "tma", "dma"])
     ap.add_argument("--reduce", default="sm", choices=["sm", "dma"],
                     help="scheduler gradient reduce: SM NVLink pulls / copy-engine staged")
@@ -70,8 +73,23 @@ def main():
     # "chunky": three raw tensors (300M params) so the host-buffer step spans
     # two 2^28-element upload chunks, with the chunk boundary inside a tensor.
     model = [200_000_000, 100_000_008, 64] if args.model == "chunky" else S.model(args.model)
+    ring = 0
+    if args.ring:
+        from paper_2311_00257_b200.engine import Scheduler, b200_profile
+        probe = Engine(model, plan, dp, rank=rank, device=local, layout=args.layout,
+                       skip_gathers=True, micro_batches=MB,
+                       grad_ring=S.model(args.model).total_params)
+        probe.connect()
+        ps = Scheduler(probe, S.model(args.model, micro_batch_count=MB), b200_profile(),
+                       S.CostConfig(bucket_size=1 << 20),
+                       S.SimConfig(overlap_tier="ag_rs_ar_bc", peak_flops_per_gpu=1e16),
+                       grad_source="synth")
+        ring = ps.info.grad_ring_need
+        ps.close()
+        probe.close()
+        dist.barrier()
     e = Engine(model, plan, dp, rank=rank, device=local, layout=args.layout,
-               skip_gathers=args.sched, micro_batches=MB)
+               skip_gathers=args.sched, micro_batches=MB, grad_ring=ring)
     e.connect()
     if args.variant:
         e.tune(args.variant)

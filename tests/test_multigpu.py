@@ -81,7 +81,13 @@ CASES = [c + (0,) for c in CASES] + [
     # two schedulers on one engine, alternating steps, no host sync (the
     # barrier epochs must keep growing across schedulers)
     (2, "2x1", None, "greedy", "sched+synth+two", 0),
-    (4, "4x1", None, "greedy", "4x1+sched+synth+two", 0)]
+    (4, "4x1", None, "greedy", "4x1+sched+synth+two", 0),
+    # the gradient ring at the schedule's smallest size (D_g = G shard + ring)
+    (2, "2x1", None, "greedy", "g=2x1+sched+synth+ring", 0),
+    (2, "2x1", None, "greedy", "g=2x1+mb=3+sched+synth+ring", 0),
+    (4, "4x1", None, "greedy", "4x1+mb=2+sched+synth+ring", 0),
+    (4, "4x1", None, "greedy", "2x1+mb=2+sched+synth+ring", 0),
+    (4, "2x2", "2x2", "greedy", "g=2x2+mb=2+sched+synth+ring", 0)]
 
 # With AMSP_OVERSUB=1: run on a 1-GPU box with all ranks sharing the device.
 CORE = {(2, "2x1", None, "greedy", None, 0), (2, "2x1", None, "greedy", "2x1", 0),
@@ -133,6 +139,8 @@ def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh, variant):
         cmd += ["--synth"]
     if "two" in words:
         cmd += ["--two-scheds"]
+    if "ring" in words:
+        cmd += ["--ring"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=REPO,
                        env={**os.environ, "OMP_NUM_THREADS": "4"})
     out = r.stdout + r.stderr

@@ -295,8 +295,10 @@ def test_gradient_ring_bit_exact(cuda, world, dp, p, g, os_, mb):
     # the transient ring and gather slots, nothing of size Phi beyond that
     mbd = S.memory_breakdown(model, plan)
     for e in engines:
-        # + the greedy OS map's imbalance over Phi/s_os (few tensors in the tiny model)
-        imbalance = 12 * max(0, e.info.owned - phi // plan.sos())
+        # + the greedy OS map's imbalance over Phi/s_os (few tensors in the tiny
+        # model), in the OS shard and in an OS-indexed accumulator
+        imbalance = (12 * max(0, e.info.owned - phi // plan.sos()) +
+                     2 * max(0, e.info.acc_elems - phi // plan.sg()))
         extra = 2 * need + 2 * 2 * e.info.slot_elems + imbalance + (1 << 20)
         assert e.info.device_bytes <= mbd.d_modelstate + extra, (e.info.device_bytes,
                                                                  mbd.d_modelstate)

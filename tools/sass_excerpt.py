@@ -16,7 +16,7 @@ KERNELS = {  # engine_impl.h retune(): the auto variant per W
     "fused_step_tma_kernelILi1ELi3ELi2ELb0E": "W=1 default (variant 5: 3-stage ring, 2 CTAs/SM)",
     "fused_step_tma_kernelILi2ELi5ELi1ELb1E": "W=2 default (variant 11: 5 stages + bulk drain)",
     "fused_step_tma_kernelILi4ELi4ELi2ELb0E": "W=4 default (variant 10: 4-stage ring)",
-    "fused_step_tma_kernelILi8ELi3ELi1ELb0E": "W=8 default (variant 6: ring sized for 1 CTA/SM)",
+    "fused_step_tma_kernelILi8ELi2ELi2ELb0E": "W=8 default (variant 5: 2-stage ring, 2 CTAs/SM)",
     "gather_tma_kernel": "all-gather (s_p > 1) default",
 }
 text = subprocess.run(["cuobjdump", "-sass", str(LIB)], capture_output=True, text=True,
