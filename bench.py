@@ -727,7 +727,16 @@ def run_ours(args):
                 (Path(args.trace_dir) / f"measured_{tag}.json").write_text(text)
                 (Path(args.trace_dir) / f"predicted_{tag}.json").write_text(
                     sched.predicted_trace())
-        eng.stats()  # barrier error flag of the scheduled steps
+        try:
+            eng.stats()  # barrier error flag of the scheduled steps
+        except Exception as ex:
+            import re
+            m = re.search(r"barrier id (\d+)", str(ex))
+            if m and int(m.group(1)) >= 16:
+                ev, role, mbi = sched.barrier_owner(int(m.group(1)))
+                raise RuntimeError(f"{ex} -> scheduler event {ev} of {si.n_events}, {role} "
+                                   f"barrier, micro-batch {mbi}, compute={compute}") from ex
+            raise
         sched.close()
         return {"compute": compute, "tier": args.tier,
                 "tokens_per_microbatch": args.micro_batch * args.seq_len,
@@ -844,27 +853,31 @@ def run_ours(args):
     overlap_ring = None
     if args.overlap and plan.sg() > 1 and args.grad_ring:
         eng.close()
-        ring = max(info.owned, 1 << 26)
-        for _ in range(2):  # a ring too small for the schedule reports what it needs
+        from paper_2311_00257_b200.engine import Scheduler, b200_profile
+        ring, need = max(info.owned, 1 << 26), None
+        for _ in range(3):
+            # probe: a scheduler on a ring too small reports the size it needs;
+            # the measured engine gets exactly the schedule's smallest ring
             eng = Engine(model, plan, dp, rank=rank, device=local, layout=args.layout,
                          micro_batches=MB, skip_gathers=True, grad_ring=ring)
             eng.connect()
+            if need is not None:
+                break
             try:
-                from paper_2311_00257_b200.engine import Scheduler, b200_profile
                 probe = Scheduler(eng, S.model(args.model, micro_batch=args.micro_batch,
                                                seq_len=args.seq_len, micro_batch_count=MB),
                                   b200_profile(), S.CostConfig(),
                                   S.SimConfig(overlap_tier=args.tier), grad_source="synth")
                 need = probe.info.grad_ring_need
                 probe.close()
-                break
             except Exception as ex:
                 import re
                 m = re.search(r"it needs (\d+)", str(ex))
                 if not m:
                     raise
-                ring = int(m.group(1))
-                eng.close()
+                need = int(m.group(1))
+            ring = need
+            eng.close()
         eng.init_state(stream)
         torch.cuda.synchronize()
         rinfo = eng._info()

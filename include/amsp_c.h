@@ -491,6 +491,12 @@ typedef struct {
 int amsp_sched_create(amsp_engine_t* e, const amsp_sched_config_t* cfg,
                       const amsp_profile_t* profile, amsp_sched_t** out);
 int amsp_sched_info(const amsp_sched_t* s, amsp_sched_info_t* info);
+/* Which graph event uses barrier `id` (diagnostics for a barrier timeout):
+ * *event = the event index (-1: a step-level barrier), *role = 0 pre-reduce,
+ * 1 second (optimizer) barrier, 2 release, 3 head accumulation, 4 head
+ * release, 5 end-of-step A, 6 end-of-step B, 7 flush; *mb = its micro-batch.
+ * Returns 1 (invalid) for an id no event uses. */
+int amsp_sched_barrier_owner(const amsp_sched_t* s, int id, int* event, int* role, int* mb);
 /* One step. mode 1 = the full step; 0 = compute only; 2 = compute + the
  * optimizer's local HBM work without any NVLink traffic (a timing proxy for
  * the exposed-communication baseline, not a valid update). stream = the

@@ -197,6 +197,7 @@ SIGNATURES = {
     "amsp_engine_gather": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "amsp_engine_link_local": (C.c_int, [P(vp), C.c_int]),
     "amsp_engine_link_local_sync": (C.c_int, [P(vp), C.c_int]),
+    "amsp_sched_barrier_owner": (C.c_int, [vp, C.c_int, P(C.c_int), P(C.c_int), P(C.c_int)]),
     "amsp_engine_init_state": (C.c_int, [vp, vp]),
     "amsp_engine_synth_grads": (C.c_int, [vp, C.c_int, vp]),
     "amsp_engine_synth_grads_mb": (C.c_int, [vp, C.c_int, C.c_int, vp]),

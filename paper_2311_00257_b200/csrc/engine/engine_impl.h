@@ -243,9 +243,14 @@ struct amsp_engine {
   }
 
   void check_err() {
-    int h = 0;
-    ck(cudaMemcpy(&h, err, sizeof(int), cudaMemcpyDeviceToHost), "read error flag");
-    if (h) throw amsp::CudaFailure("cross-GPU barrier timed out (a peer did not arrive)");
+    int h[5] = {};
+    ck(cudaMemcpy(h, err, sizeof(h), cudaMemcpyDeviceToHost), "read error flag");
+    if (h[0])
+      throw amsp::CudaFailure(
+          "cross-GPU barrier timed out (a peer did not arrive): rank " + std::to_string(rank) +
+          " barrier id " + std::to_string(h[1]) + " (ids >= 16: scheduler) epoch " +
+          std::to_string(h[2]) + ", peer " + std::to_string(h[3]) + " at epoch " +
+          std::to_string(h[4]));
   }
 
   // Host-buffer step (s_p = 1), pipelined: the gradient upload is cut into

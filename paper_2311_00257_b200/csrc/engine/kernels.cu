@@ -301,7 +301,14 @@ __global__ void barrier_kernel(uint32_t* const* peer_flags, int world, int rank,
       uint64_t now;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       if (now - t0 > 20000000000ull) {
-        atomicExch(err, 1);
+        // diagnostics for the host: which barrier, epoch, the late peer and
+        // the epoch it had reached (the first timeout of the rank wins)
+        if (atomicCAS(err, 0, 1) == 0) {
+          err[1] = id;
+          err[2] = static_cast<int>(epoch);
+          err[3] = t;
+          err[4] = static_cast<int>(seen);
+        }
         break;
       }
       __nanosleep(64);

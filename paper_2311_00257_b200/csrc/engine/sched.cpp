@@ -48,6 +48,7 @@
 //       member directly (NVLink stores inside the update); BroadcastShard is
 //       a marker.
 #include <cmath>
+#include <cstdlib>
 
 #include "blas.h"
 #include "compute.h"
@@ -681,7 +682,8 @@ struct amsp_sched {
       // the optimizer's HBM and SM work without any NVLink traffic or
       // barrier (a timing proxy; the values are not the step's). So the
       // exposed communication t(full) - t(this) compares like with like.
-      local_fused(resid, e->sms * amsp::fused_blocks_per_sm(1, 0), main);
+      local_fused(resid, e->sms * amsp::fused_blocks_per_sm(1, tail_variant()), main,
+                  tail_variant());
       local_fused(pending, e->sms * 2, main);
       return;
     }
@@ -691,11 +693,27 @@ struct amsp_sched {
     // The LDG kernel: measured 156.7 ms vs 160.4 ms with the TMA pipeline
     // for the 7B W=1 GEMM step (profiles/r01_final_n1.json vs
     // r01_bench_n1_f3.json) over the per-tensor residual table.
-    const int full_grid = e->sms * amsp::fused_blocks_per_sm(e->world, 0);
+    const int tv = tail_variant();
+    const int full_grid = e->sms * amsp::fused_blocks_per_sm(e->world, tv);
     barrier(end_a, main);
-    fused(resid, full_grid, main);
+    fused(resid, full_grid, main, tv);
     adam_push(pending, e->sms * 2, main);
     barrier(end_b, main);
+  }
+
+  // Kernel of the end-of-step update over the residual table: the engine's
+  // auto TMA variant when every residual piece is 8-element aligned and no
+  // accumulators are summed (those are on the LDG kernels), else LDG. With
+  // real compute at W=1 the TMA tail gives a 241.7 ms step vs 248.6 ms
+  // (profiles/r02_tail_ab_7b_w1.jsonl). Tuning hook AMSP_TAIL_VARIANT.
+  bool resid_aligned = false;
+  int tail_variant() const {
+    static const int forced = [] {
+      const char* x = std::getenv("AMSP_TAIL_VARIANT");
+      return x ? std::atoi(x) : -1;
+    }();
+    if (forced >= 0) return forced;
+    return (resid_aligned && !e->staged && e->variant >= 5) ? e->variant : 0;
   }
 
   // Mirrored broadcast: pull every block now (after the last step), then a
@@ -1352,6 +1370,11 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
   }
   s->resid = owned_pieces(e->layout, rest, rsegs);
   s->pending = owned_pieces(e->layout, pend, rsegs);
+  s->resid_aligned = true;
+  for (int j = s->resid.begin; j < s->resid.begin + s->resid.nseg; ++j) {
+    const amsp::Seg& sg = rsegs[static_cast<std::size_t>(j)];
+    if ((sg.flat | sg.os | sg.dst | sg.len) & 7u) s->resid_aligned = false;
+  }
   if (e->ring) {
     if (!s->gemm_mode && s->grad_source == 0)
       throw Error("sched: a gradient ring is written by the step's own grad-weight events: use "
@@ -1536,6 +1559,41 @@ int amsp_sched_info(const amsp_sched_t* s, amsp_sched_info_t* info) {
     info->predicted_compute_s = s->predicted_compute;
     info->mirrored_bc = s->mirror ? 1 : 0;
     info->grad_ring_need = s->ring_need;
+  });
+}
+
+int amsp_sched_barrier_owner(const amsp_sched_t* s, int id, int* event, int* role, int* mb) {
+  return amsp::guarded([&] {
+    if (!s || !event || !role || !mb) throw Error("sched: null argument");
+    *event = -1;
+    *mb = 0;
+    const int step_level[3] = {s->end_a, s->end_b, s->flush_barrier};
+    for (int k = 0; k < 3; ++k)
+      if (id == step_level[k]) {
+        *role = 5 + k;
+        return;
+      }
+    for (std::size_t i = 0; i < s->work.size(); ++i) {
+      const EventWork& w = s->work[i];
+      const int ids[3] = {w.barrier, w.barrier2, w.rel_barrier};
+      for (int k = 0; k < 3; ++k)
+        if (ids[k] == id) {
+          *event = static_cast<int>(i);
+          *role = k;
+          *mb = w.mb;
+          return;
+        }
+      if (w.head_acc >= 0) {
+        const HeadAccum& h = s->head_acc[static_cast<std::size_t>(w.head_acc)];
+        if (h.barrier == id || h.rel_barrier == id) {
+          *event = static_cast<int>(i);
+          *role = h.barrier == id ? 3 : 4;
+          *mb = h.mb;
+          return;
+        }
+      }
+    }
+    throw Error("sched: no event uses barrier id " + std::to_string(id));
   });
 }
 

@@ -268,6 +268,16 @@ class Scheduler:
         mode = 2 if with_comm == "optimizer" else int(bool(with_comm))
         N.check(N.lib().amsp_sched_step(self._h, step, _stream_ptr(stream), mode))
 
+    def barrier_owner(self, barrier_id: int):
+        """(event index, role, micro-batch) of the graph event using a barrier
+        id (diagnostics of a barrier timeout; amsp_sched_barrier_owner)."""
+        ev, role, mb = C.c_int(), C.c_int(), C.c_int()
+        N.check(N.lib().amsp_sched_barrier_owner(self._h, barrier_id, C.byref(ev),
+                                                 C.byref(role), C.byref(mb)))
+        roles = ["pre-reduce", "optimizer", "release", "head accumulation", "head release",
+                 "end of step A", "end of step B", "flush"]
+        return ev.value, roles[role.value], mb.value
+
     def flush(self, stream=None) -> None:
         """Mirrored broadcast (info.mirrored_bc): pull the other owners'
         updated parameters after the last step (every rank calls it)."""

@@ -344,3 +344,59 @@ def test_gradient_ring_errors(cuda):
                   S.SimConfig(peak_flops_per_gpu=1e18))
     for e in engines:
         e.close()
+
+
+@pytest.mark.parametrize("world,g,mb,opt_overlap,bucket", [
+    (2, 2, 2, False, 1 << 20), (2, 2, 2, True, 1 << 20), (2, 2, 4, False, 1 << 20),
+    (2, 1, 2, False, 1 << 20), (2, 2, 1, False, 1 << 20), (2, 2, 4, False, 1 << 27),
+    (4, 2, 4, False, 1 << 27)])
+def test_synced_scheduler_real_gemm_micro_batches(cuda, world, g, mb, opt_overlap, bucket):
+    """compute='gemm' with M micro-batches (grad-weight GEMMs produce every
+    micro-batch's gradients; s_g = g > 1 folds the non-last ones into the G
+    shard between backward passes), optimizer after the barrier or in
+    backward, run like bench.py's overlap measurement: full steps, then
+    compute-only steps, then compute + local optimizer steps, the phases
+    separated by a device synchronisation. No barrier may time out and the
+    replicated parameters must agree on every rank after the full steps."""
+    from paper_2311_00257_b200.engine import Scheduler, b200_profile
+    model = S.model("tiny", seq_len=256, micro_batch_count=mb)
+    plan = S.ShardingPlan(M(1, 1), M(g, 1), M(world, 1))
+    engines = [Engine(model, plan, M(world, 1), rank=r, micro_batches=mb) for r in range(world)]
+    link_local(engines, sync=True)
+    streams = _streams(cuda, world)
+    scheds = [Scheduler(e, model, b200_profile(), S.CostConfig(bucket_size=bucket),
+                        S.SimConfig(peak_flops_per_gpu=1e15), compute="gemm",
+                        optimizer_overlap=opt_overlap) for e in engines]
+    for e, s in zip(engines, streams):
+        e.init_state(s)
+    for sc, s in zip(scheds, streams):
+        sc.step(1, s, with_comm=False)
+    cuda.cuda.synchronize()
+    t = 0
+    for _ in range(3):
+        t += 1
+        for r, (sc, s) in enumerate(zip(scheds, streams)):
+            if r > 0:
+                _delay(s, 500_000)
+            sc.step(t, s)
+    for sc, s in zip(scheds, streams):
+        sc.flush(s)
+    cuda.cuda.synchronize()
+    for e in engines:
+        e.stats()
+    params = [e.read("params") for e in engines]
+    for prm in params[1:]:
+        assert np.array_equal(prm, params[0])
+    # the bench's baselines: compute only, then compute + local optimizer
+    for mode in (False, "optimizer", True):
+        for _ in range(2):
+            t += 1
+            for sc, s in zip(scheds, streams):
+                sc.step(t, s, with_comm=mode)
+        cuda.cuda.synchronize()
+    for e in engines:
+        e.stats()
+    for sc in scheds:
+        sc.close()
+    for e in engines:
+        e.close()
