@@ -449,7 +449,10 @@ struct amsp_engine {
     if (staged) {
       // the holders' accumulators first, then the raw last micro-batch
       set_acc(a.acc, &a.nacc, &a.acc_by_dst);
-      if (v >= 5) {  // the accumulator sources are on the LDG kernels only
+      const int acc_blocks = v >= 5 ? amsp::tma_acc_blocks_per_sm(world, v) : 0;
+      if (acc_blocks > 0) {  // TMA ring with W + W/2 source slots per stage
+        g = std::max(1, std::min(ntiles, sms * acc_blocks));
+      } else if (v >= 5) {   // no accumulator instantiation: the LDG kernels
         v = world <= 4 ? 2 : 1;
         g = std::max(1, std::min(ntiles, sms * amsp::fused_blocks_per_sm(world, v)));
       }

@@ -963,12 +963,17 @@ __device__ __forceinline__ void bulk_s2g_nocommit(void* gmem_dst, const void* sm
                : "memory");
 }
 
-template <int W, int kStages, int kMinBlocks, bool kBulkOut>
+// NA > 0: up to NA bf16 G-shard accumulators (the holders' of micro-batches
+// 0..M-2, a.nacc <= NA of them) are pulled per stage beside the W raw
+// gradients and summed first, in holder order, then the raw gradients in
+// rank order: the LDG kernels' (and the oracle's) rounding sequence.
+template <int W, int NA, int kStages, int kMinBlocks, bool kBulkOut>
 __global__ void __launch_bounds__(kTmaConsumers + 32, kMinBlocks)
 fused_step_tma_kernel(const FusedArgs a) {
+  constexpr int G = W + NA;  // bf16 source slots per stage
   extern __shared__ __align__(128) unsigned char smem[];
-  uint16_t* s_g = reinterpret_cast<uint16_t*>(smem);  // [kStages][W][kTmaTile]
-  float* s_p = reinterpret_cast<float*>(smem + kStages * W * kTmaTile * 2);
+  uint16_t* s_g = reinterpret_cast<uint16_t*>(smem);  // [kStages][G][kTmaTile]
+  float* s_p = reinterpret_cast<float*>(smem + kStages * G * kTmaTile * 2);
   float* s_m = s_p + kStages * kTmaTile;
   float* s_v = s_m + kStages * kTmaTile;
   uint16_t* s_o = reinterpret_cast<uint16_t*>(s_v + kStages * kTmaTile);  // kBulkOut only
@@ -1034,12 +1039,18 @@ fused_step_tma_kernel(const FusedArgs a) {
         unsigned long long len = 0;
         if (base < sg.len) len = sg.len - base < kTmaTile ? sg.len - base : kTmaTile;
         meta[s] = {sg.os + base, sg.dst + base, len};
-        mbar_expect_tx(&full[s], static_cast<uint32_t>(len * (2 * W + 12)));
+        const int nacc = NA > 0 ? a.nacc : 0;
+        mbar_expect_tx(&full[s], static_cast<uint32_t>(len * (2 * (W + nacc) + 12)));
         if (len) {
 #pragma unroll
           for (int r = 0; r < W; ++r)
-            bulk_g2s(s_g + (s * W + r) * kTmaTile, a.grads[r] + sg.flat + base, len * 2,
+            bulk_g2s(s_g + (s * G + r) * kTmaTile, a.grads[r] + sg.flat + base, len * 2,
                      &full[s]);
+          if (NA > 0) {
+            const unsigned long long ai = (a.acc_by_dst ? sg.dst : sg.os) + base;
+            for (int j = 0; j < nacc; ++j)
+              bulk_g2s(s_g + (s * G + W + j) * kTmaTile, a.acc[j] + ai, len * 2, &full[s]);
+          }
           bulk_g2s(s_p + s * kTmaTile, a.master + sg.os + base, len * 4, &full[s]);
           bulk_g2s(s_m + s * kTmaTile, a.exp_avg + sg.os + base, len * 4, &full[s]);
           bulk_g2s(s_v + s * kTmaTile, a.exp_avg_sq + sg.os + base, len * 4, &full[s]);
@@ -1070,7 +1081,26 @@ fused_step_tma_kernel(const FusedArgs a) {
       uint4 graw[W];
 #pragma unroll
       for (int r = 0; r < W; ++r)
-        graw[r] = *reinterpret_cast<const uint4*>(s_g + (s * W + r) * kTmaTile + e);
+        graw[r] = *reinterpret_cast<const uint4*>(s_g + (s * G + r) * kTmaTile + e);
+      float accs[8];
+      if (NA > 0 && a.nacc > 0) {
+        const uint4 w0 = *reinterpret_cast<const uint4*>(s_g + (s * G + W) * kTmaTile + e);
+        const uint32_t* u0 = reinterpret_cast<const uint32_t*>(&w0);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          accs[2 * w] = bf16_lo(u0[w]);
+          accs[2 * w + 1] = bf16_hi(u0[w]);
+        }
+        for (int j = 1; j < a.nacc; ++j) {
+          const uint4 wj = *reinterpret_cast<const uint4*>(s_g + (s * G + W + j) * kTmaTile + e);
+          const uint32_t* uj = reinterpret_cast<const uint32_t*>(&wj);
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            accs[2 * w] = __fadd_rn(accs[2 * w], bf16_lo(uj[w]));
+            accs[2 * w + 1] = __fadd_rn(accs[2 * w + 1], bf16_hi(uj[w]));
+          }
+        }
+      }
       float4 p[2], m[2], v[2];
       p[0] = *reinterpret_cast<const float4*>(s_p + s * kTmaTile + e);
       p[1] = *reinterpret_cast<const float4*>(s_p + s * kTmaTile + e + 4);
@@ -1086,6 +1116,10 @@ fused_step_tma_kernel(const FusedArgs a) {
       for (int w = 0; w < 4; ++w) {
         const uint32_t* g0 = reinterpret_cast<const uint32_t*>(&graw[0]);
         float glo = bf16_lo(g0[w]), ghi = bf16_hi(g0[w]);
+        if (NA > 0 && a.nacc > 0) {  // accumulators first, then the raw gradients
+          glo = __fadd_rn(accs[2 * w], glo);
+          ghi = __fadd_rn(accs[2 * w + 1], ghi);
+        }
 #pragma unroll
         for (int r = 1; r < W; ++r) {  // fixed rank order, as the LDG kernel
           const uint32_t* gr = reinterpret_cast<const uint32_t*>(&graw[r]);
@@ -1254,12 +1288,13 @@ FusedFn select_fused(int world, int variant) {
 }  // namespace
 
 // Variants 5 / 6: the TMA pipeline, ring sized for 2 / 1 CTAs per SM.
-template <int W, int V>
+template <int W, int V, int NA = 0>
 struct Tma {
   static constexpr bool kOut = tma_bulk_out(V);
-  static constexpr int kStages = tma_stages(W, V);
-  static constexpr int kSmem = tma_smem(W, kStages, kOut);
-  static constexpr auto kFn = fused_step_tma_kernel<W, kStages, tma_two_ctas(V) ? 2 : 1, kOut>;
+  static constexpr int kStages = tma_stages(W + NA, V);
+  static constexpr int kSmem = tma_smem(W + NA, kStages, kOut);
+  static constexpr auto kFn =
+      fused_step_tma_kernel<W, NA, kStages, tma_two_ctas(V) ? 2 : 1, kOut>;
   // The >48 KB dynamic shared-memory opt-in, once per device.
   static cudaError_t prepare() {
     static bool done[kMaxDevices] = {};
@@ -1299,6 +1334,46 @@ int tma_blocks_per_sm(int world) {
   }
 }
 
+// Accumulator sources (M > 1, s_g > 1): the per-W default variants only
+// (5, 10, 11), with room for W/2 holders (s_g >= 2).
+template <int V>
+cudaError_t tma_launch_acc_v(const FusedArgs& a, int world, int grid, cudaStream_t stream) {
+  if (a.nacc > (world > 1 ? world / 2 : 0)) return cudaErrorInvalidValue;
+  switch (world) {
+    case 2: return Tma<2, V, 1>::launch(a, grid, stream);
+    case 4: return Tma<4, V, 2>::launch(a, grid, stream);
+    case 6: return Tma<6, V, 3>::launch(a, grid, stream);
+    case 8: return Tma<8, V, 4>::launch(a, grid, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t tma_launch_acc(const FusedArgs& a, int world, int grid, int variant,
+                           cudaStream_t stream) {
+  if (variant == 5) return tma_launch_acc_v<5>(a, world, grid, stream);
+  if (variant == 10) return tma_launch_acc_v<10>(a, world, grid, stream);
+  if (variant == 11) return tma_launch_acc_v<11>(a, world, grid, stream);
+  return cudaErrorInvalidValue;
+}
+
+// CTAs per SM of the accumulator-source instantiation (0 = none exists).
+int tma_acc_blocks_per_sm(int world, int variant) {
+  auto pick = [&](auto tag) -> int {
+    constexpr int V = decltype(tag)::value;
+    switch (world) {
+      case 2: return Tma<2, V, 1>::blocks_per_sm();
+      case 4: return Tma<4, V, 2>::blocks_per_sm();
+      case 6: return Tma<6, V, 3>::blocks_per_sm();
+      case 8: return Tma<8, V, 4>::blocks_per_sm();
+      default: return 0;
+    }
+  };
+  if (variant == 5) return pick(std::integral_constant<int, 5>{});
+  if (variant == 10) return pick(std::integral_constant<int, 10>{});
+  if (variant == 11) return pick(std::integral_constant<int, 11>{});
+  return 0;
+}
+
 template <int V>
 cudaError_t tma_launch(const FusedArgs& a, int world, int grid, cudaStream_t stream) {
   switch (world) {
@@ -1332,7 +1407,7 @@ int fused_blocks_per_sm(int world, int variant) {
 cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int variant,
                               cudaStream_t stream) {
   if (a.ntiles == 0) return cudaSuccess;
-  if (a.nacc > 0 && variant >= 5) return cudaErrorInvalidValue;  // LDG kernels only
+  if (a.nacc > 0 && variant >= 5) return tma_launch_acc(a, world, grid, variant, stream);
   if (variant == 5) return tma_launch<5>(a, world, grid, stream);  // 8-aligned segments only
   if (variant == 6) return tma_launch<6>(a, world, grid, stream);
   if (variant == 7) return tma_launch<7>(a, world, grid, stream);

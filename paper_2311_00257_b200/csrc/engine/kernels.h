@@ -77,6 +77,9 @@ AdamScalars make_adam_scalars(double lr, double beta1, double beta2, double eps,
 // Blocks per SM the fused kernel sustains for `world` gradient sources and
 // tuning `variant` (kernels.cu: 0 = auto).
 int fused_blocks_per_sm(int world, int variant);
+// CTAs per SM of the TMA variant's accumulator-source instantiation (M > 1,
+// s_g > 1; W in {2, 4, 6, 8}, variants 5 / 10 / 11), 0 when there is none.
+int tma_acc_blocks_per_sm(int world, int variant);
 
 cudaError_t launch_fused_step(const FusedArgs& a, int world, int grid, int variant,
                               cudaStream_t stream);

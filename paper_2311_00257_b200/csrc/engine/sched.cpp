@@ -694,7 +694,7 @@ struct amsp_sched {
     // for the 7B W=1 GEMM step (profiles/r01_final_n1.json vs
     // r01_bench_n1_f3.json) over the per-tensor residual table.
     const int tv = tail_variant();
-    const int full_grid = e->sms * amsp::fused_blocks_per_sm(e->world, tv);
+    const int full_grid = e->sms * tail_blocks_per_sm(tv);
     barrier(end_a, main);
     fused(resid, full_grid, main, tv);
     adam_push(pending, e->sms * 2, main);
@@ -713,7 +713,13 @@ struct amsp_sched {
       return x ? std::atoi(x) : -1;
     }();
     if (forced >= 0) return forced;
-    return (resid_aligned && !e->staged && e->variant >= 5) ? e->variant : 0;
+    if (!resid_aligned || e->variant < 5) return 0;
+    if (e->staged && amsp::tma_acc_blocks_per_sm(e->world, e->variant) == 0) return 0;
+    return e->variant;
+  }
+  int tail_blocks_per_sm(int v) const {
+    return (v >= 5 && e->staged) ? amsp::tma_acc_blocks_per_sm(e->world, v)
+                                 : amsp::fused_blocks_per_sm(e->world, v);
   }
 
   // Mirrored broadcast: pull every block now (after the last step), then a

@@ -346,11 +346,15 @@ def test_gradient_ring_errors(cuda):
         e.close()
 
 
-@pytest.mark.parametrize("world,g,mb,opt_overlap,bucket", [
-    (2, 2, 2, False, 1 << 20), (2, 2, 2, True, 1 << 20), (2, 2, 4, False, 1 << 20),
-    (2, 1, 2, False, 1 << 20), (2, 2, 1, False, 1 << 20), (2, 2, 4, False, 1 << 27),
-    (4, 2, 4, False, 1 << 27)])
-def test_synced_scheduler_real_gemm_micro_batches(cuda, world, g, mb, opt_overlap, bucket):
+@pytest.mark.parametrize("world,g,mb,opt_overlap,bucket,ring", [
+    (2, 2, 2, False, 1 << 20, False), (2, 2, 2, True, 1 << 20, False),
+    (2, 2, 4, False, 1 << 20, False), (2, 1, 2, False, 1 << 20, False),
+    (2, 2, 1, False, 1 << 20, False), (2, 2, 4, False, 1 << 27, False),
+    (4, 4, 4, False, 1 << 27, False),
+    # the gradient ring under real compute (bench.py's overlap_grad_ring)
+    (2, 2, 4, False, 1 << 20, True), (4, 4, 2, True, 1 << 20, True)])
+def test_synced_scheduler_real_gemm_micro_batches(cuda, world, g, mb, opt_overlap, bucket,
+                                                  ring):
     """compute='gemm' with M micro-batches (grad-weight GEMMs produce every
     micro-batch's gradients; s_g = g > 1 folds the non-last ones into the G
     shard between backward passes), optimizer after the barrier or in
@@ -361,7 +365,19 @@ def test_synced_scheduler_real_gemm_micro_batches(cuda, world, g, mb, opt_overla
     from paper_2311_00257_b200.engine import Scheduler, b200_profile
     model = S.model("tiny", seq_len=256, micro_batch_count=mb)
     plan = S.ShardingPlan(M(1, 1), M(g, 1), M(world, 1))
-    engines = [Engine(model, plan, M(world, 1), rank=r, micro_batches=mb) for r in range(world)]
+    need = 0
+    if ring:  # the schedule's smallest ring, learned from a generous one
+        probe = [Engine(model, plan, M(world, 1), rank=r, micro_batches=mb,
+                        grad_ring=model.total_params) for r in range(world)]
+        link_local(probe, sync=True)
+        ps = Scheduler(probe[0], model, b200_profile(), S.CostConfig(bucket_size=bucket),
+                       S.SimConfig(peak_flops_per_gpu=1e15), compute="gemm")
+        need = ps.info.grad_ring_need
+        ps.close()
+        for e in probe:
+            e.close()
+    engines = [Engine(model, plan, M(world, 1), rank=r, micro_batches=mb, grad_ring=need)
+               for r in range(world)]
     link_local(engines, sync=True)
     streams = _streams(cuda, world)
     scheds = [Scheduler(e, model, b200_profile(), S.CostConfig(bucket_size=bucket),
