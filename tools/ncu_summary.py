@@ -69,14 +69,15 @@ def launches(path):
     print(json.dumps(res, indent=1))
 
 
-def alg(plain_log):
+def alg(plain_log, key=None):
     """Per-launch algorithmic bytes from a tools/ncu_targets.py or
     tools/bench_raw.py JSON line (prints nothing when absent)."""
     for line in open(plain_log):
         if line.startswith("{"):
             d = json.loads(line)
-            for k in ("algorithmic_bytes_per_launch", "algorithmic_bytes_per_unit",
-                      "algorithmic_bytes"):
+            keys = [key] if key else ["algorithmic_bytes_per_launch",
+                                      "algorithmic_bytes_per_unit", "algorithmic_bytes"]
+            for k in keys:
                 if k in d:
                     print(int(d[k]))
                     return

@@ -6,6 +6,8 @@ are the multi-GPU kernel's HBM + NVLink bytes landing on one device).
 
   python tools/ncu_targets.py fused  --world W [--model llama-1b] [--variant 0]
   python tools/ncu_targets.py gather --world W [--model llama-1b]   (ZeRO-3, TMA gather)
+  python tools/ncu_targets.py staged --world W [--model llama-1b]   (ZeRO-2, M=2: the
+      accumulate_kernel of micro-batch 0, then the fused update with accumulator sources)
 
 Prints one JSON line: kernel name, variant, grid, per-launch algorithmic
 bytes and CUDA-event ms per launch (outside ncu only).
@@ -25,7 +27,7 @@ from paper_2311_00257_b200.engine import Engine, link_local  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["fused", "gather"])
+    ap.add_argument("what", choices=["fused", "gather", "staged"])
     ap.add_argument("--model", default="llama-1b")
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--variant", type=int, default=0)
@@ -35,11 +37,15 @@ def main():
     M = S.DeviceMesh
     W = args.world
     model = S.model(args.model)
+    mb = 1
     if args.what == "fused":
         plan = S.ShardingPlan(M(1, 1), M(1, 1), M(W, 1))
+    elif args.what == "staged":
+        plan = S.ShardingPlan(M(1, 1), M(W, 1), M(W, 1))
+        mb = 2
     else:
         plan = S.ShardingPlan(M(W, 1), M(W, 1), M(W, 1))
-    engines = [Engine(model, plan, M(W, 1), rank=r) for r in range(W)]
+    engines = [Engine(model, plan, M(W, 1), rank=r, micro_batches=mb) for r in range(W)]
     if W > 1:
         link_local(engines)
     for e in engines:
@@ -52,7 +58,32 @@ def main():
     info = engines[0]._info()
     out = {"what": args.what, "model": args.model, "phi": phi, "world": W,
            "variant": info.variant, "grid": info.grid}
-    if args.what == "fused":
+    if args.what == "staged":
+        # accumulate (rank 0): acc_elems x (2 B from each of the W G-block
+        # ranks + 2 B accumulator write; first micro-batch: no read); fused:
+        # owned x (2 B x W holders' accumulators... here W/s_g = 1 holder:
+        # 2 B + 2 B x W raw grads + 24 B state + 2 B x W param stores)
+        acc = info.acc_elems
+        out["algorithmic_bytes_accumulate"] = acc * (2 * W + 2)
+        out["algorithmic_bytes_per_launch"] = info.owned * (2 + 2 * W + 24 + 2 * W)
+        for e in engines:
+            e.time_kernel(True)
+        for t in range(1, args.steps + 1):
+            for k in range(mb):
+                for e in engines:
+                    e.synth_grads(t, mb=k)
+                if k + 1 < mb:
+                    for e in engines:
+                        e.accumulate(t, k)
+            for e in engines:
+                e.step(t)
+        torch.cuda.synchronize()
+        ms, n = engines[0].kernel_ms()
+        ams, an = engines[0].accum_ms()
+        out["kernel_ms"] = ms / max(n, 1)
+        out["accumulate_ms"] = ams / max(an, 1)
+        out["variant"] = engines[0]._info().variant
+    elif args.what == "fused":
         # per launch (rank 0): owned elements x (2 B grad from each of W ranks +
         # 24 B state r/w + 2 B param store into each of the W OS-group ranks)
         owned = info.owned
