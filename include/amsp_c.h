@@ -313,6 +313,8 @@ typedef struct {
   int acc_sources;              /* ranks pulled per accumulation (|G block|) */
   int acc_holders;              /* accumulators summed by the last micro-batch */
   uint64_t grad_elems;          /* elements of the local gradient buffer */
+  int secondary_shards;         /* ZeRO++ secondary mesh size s2 (1: none) */
+  uint64_t secondary_elems;     /* this rank's secondary slice (Phi/s2) */
 } amsp_engine_info_t;
 
 #define AMSP_IPC_HANDLE_BYTES 64
@@ -328,6 +330,9 @@ int amsp_engine_export_handle(amsp_engine_t* e, void* handle64);
 int amsp_engine_unit(const amsp_engine_t* e, int unit, int* first_tensor, int* n_tensors,
                      uint64_t* elems);
 int amsp_engine_gather(amsp_engine_t* e, int unit, int slot, void* stream);
+/* ZeRO++ (plan.has_secondary): the same all-gather from the secondary
+ * group's secondary slices (the backward gather of the step). */
+int amsp_engine_gather_secondary(amsp_engine_t* e, int unit, int slot, void* stream);
 /* Map every other rank's buffer; handles = world * 64 bytes in rank order. */
 int amsp_engine_import_handles(amsp_engine_t* e, const void* handles, int world);
 /* Single-GPU emulation of a DP group (tests / smoke): link n engines created

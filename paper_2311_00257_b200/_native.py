@@ -121,7 +121,8 @@ class EngineInfo(C.Structure):
                 ("n_units", C.c_int), ("slot_elems", C.c_uint64),
                 ("variant", C.c_int), ("micro_batches", C.c_int), ("grad_shards", C.c_int),
                 ("acc_elems", C.c_uint64), ("acc_sources", C.c_int),
-                ("acc_holders", C.c_int), ("grad_elems", C.c_uint64)]
+                ("acc_holders", C.c_int), ("grad_elems", C.c_uint64),
+                ("secondary_shards", C.c_int), ("secondary_elems", C.c_uint64)]
 
 
 class SchedConfig(C.Structure):
@@ -195,6 +196,7 @@ SIGNATURES = {
     "amsp_engine_import_handles": (C.c_int, [vp, vp, C.c_int]),
     "amsp_engine_unit": (C.c_int, [vp, C.c_int, P(C.c_int), P(C.c_int), P(u64)]),
     "amsp_engine_gather": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+    "amsp_engine_gather_secondary": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "amsp_engine_link_local": (C.c_int, [P(vp), C.c_int]),
     "amsp_engine_link_local_sync": (C.c_int, [P(vp), C.c_int]),
     "amsp_sched_barrier_owner": (C.c_int, [vp, C.c_int, P(C.c_int), P(C.c_int), P(C.c_int)]),

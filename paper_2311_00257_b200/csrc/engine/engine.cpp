@@ -110,6 +110,43 @@ void plan_units(amsp_engine* e, std::vector<amsp::CopySeg>& copy) {
   }
 }
 
+// ZeRO++ secondary parameter shard (hpZ; plan.secondary_params, domain.hpp:
+// 90-97): every rank keeps slice `position` of each tensor over its
+// secondary group (Phi/s2 bf16, cost_model.cpp:148-150), refreshed from the
+// forward all-gather; the backward all-gathers read the secondary group's
+// slices instead of the primary P shards (overlap_sim.cpp:222-230,
+// cost_model.cpp:41). Same gather units, a second copy table.
+void plan_secondary(amsp_engine* e, const DeviceMesh& dp, const shardplan::ShardingPlan& plan,
+                    std::vector<amsp::CopySeg>& copy) {
+  if (!plan.secondary_params) return;
+  if (e->sp == 1)
+    throw Error("engine: a secondary parameter mesh needs parameter sharding (s_p > 1)");
+  e->s2 = plan.secondary_params->size();
+  if (e->s2 > e->world) throw Error("engine: secondary parameter mesh larger than the DP mesh");
+  e->sec_group = amsp::mesh_group(dp, *plan.secondary_params, e->rank);
+  e->smap = amsp::pshard_map(e->tensor_sizes, e->s2);
+  for (auto& u : e->units) {
+    GatherUnit v = u;
+    const std::uint64_t base = e->pmap.tensor_offset[u.first_tensor];
+    long long tiles = 0;
+    v.seg_begin = static_cast<int>(copy.size());
+    for (int i = 0; i < u.n_tensors; ++i) {
+      const std::size_t ti = static_cast<std::size_t>(u.first_tensor + i);
+      amsp::CopySeg c{};
+      c.dst = e->pmap.tensor_offset[ti] - base;
+      c.src = e->smap.pshard_offset[ti];
+      c.len = e->smap.slice_len[ti];
+      c.tile0 = static_cast<unsigned long long>(tiles);
+      tiles += static_cast<long long>((c.len + amsp::kTile - 1) / amsp::kTile) * e->s2;
+      copy.push_back(c);
+    }
+    if (tiles > 0x7fffffffLL) throw Error("engine: gather unit too large");
+    v.ntiles = static_cast<int>(tiles);
+    v.nseg = u.n_tensors;
+    e->units2.push_back(v);
+  }
+}
+
 void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   if (!cfg || !out) throw Error("engine: null argument");
   auto e = std::make_unique<amsp_engine>();
@@ -142,8 +179,13 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   if (!v.ok())
     throw Error("engine: plan " + shardplan::to_string(plan) + " violates " +
                 v.violations.front().constraint);
-  if (cfg->plan.has_secondary)
-    throw Error("engine: ZeRO++ secondary parameter meshes are not supported");
+  if (cfg->plan.has_secondary) {
+    plan.secondary_params = to_mesh(cfg->plan.secondary);
+    if (plan.secondary_params->per_node > dp.per_node || plan.secondary_params->nodes > dp.nodes)
+      throw Error("engine: secondary parameter mesh " +
+                  shardplan::to_string(*plan.secondary_params) + " does not fit dp mesh " +
+                  shardplan::to_string(dp));
+  }
   plan_groups(e.get(), dp, plan);
   e->micro = cfg->micro_batches > 0 ? cfg->micro_batches : 1;
   if (e->micro > 16) throw Error("engine: at most 16 micro-batches per step");
@@ -156,6 +198,7 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   e->grad_elems = e->ring ? (cfg->grad_ring_elems + 63) / 64 * 64 : e->phi;
   std::vector<amsp::CopySeg> copy;
   plan_units(e.get(), copy);
+  plan_secondary(e.get(), dp, plan, copy);
   // In-step all-gathers default to the TMA bulk-copy kernel when every P
   // slice is 8-element aligned: 640 vs 608 GB/s ingress for the SM kernel
   // and 357 for the copy engines on 13B ZeRO-3 at W = 4
@@ -169,7 +212,9 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   e->off_grads = 0;
   e->off_params = align_up(e->grad_elems * 2);
   e->off_flags = e->off_params + align_up(e->param_elems * 2);
-  e->off_acc = e->off_flags + align_up(kFlagBytes);  // last: its size may differ per rank
+  e->off_sec = e->off_flags + align_up(kFlagBytes);
+  e->off_acc = e->off_sec + align_up(e->s2 > 1 ? e->smap.pshard_elems * 2 : 0);
+  // (the accumulator last: its size may differ per rank)
   e->shared_bytes = e->off_acc + align_up(e->acc_elems * 2);
   ck(cudaMalloc(&e->shared, e->shared_bytes), "cudaMalloc shared");
   ck(cudaMemset(e->shared + e->off_flags, 0, kFlagBytes), "zero flags");
@@ -323,6 +368,8 @@ int amsp_engine_info(const amsp_engine_t* e, amsp_engine_info_t* info) {
     info->acc_sources = static_cast<int>(e->acc_sources.size());
     info->acc_holders = static_cast<int>(e->acc_holders.size());
     info->grad_elems = e->grad_elems;
+    info->secondary_shards = e->s2;
+    info->secondary_elems = e->s2 > 1 ? e->smap.pshard_elems : 0;
   });
 }
 
@@ -344,6 +391,14 @@ int amsp_engine_gather(amsp_engine_t* e, int unit, int slot, void* stream) {
     if (!e) throw Error("engine: null argument");
     e->use_device();
     e->gather(unit, slot, e->pick(stream));
+  });
+}
+
+int amsp_engine_gather_secondary(amsp_engine_t* e, int unit, int slot, void* stream) {
+  return amsp::guarded([&] {
+    if (!e) throw Error("engine: null argument");
+    e->use_device();
+    e->gather(unit, slot, e->pick(stream), true);
   });
 }
 

@@ -91,9 +91,18 @@ struct amsp_engine {
   amsp::Seg* d_acc_segs = nullptr;
   int nacc_seg = 0, nacc_tiles = 0;
 
+  // ZeRO++ secondary parameter shard (plan.secondary_params; engine.cpp
+  // plan_secondary): s2 > 1 keeps Phi/s2 bf16 of every tensor's slice over
+  // the secondary group, written from the forward all-gather, read by the
+  // group's backward all-gathers.
+  int s2 = 1;
+  amsp::MeshGroup sec_group;
+  amsp::PShardMap smap;
+  std::vector<GatherUnit> units2;  // the units' secondary copy tables
+
   // Shared region and its offsets (identical on every rank).
   char* shared = nullptr;
-  std::size_t shared_bytes = 0, off_grads = 0, off_params = 0, off_flags = 0;
+  std::size_t shared_bytes = 0, off_grads = 0, off_params = 0, off_flags = 0, off_sec = 0;
   std::uint64_t param_elems = 0;
   void* peer_base[amsp::kMaxRanks] = {};
   bool imported = false;
@@ -173,6 +182,9 @@ struct amsp_engine {
   }
   uint16_t* params_of(int r) const {
     return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_params);
+  }
+  uint16_t* sec_of(int r) const {
+    return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_sec);
   }
   uint16_t* acc_of(int r) const {
     return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_acc);
@@ -338,25 +350,33 @@ struct amsp_engine {
       throw Error("engine: peers not imported (amsp_engine_import_handles)");
   }
 
-  // AG of one gather unit into slot `slot` (s_p > 1).
-  void gather(int unit, int slot, cudaStream_t s) {
+  // AG of one gather unit into `dst` (default: slot `slot`; s_p > 1), from
+  // the P shards of the P group, or with `secondary` from the secondary
+  // shards of the secondary group (the ZeRO++ backward all-gather).
+  void gather(int unit, int slot, cudaStream_t s, bool secondary = false,
+              uint16_t* dst = nullptr) {
     if (sp == 1) throw Error("engine: gather needs parameter sharding (s_p > 1)");
     if (unit < 0 || unit >= static_cast<int>(units.size()))
       throw Error("engine: gather unit out of range");
+    if (secondary && s2 == 1) throw Error("engine: no secondary parameter mesh");
     require_peers();
-    const GatherUnit& u = units[unit];
+    const GatherUnit& u = secondary ? units2[static_cast<std::size_t>(unit)] : units[unit];
+    const int n = secondary ? s2 : sp;
+    const amsp::MeshGroup& grp = secondary ? sec_group : p_group;
+    const amsp::PShardMap& map = secondary ? smap : pmap;
+    if (!dst) dst = slots[slot & 1];
+    auto src_of = [&](int q) { return secondary ? sec_of(grp.members[q]) : params_of(grp.members[q]); };
     if (gather_grid == kGatherDma) {
       // Copy-engine all-gather: per tensor of the unit, one peer-to-local
-      // DMA per P-group member (rotated start), no SMs involved.
-      uint16_t* dst = slots[slot & 1];
+      // DMA per group member (rotated start), no SMs involved.
       const std::uint64_t base = pmap.tensor_offset[u.first_tensor];
       for (int i = 0; i < u.n_tensors; ++i) {
         const std::size_t t = static_cast<std::size_t>(u.first_tensor + i);
-        const std::uint64_t len = pmap.slice_len[t];
-        for (int j = 0; j < sp; ++j) {
-          const int q = (p_group.position + 1 + j) % sp;
+        const std::uint64_t len = map.slice_len[t];
+        for (int j = 0; j < n; ++j) {
+          const int q = (grp.position + 1 + j) % n;
           ck(cudaMemcpyAsync(dst + (pmap.tensor_offset[t] - base) + q * len,
-                             params_of(p_group.members[q]) + pmap.pshard_offset[t], len * 2,
+                             src_of(q) + map.pshard_offset[t], len * 2,
                              cudaMemcpyDeviceToDevice, s),
              "gather DMA");
         }
@@ -367,14 +387,32 @@ struct amsp_engine {
     g.segs = d_copy + u.seg_begin;
     g.nseg = u.nseg;
     g.ntiles = u.ntiles;
-    for (int q = 0; q < sp; ++q) g.src[q] = params_of(p_group.members[q]);
-    g.dst = slots[slot & 1];
+    for (int q = 0; q < n; ++q) g.src[q] = src_of(q);
+    g.dst = dst;
     g.grid = gather_grid > 0 ? gather_grid : 0;
-    g.sp = sp;
-    g.rot = (p_group.position + 1) % sp;
+    g.sp = n;
+    g.rot = (grp.position + 1) % n;
     ck(gather_grid == kGatherTma ? amsp::launch_gather_tma(g, s) : amsp::launch_gather(g, s),
        "gather launch");
     ++launches;
+  }
+
+  // ZeRO++: keep this rank's secondary slice of every tensor of a unit the
+  // forward all-gather just assembled in `src` (local copy-engine copies).
+  void refresh_secondary_tensor(int t, const uint16_t* gathered, cudaStream_t s) {
+    const std::uint64_t len = smap.slice_len[static_cast<std::size_t>(t)];
+    ck(cudaMemcpyAsync(sec_of(rank) + smap.pshard_offset[static_cast<std::size_t>(t)],
+                       gathered + static_cast<std::uint64_t>(sec_group.position) * len, len * 2,
+                       cudaMemcpyDeviceToDevice, s),
+       "secondary refresh");
+  }
+  void refresh_secondary(int unit, int slot, cudaStream_t s) {
+    const GatherUnit& u = units[static_cast<std::size_t>(unit)];
+    const std::uint64_t base = pmap.tensor_offset[u.first_tensor];
+    for (int i = 0; i < u.n_tensors; ++i) {
+      const int t = u.first_tensor + i;
+      refresh_secondary_tensor(t, slots[slot & 1] + (pmap.tensor_offset[t] - base), s);
+    }
   }
 
   // The step's gradient is the mean over W ranks x M micro-batches.
@@ -427,8 +465,14 @@ struct amsp_engine {
       // cost_model.cpp:46-49); RS is fused into the optimizer kernel below.
       cudaEvent_t g_end = record_begin(gather_events, gather_events_used, s);
       const int n = static_cast<int>(units.size());
-      for (int u = 0; u < n; ++u) gather(u, u, s);
-      for (int u = n - 1; u >= 0; --u) gather(u, u, s);
+      for (int u = 0; u < n; ++u) {
+        gather(u, u, s);
+        if (s2 > 1) refresh_secondary(u, u, s);
+      }
+      // ZeRO++: every rank's secondary slices are in place before the
+      // backward all-gathers read them from the secondary group
+      if (s2 > 1) barrier(s);
+      for (int u = n - 1; u >= 0; --u) gather(u, u, s, s2 > 1);
       if (g_end) ck(cudaEventRecord(g_end, s), "event record");
     }
     amsp::FusedArgs a{};

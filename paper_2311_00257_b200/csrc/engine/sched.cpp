@@ -83,6 +83,10 @@ struct EventWork {
   int tensor = -1;
   Gemm gemm = Gemm::None;
   int g_in = 0, g_out = 0;
+  // ZeRO++ (engine s2 > 1): the step's first all-gather of a tensor reads
+  // the P shards and refreshes this rank's secondary slice; every later one
+  // (backward, recompute, later micro-batches) reads the secondary group
+  bool secondary = false, refresh = false;
   bool attention = false;  // attention core before (Fwd) / after (DGrad) the GEMM
   int barrier = -1;
   int seg_begin = 0, nseg = 0, ntiles = 0;
@@ -181,6 +185,7 @@ struct amsp_sched {
   }
   amsp::Seg* d_rsegs = nullptr;
   amsp::CopySeg* d_tcopy = nullptr;
+  amsp::CopySeg* d_tcopy2 = nullptr;  // ZeRO++ secondary slices
   // Micro-batch accumulation tables (Seg::os = G-shard accumulator offset),
   // the release event of every Work::Accumulate event, and the head pieces.
   amsp::Seg* d_asegs = nullptr;
@@ -434,6 +439,7 @@ struct amsp_sched {
       if (s) cudaStreamDestroy(s);
     cudaFree(d_rsegs);
     cudaFree(d_tcopy);
+    cudaFree(d_tcopy2);
     cudaFree(d_asegs);
     cudaFree(d_ssegs);
     cudaFree(stage);
@@ -534,29 +540,34 @@ struct amsp_sched {
     ++e->launches;
   }
 
-  void gather_tensor(int t, cudaStream_t s) {
+  void gather_tensor(int t, cudaStream_t s, bool secondary = false) {
+    const int n = secondary ? e->s2 : e->sp;
+    const amsp::MeshGroup& grp = secondary ? e->sec_group : e->p_group;
+    const amsp::PShardMap& map = secondary ? e->smap : e->pmap;
+    auto src_of = [&](int q) {
+      return secondary ? e->sec_of(grp.members[q]) : e->params_of(grp.members[q]);
+    };
     if (gather_dma) {
-      // Copy-engine all-gather: one peer-to-local DMA per P-group member
+      // Copy-engine all-gather: one peer-to-local DMA per group member
       // (rotated start, like the SM kernel) — no SMs taken from compute.
-      const std::uint64_t len = e->pmap.slice_len[t], src = e->pmap.pshard_offset[t];
+      const std::uint64_t len = map.slice_len[t], src = map.pshard_offset[t];
       uint16_t* dst = gather_dst(t);
-      for (int j = 0; j < e->sp; ++j) {
-        const int q = (e->p_group.position + 1 + j) % e->sp;
-        ck(cudaMemcpyAsync(dst + static_cast<std::uint64_t>(q) * len,
-                           e->params_of(e->p_group.members[q]) + src, len * 2,
+      for (int j = 0; j < n; ++j) {
+        const int q = (grp.position + 1 + j) % n;
+        ck(cudaMemcpyAsync(dst + static_cast<std::uint64_t>(q) * len, src_of(q) + src, len * 2,
                            cudaMemcpyDeviceToDevice, s),
            "gather DMA");
       }
       return;
     }
     amsp::GatherArgs g{};
-    g.segs = d_tcopy + t;
+    g.segs = (secondary ? d_tcopy2 : d_tcopy) + t;
     g.nseg = 1;
-    const unsigned long long len = e->pmap.slice_len[t];
-    g.ntiles = static_cast<int>((len + amsp::kTile - 1) / amsp::kTile) * e->sp;
-    g.sp = e->sp;
-    g.rot = (e->p_group.position + 1) % e->sp;
-    for (int q = 0; q < e->sp; ++q) g.src[q] = e->params_of(e->p_group.members[q]);
+    const unsigned long long len = map.slice_len[t];
+    g.ntiles = static_cast<int>((len + amsp::kTile - 1) / amsp::kTile) * n;
+    g.sp = n;
+    g.rot = (grp.position + 1) % n;
+    for (int q = 0; q < n; ++q) g.src[q] = src_of(q);
     g.dst = gather_dst(t);
     g.grid = comm_ctas;
     ck(gather_tma ? amsp::launch_gather_tma(g, s) : amsp::launch_gather(g, s), "sched gather");
@@ -610,7 +621,13 @@ struct amsp_sched {
           }
           break;
         case Work::Gather:
-          if (with_comm) gather_tensor(w.tensor, st);
+          if (with_comm) {
+            // ZeRO++: every rank's secondary slices exist before the first
+            // gather from the secondary group
+            if (w.barrier >= 0) barrier(w.barrier, st);
+            gather_tensor(w.tensor, st, w.secondary);
+            if (w.refresh) e->refresh_secondary_tensor(w.tensor, gather_dst(w.tensor), st);
+          }
           break;
         case Work::Reduce:
           if (with_comm) {
@@ -1163,6 +1180,8 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
   std::vector<std::vector<std::vector<int>>> release(
       static_cast<std::size_t>(Mb), std::vector<std::vector<int>>(n));
   const std::vector<int> head_tensors = {static_cast<int>(n) - 1, static_cast<int>(n) - 2, 0};
+  std::vector<char> ag_seen(n, 0);  // ZeRO++: the step's first gather of the tensor
+  bool first_secondary = true;
   std::vector<char> covered(n, 0);  // reduced by some event
   std::vector<char> updated(n, 0);  // optimizer already applied by some event
   int next_barrier = kFirstSchedBarrier;
@@ -1269,6 +1288,18 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
       case shardplan::EventKind::AllGather:
         w.kind = Work::Gather;
         w.tensor = tensor_of(ev.layer, ev.module);
+        if (e->s2 > 1) {
+          if (!ag_seen[static_cast<std::size_t>(w.tensor)]) {
+            ag_seen[static_cast<std::size_t>(w.tensor)] = 1;
+            w.refresh = true;
+          } else {
+            w.secondary = true;
+            if (first_secondary) {
+              w.barrier = next_barrier++;
+              first_secondary = false;
+            }
+          }
+        }
         ++s->n_gather;
         break;
       case shardplan::EventKind::ReduceScatter: {
@@ -1443,6 +1474,13 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
     ck(cudaMalloc(&s->d_tcopy, n * sizeof(amsp::CopySeg)), "cudaMalloc tensor copies");
     ck(cudaMemcpy(s->d_tcopy, tc.data(), n * sizeof(amsp::CopySeg), cudaMemcpyHostToDevice),
        "copy tensor copies");
+    if (e->s2 > 1) {
+      for (std::size_t t = 0; t < n; ++t)
+        tc[t] = {0, e->smap.pshard_offset[t], e->smap.slice_len[t], 0};
+      ck(cudaMalloc(&s->d_tcopy2, n * sizeof(amsp::CopySeg)), "cudaMalloc secondary copies");
+      ck(cudaMemcpy(s->d_tcopy2, tc.data(), n * sizeof(amsp::CopySeg), cudaMemcpyHostToDevice),
+         "copy secondary copies");
+    }
   }
   if (!asegs.empty()) {
     ck(cudaMalloc(&s->d_asegs, asegs.size() * sizeof(amsp::Seg)), "cudaMalloc accumulation segs");

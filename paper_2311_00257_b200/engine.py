@@ -146,8 +146,11 @@ class Engine:
         N.check(N.lib().amsp_engine_unit(self._h, u, C.byref(f), C.byref(n), C.byref(el)))
         return f.value, n.value, el.value
 
-    def gather(self, unit: int, slot: int = 0, stream=None) -> None:
-        N.check(N.lib().amsp_engine_gather(self._h, unit, slot, _stream_ptr(stream)))
+    def gather(self, unit: int, slot: int = 0, stream=None, secondary: bool = False) -> None:
+        """All-gather of one unit into slot `slot`, from the P shards, or with
+        `secondary` from the ZeRO++ secondary group's slices."""
+        fn = N.lib().amsp_engine_gather_secondary if secondary else N.lib().amsp_engine_gather
+        N.check(fn(self._h, unit, slot, _stream_ptr(stream)))
 
     def tune(self, variant: int = 0, grid: int = 0) -> None:
         N.check(N.lib().amsp_engine_tune(self._h, variant, grid))

@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--g-mesh", default=None,
                     help="explicit G mesh (default: the P mesh when given, else 1x1)")
     ap.add_argument("--micro-batches", type=int, default=1)
+    ap.add_argument("--p2-mesh", default=None,
+                    help="ZeRO++ secondary parameter mesh (backward all-gathers)")
     ap.add_argument("--synth", action="store_true",
                     help="scheduler: every grad-weight event writes its micro-batch gradient "
                          "during the step (grad_source=synth); no host barriers anywhere")
@@ -69,7 +71,8 @@ def main():
     if args.g_mesh:
         g_mesh = mesh(args.g_mesh)
     MB = args.micro_batches
-    plan = S.ShardingPlan(p_mesh, g_mesh, os_mesh)
+    plan = S.ShardingPlan(p_mesh, g_mesh, os_mesh,
+                          secondary_params=mesh(args.p2_mesh) if args.p2_mesh else None)
     # "chunky": three raw tensors (300M params) so the host-buffer step spans
     # two 2^28-element upload chunks, with the chunk boundary inside a tensor.
     model = [200_000_000, 100_000_008, 64] if args.model == "chunky" else S.model(args.model)

@@ -87,7 +87,11 @@ CASES = [c + (0,) for c in CASES] + [
     (2, "2x1", None, "greedy", "g=2x1+mb=3+sched+synth+ring", 0),
     (4, "4x1", None, "greedy", "4x1+mb=2+sched+synth+ring", 0),
     (4, "4x1", None, "greedy", "2x1+mb=2+sched+synth+ring", 0),
-    (4, "2x2", "2x2", "greedy", "g=2x2+mb=2+sched+synth+ring", 0)]
+    (4, "2x2", "2x2", "greedy", "g=2x2+mb=2+sched+synth+ring", 0),
+    # ZeRO++ secondary parameter mesh (backward all-gathers from the secondary group)
+    (4, "4x1", None, "greedy", "4x1+p2=2x1", 0),
+    (4, "4x1", None, "greedy", "4x1+p2=2x1+sched+synth", 0),
+    (4, "4x1", None, "greedy", "4x1+p2=2x1+mb=2+sched+synth", 0)]
 
 # With AMSP_OVERSUB=1: run on a 1-GPU box with all ranks sharing the device.
 CORE = {(2, "2x1", None, "greedy", None, 0), (2, "2x1", None, "greedy", "2x1", 0),
@@ -141,6 +145,8 @@ def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh, variant):
         cmd += ["--two-scheds"]
     if "ring" in words:
         cmd += ["--ring"]
+    if "p2" in opts:
+        cmd += ["--p2-mesh", opts["p2"]]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=REPO,
                        env={**os.environ, "OMP_NUM_THREADS": "4"})
     out = r.stdout + r.stderr

@@ -416,3 +416,90 @@ def test_synced_scheduler_real_gemm_micro_batches(cuda, world, g, mb, opt_overla
         sc.close()
     for e in engines:
         e.close()
+
+
+# ---------------------------------------------------------------- ZeRO++ secondary shard
+# plan.secondary_params (domain.hpp:90-97): the backward all-gathers read the
+# secondary group's slices (overlap_sim.cpp:222-230, cost_model.cpp:41), each
+# rank keeping Phi/s2 more bf16 (cost_model.cpp:148-150).
+@pytest.mark.parametrize("world,p,sec", [(4, 4, 2), (8, 8, 2), (8, 8, 4), (4, 2, 2)])
+def test_zeropp_secondary_shard(cuda, world, p, sec):
+    model = S.model("tiny")
+    plan = S.ShardingPlan(M(p, 1), M(p, 1), M(world, 1) if p < world else M(p, 1),
+                          secondary_params=M(sec, 1))
+    engines = [Engine(model, plan, M(world, 1), rank=r) for r in range(world)]
+    link_local(engines, sync=True)
+    phi = model.total_params
+    plain = Engine(model, S.ShardingPlan(plan.p, plan.g, plan.os), M(world, 1))
+    assert engines[0].info.secondary_shards == sec
+    assert engines[0].info.secondary_elems == phi // sec
+    assert engines[0].info.device_bytes - plain.info.device_bytes >= 2 * phi // sec
+    plain.close()
+    streams = _streams(cuda, world)
+    for e, s in zip(engines, streams):
+        e.tune_gather("tma")
+        e.init_state(s)
+    steps = 3
+    for t in range(1, steps + 1):
+        for r, (e, s) in enumerate(zip(engines, streams)):
+            if r > 0:
+                _delay(s, 300_000)
+            e.synth_grads(t, s)
+            e.step(t, s)
+    want = O.trajectory_range(0, phi, DEFAULT_SEED, steps, world, H)
+    prev = O.trajectory_range(0, phi, DEFAULT_SEED, steps - 1, world, H)
+    for e in engines:
+        e.stats()
+        _check_rank(e, want, f"rank {e.rank}")
+    # the last step's backward gathers came from the secondary slices, which
+    # its forward gathers had refreshed with the step's input parameters
+    offsets = np.cumsum([0] + engines[0].tensor_sizes)
+    for e in engines:
+        for u in (0, 1):
+            first, n, elems = e.unit(u)
+            lo = offsets[first]
+            assert np.array_equal(e.read(f"slot{u}", 0, elems), prev[3][lo:lo + elems]), (e.rank, u)
+    # and gathering from the secondary group now reproduces them too
+    e = engines[-1]
+    for u in range(e.info.n_units):
+        first, n, elems = e.unit(u)
+        e.gather(u, u % 2, streams[-1], secondary=True)
+        lo = offsets[first]
+        assert np.array_equal(e.read(f"slot{u % 2}", 0, elems), prev[3][lo:lo + elems]), u
+    for e in engines:
+        e.close()
+
+
+@pytest.mark.parametrize("world,p,sec,mb", [(4, 4, 2, 1), (4, 4, 2, 2), (8, 8, 4, 1)])
+def test_zeropp_scheduler(cuda, world, p, sec, mb):
+    """The overlap scheduler with a secondary mesh: each tensor's first
+    all-gather of the step refreshes the secondary slice, later ones read the
+    secondary group (after one barrier); the step stays bit-exact."""
+    from paper_2311_00257_b200.engine import Scheduler, b200_profile
+    model = S.model("tiny", micro_batch_count=mb)
+    plan = S.ShardingPlan(M(p, 1), M(p, 1), M(p, 1), secondary_params=M(sec, 1))
+    engines = [Engine(model, plan, M(world, 1), rank=r, micro_batches=mb, skip_gathers=True)
+               for r in range(world)]
+    link_local(engines, sync=True)
+    streams = _streams(cuda, world)
+    scheds = [Scheduler(e, model, b200_profile(), S.CostConfig(bucket_size=1 << 20),
+                        S.SimConfig(overlap_tier="ag_rs_ar_bc", peak_flops_per_gpu=1e18),
+                        grad_source="synth", gather="tma") for e in engines]
+    assert scheds[0].info.n_gather > 0
+    for e, s in zip(engines, streams):
+        e.init_state(s)
+    steps = 3
+    for t in range(1, steps + 1):
+        for r, s in enumerate(streams):
+            if r > 0:
+                _delay(s, 300_000)
+            scheds[r].step(t, s)
+    acc = O.accum(mb, plan.sg(), O.mesh_blocks((world, 1), (p, 1), world))
+    want = O.trajectory_range(0, model.total_params, DEFAULT_SEED, steps, world, H, acc)
+    for e in engines:
+        e.stats()
+        _check_rank(e, want, f"rank {e.rank}")
+    for sc in scheds:
+        sc.close()
+    for e in engines:
+        e.close()
