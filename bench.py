@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--model", default="llama-7b")
     ap.add_argument("--plan", default="zero1",
                     help="zero1 (P/G replica, OS over dp) | replica | zero3 | roofline (the "
-                         "native B200 roofline solver's pick) | 'p=AxB,g=AxB,os=AxB'")
+                         "native B200 roofline solver's pick) | 'p=AxB,g=AxB,os=AxB[,p2=AxB]' "
+                         "(p2: ZeRO++ secondary parameter mesh)")
     ap.add_argument("--mesh", default=None, help="dp mesh per_node x nodes, default Nx1")
     ap.add_argument("--layout", default="greedy", choices=["greedy", "contiguous"])
     ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (0 auto)")
@@ -114,7 +115,8 @@ def plan_of(args, S, dp):
                            S.Topology(dp.nodes, 1, 1.0))
         return S.solve_roofline(S.model(args.model), cl, b200_profile())[0][0].plan
     parts = dict(kv.split("=") for kv in args.plan.split(","))
-    return S.ShardingPlan(mesh_of(parts["p"], S), mesh_of(parts["g"], S), mesh_of(parts["os"], S))
+    return S.ShardingPlan(mesh_of(parts["p"], S), mesh_of(parts["g"], S), mesh_of(parts["os"], S),
+                          secondary_params=mesh_of(parts["p2"], S) if "p2" in parts else None)
 
 
 def peaks():
@@ -185,7 +187,7 @@ class ClockSampler:
 
 
 def step_bytes(phi, owned, world, k, sp=1, sos=None, gathers=2, micro=1, acc_elems=0, sg=1,
-               phases=False):
+               phases=False, s2=1):
     """Algorithmic bytes per GPU of ONE step (all ranks run concurrently;
     DESIGN.md §4). k = ranks sharing this rank's P position in its OS group
     (its parameter-store destinations), R = W/s_os replica groups.
@@ -205,6 +207,9 @@ def step_bytes(phi, owned, world, k, sp=1, sos=None, gathers=2, micro=1, acc_ele
       NVL in = 2*acc_elems*(s_g-1), out = 2*Phi*(s_g-1)/s_g
     and the last micro-batch's update reads the W/s_g holders' accumulators
     (2*owned each, W/s_g - 1 over NVLink) besides the raw gradients.
+    ZeRO++ (s2 > 1): the backward pass gathers over the secondary group
+    (2*Phi*(s2-1)/s2 per direction) and the forward pass refreshes the
+    Phi/s2 secondary slice (4*Phi/s2 HBM).
     phases=True returns [(name, hbm, nvl)] per serial phase instead."""
     sos = sos or k * sp
     R = world // sos
@@ -225,8 +230,9 @@ def step_bytes(phi, owned, world, k, sp=1, sos=None, gathers=2, micro=1, acc_ele
         nvl_in = nvl_out = 0
     out.append(("update", hbm, max(nvl_in, nvl_out)))
     if sp > 1:
-        g_hbm = gathers * 4 * phi
-        g_nvl = gathers * 2 * phi * (sp - 1) // sp
+        gs = 1 if (s2 > 1 and gathers >= 2) else 0
+        g_hbm = gathers * 4 * phi + (4 * phi // s2 if gs else 0)
+        g_nvl = (gathers - gs) * 2 * phi * (sp - 1) // sp + (2 * phi * (s2 - 1) // s2 if gs else 0)
         out.insert(0, ("all_gather", g_hbm, g_nvl))
     if phases:
         return out
@@ -540,7 +546,8 @@ def run_ours(args):
     phi = info.total_params
     value = phi / (ms_per_step * 1e-3)
     pk, pk_src = peaks()
-    sb = dict(sp=info.sp, sos=plan.sos(), micro=MB, acc_elems=info.acc_elems, sg=plan.sg())
+    sb = dict(sp=info.sp, sos=plan.sos(), micro=MB, acc_elems=info.acc_elems, sg=plan.sg(),
+              s2=info.secondary_shards)
     hbm_b, nvl_b = step_bytes(phi, info.owned, world, info.os_group_size, **sb)
     phases = step_bytes(phi, info.owned, world, info.os_group_size, phases=True, **sb)
     # s_p = 1, M = 1: the step is one fused launch (+2 tiny barriers) -> time

@@ -49,9 +49,16 @@ StepTraffic step_traffic(const std::vector<std::uint64_t>& tensor_sizes, const S
   s.nvl_out = 2 * (R * phi - s.owned) + 2 * s.owned * static_cast<std::uint64_t>(k - 1);
   if (sp > 1) {
     const std::uint64_t g = static_cast<std::uint64_t>(gathers);
-    s.hbm += g * 4 * phi;
-    s.nvl_in += g * 2 * phi * (usp - 1) / usp;
-    s.nvl_out += g * 2 * phi * (usp - 1) / usp;
+    // ZeRO++: the backward pass (the second of the two) gathers over the
+    // secondary group, and the forward pass refreshes the Phi/s2 slice
+    const std::uint64_t u2 =
+        plan.secondary_params ? static_cast<std::uint64_t>(plan.secondary_params->size()) : 0;
+    const std::uint64_t gs = (u2 > 1 && g >= 2) ? 1 : 0;
+    s.hbm += g * 4 * phi + (gs ? 4 * (phi / u2) : 0);
+    const std::uint64_t nvl = (g - gs) * 2 * phi * (usp - 1) / usp +
+                              (gs ? 2 * phi * (u2 - 1) / u2 : 0);
+    s.nvl_in += nvl;
+    s.nvl_out += nvl;
   }
   if (W == 1) s.nvl_in = s.nvl_out = 0;
   s.t_hbm = static_cast<double>(s.hbm) / hbm_bw;
@@ -116,7 +123,9 @@ std::vector<RooflineResult> solve_roofline(const shardplan::ModelSpec& model,
     if (!any || r.result.memory.d_total < leanest.memory.d_total) leanest = r.result;
     any = true;
     r.runnable = std::all_of(tensors.begin(), tensors.end(), [&](std::uint64_t t) {
-      return t % static_cast<std::uint64_t>(plan.sp()) == 0;
+      return t % static_cast<std::uint64_t>(plan.sp()) == 0 &&
+             (!plan.secondary_params ||
+              t % static_cast<std::uint64_t>(plan.secondary_params->size()) == 0);
     });
     if (!r.result.feasible || !r.runnable) continue;
     r.step = step_traffic_max(tensors, plan, dp, layout, 2, hbm_bw, nvlink_bw, nullptr);

@@ -101,3 +101,23 @@ def test_roofline_solver_reports_infeasible_with_the_leanest_plan():
     with pytest.raises(S.NoFeasiblePlanError) as ei:
         S.solve_roofline(model, _cluster(M(2, 1), capacity=10_000_000_000), b200_profile())
     assert ei.value.closest().plan == S.ShardingPlan(M(2, 1), M(2, 1), M(2, 1))
+
+
+@pytest.mark.parametrize("s2", [2, 4])
+def test_zeropp_secondary_mesh_bytes(s2):
+    """ZeRO++ (plan.secondary_params): the backward all-gather pass moves
+    2*Phi*(s2-1)/s2 per direction over the secondary group instead of
+    2*Phi*(s_p-1)/s_p, and the forward pass refreshes the Phi/s2 slice; the
+    native roofline and bench.step_bytes agree."""
+    m = S.model("llama-13b")
+    tensors = S.model_tensors(m)
+    phi = sum(tensors)
+    dp = M(8, 1)
+    plan = S.ShardingPlan(M(8, 1), M(8, 1), M(8, 1), secondary_params=M(s2, 1))
+    st, _ = S.step_roofline(tensors, plan, dp, 0)
+    _, owned = pshard_layout(tensors, 8, 0, 1, 0, "greedy")
+    hbm, nvl = bench.step_bytes(phi, owned, 8, 1, 8, 8, s2=s2)
+    assert (st.hbm_bytes, max(st.nvlink_in_bytes, st.nvlink_out_bytes)) == (hbm, nvl)
+    plain, _ = S.step_roofline(tensors, S.ShardingPlan(M(8, 1), M(8, 1), M(8, 1)), dp, 0)
+    fewer = 2 * phi * 7 // 8 - 2 * phi * (s2 - 1) // s2
+    assert max(plain.nvlink_in_bytes, plain.nvlink_out_bytes) - nvl == fewer
