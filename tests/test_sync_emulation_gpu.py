@@ -455,7 +455,7 @@ def test_zeropp_secondary_shard(cuda, world, p, sec):
     # its forward gathers had refreshed with the step's input parameters
     offsets = np.cumsum([0] + engines[0].tensor_sizes)
     for e in engines:
-        for u in (0, 1):
+        for u in range(min(2, e.info.n_units)):
             first, n, elems = e.unit(u)
             lo = offsets[first]
             assert np.array_equal(e.read(f"slot{u}", 0, elems), prev[3][lo:lo + elems]), (e.rank, u)
