@@ -125,6 +125,15 @@ void plan_secondary(amsp_engine* e, const DeviceMesh& dp, const shardplan::Shard
   if (e->s2 > e->world) throw Error("engine: secondary parameter mesh larger than the DP mesh");
   e->sec_group = amsp::mesh_group(dp, *plan.secondary_params, e->rank);
   e->smap = amsp::pshard_map(e->tensor_sizes, e->s2);
+  // the forward gathers write the secondary slice as they go (GatherArgs::sec)
+  // when every primary and secondary slice is 8-element aligned
+  e->sec_fused = true;
+  for (std::size_t t = 0; t < e->tensor_sizes.size(); ++t)
+    if ((e->pmap.slice_len[t] | e->smap.slice_len[t]) & 7u) e->sec_fused = false;
+  for (const auto& u : e->units)
+    for (int i = 0; i < u.n_tensors; ++i)
+      copy[static_cast<std::size_t>(u.seg_begin + i)].sec =
+          e->smap.pshard_offset[static_cast<std::size_t>(u.first_tensor + i)];
   for (auto& u : e->units) {
     GatherUnit v = u;
     const std::uint64_t base = e->pmap.tensor_offset[u.first_tensor];

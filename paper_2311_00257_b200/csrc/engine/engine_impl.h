@@ -96,6 +96,7 @@ struct amsp_engine {
   // the secondary group, written from the forward all-gather, read by the
   // group's backward all-gathers.
   int s2 = 1;
+  bool sec_fused = false;  // forward gathers store the secondary slice themselves
   amsp::MeshGroup sec_group;
   amsp::PShardMap smap;
   std::vector<GatherUnit> units2;  // the units' secondary copy tables
@@ -354,7 +355,7 @@ struct amsp_engine {
   // the P shards of the P group, or with `secondary` from the secondary
   // shards of the secondary group (the ZeRO++ backward all-gather).
   void gather(int unit, int slot, cudaStream_t s, bool secondary = false,
-              uint16_t* dst = nullptr) {
+              uint16_t* dst = nullptr, bool refresh = false) {
     if (sp == 1) throw Error("engine: gather needs parameter sharding (s_p > 1)");
     if (unit < 0 || unit >= static_cast<int>(units.size()))
       throw Error("engine: gather unit out of range");
@@ -365,8 +366,10 @@ struct amsp_engine {
     const amsp::MeshGroup& grp = secondary ? sec_group : p_group;
     const amsp::PShardMap& map = secondary ? smap : pmap;
     if (!dst) dst = slots[slot & 1];
-    auto src_of = [&](int q) { return secondary ? sec_of(grp.members[q]) : params_of(grp.members[q]); };
-    if (gather_grid == kGatherDma) {
+    auto src_of = [&](int q) {
+      return secondary ? sec_of(grp.members[q]) : params_of(grp.members[q]);
+    };
+    if (gather_grid == kGatherDma || (refresh && !sec_fused)) {
       // Copy-engine all-gather: per tensor of the unit, one peer-to-local
       // DMA per group member (rotated start), no SMs involved.
       const std::uint64_t base = pmap.tensor_offset[u.first_tensor];
@@ -380,10 +383,17 @@ struct amsp_engine {
                              cudaMemcpyDeviceToDevice, s),
              "gather DMA");
         }
+        if (refresh)
+          refresh_secondary_tensor(static_cast<int>(t), dst + (pmap.tensor_offset[t] - base), s);
       }
       return;
     }
     amsp::GatherArgs g{};
+    if (refresh) {
+      g.sec = sec_of(rank);
+      g.s2 = s2;
+      g.pos2 = sec_group.position;
+    }
     g.segs = d_copy + u.seg_begin;
     g.nseg = u.nseg;
     g.ntiles = u.ntiles;
@@ -397,22 +407,14 @@ struct amsp_engine {
     ++launches;
   }
 
-  // ZeRO++: keep this rank's secondary slice of every tensor of a unit the
-  // forward all-gather just assembled in `src` (local copy-engine copies).
+  // ZeRO++: keep this rank's secondary slice of tensor t from the gathered
+  // tensor (a local copy; used when the gather cannot store it itself).
   void refresh_secondary_tensor(int t, const uint16_t* gathered, cudaStream_t s) {
     const std::uint64_t len = smap.slice_len[static_cast<std::size_t>(t)];
     ck(cudaMemcpyAsync(sec_of(rank) + smap.pshard_offset[static_cast<std::size_t>(t)],
                        gathered + static_cast<std::uint64_t>(sec_group.position) * len, len * 2,
                        cudaMemcpyDeviceToDevice, s),
        "secondary refresh");
-  }
-  void refresh_secondary(int unit, int slot, cudaStream_t s) {
-    const GatherUnit& u = units[static_cast<std::size_t>(unit)];
-    const std::uint64_t base = pmap.tensor_offset[u.first_tensor];
-    for (int i = 0; i < u.n_tensors; ++i) {
-      const int t = u.first_tensor + i;
-      refresh_secondary_tensor(t, slots[slot & 1] + (pmap.tensor_offset[t] - base), s);
-    }
   }
 
   // The step's gradient is the mean over W ranks x M micro-batches.
@@ -465,10 +467,7 @@ struct amsp_engine {
       // cost_model.cpp:46-49); RS is fused into the optimizer kernel below.
       cudaEvent_t g_end = record_begin(gather_events, gather_events_used, s);
       const int n = static_cast<int>(units.size());
-      for (int u = 0; u < n; ++u) {
-        gather(u, u, s);
-        if (s2 > 1) refresh_secondary(u, u, s);
-      }
+      for (int u = 0; u < n; ++u) gather(u, u, s, false, nullptr, s2 > 1);
       // ZeRO++: every rank's secondary slices are in place before the
       // backward all-gathers read them from the secondary group
       if (s2 > 1) barrier(s);

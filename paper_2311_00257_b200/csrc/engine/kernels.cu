@@ -360,19 +360,33 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs a) {
         e[u] = base + (static_cast<unsigned long long>(u) * kBlock + threadIdx.x) * 8ull;
         if (e[u] + 8 <= len) v[u] = ld_ro_v4(from + src + e[u]);
       }
+      // ZeRO++ fused secondary refresh: tensor-local index of this tile's
+      // elements is q*len + e; my secondary slice is [lo2, lo2 + len2)
+      const unsigned long long len2 = a.sec ? len * a.sp / a.s2 : 0;
+      const unsigned long long lo2 = len2 * static_cast<unsigned long long>(a.pos2);
 #pragma unroll
       for (int u = 0; u < kVecPerThread; ++u) {
         if (e[u] + 8 <= len) {
           st_v4(a.dst + dst + e[u], v[u]);
+          const unsigned long long x = static_cast<unsigned long long>(q) * len + e[u];
+          if (a.sec && x >= lo2 && x < lo2 + len2) st_v4(a.sec + cs.sec + (x - lo2), v[u]);
         } else {
-          for (unsigned long long k = e[u]; k < len && k < e[u] + 8; ++k)
+          for (unsigned long long k = e[u]; k < len && k < e[u] + 8; ++k) {
             a.dst[dst + k] = from[src + k];
+            const unsigned long long x = static_cast<unsigned long long>(q) * len + k;
+            if (a.sec && x >= lo2 && x < lo2 + len2) a.sec[cs.sec + (x - lo2)] = from[src + k];
+          }
         }
       }
     } else {
+      const unsigned long long len2 = a.sec ? len * a.sp / a.s2 : 0;
+      const unsigned long long lo2 = len2 * static_cast<unsigned long long>(a.pos2);
       for (unsigned long long e = base + threadIdx.x; e < base + kTile && e < len;
-           e += blockDim.x)
+           e += blockDim.x) {
         a.dst[dst + e] = from[src + e];
+        const unsigned long long x = static_cast<unsigned long long>(q) * len + e;
+        if (a.sec && x >= lo2 && x < lo2 + len2) a.sec[cs.sec + (x - lo2)] = from[src + e];
+      }
     }
   }
 }
@@ -1181,12 +1195,6 @@ fused_step_tma_kernel(const FusedArgs a) {
 // Every CopySeg must be 8-element aligned (16-byte bulk granularity).
 constexpr int kGatherStages = 5;
 
-__device__ __forceinline__ void bulk_s2g(void* gmem_dst, const void* smem_src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
-               "r"(smem_addr(smem_src)), "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
 
 __global__ void __launch_bounds__(32) gather_tma_kernel(const GatherArgs a) {
   __shared__ __align__(128) uint16_t buf[kGatherStages][kTile];
@@ -1205,6 +1213,10 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(const GatherArgs a) {
   cur.staged = false;
   uint16_t* dst_of[kGatherStages];
   uint32_t bytes_of[kGatherStages];
+  // ZeRO++ fused secondary refresh (a.sec): part of the tile inside this
+  // rank's secondary slice, as (element offset in the tile, count, sec dst)
+  uint32_t sec_from[kGatherStages], sec_n[kGatherStages];
+  uint16_t* sec_dst[kGatherStages];
   auto load = [&](int i) {
     const int tile = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
     const CopySeg& cs = cur.at(tile);
@@ -1216,6 +1228,19 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(const GatherArgs a) {
     const int s = i % kGatherStages;
     dst_of[s] = a.dst + cs.dst + static_cast<unsigned long long>(q) * cs.len + off;
     bytes_of[s] = static_cast<uint32_t>(len * 2);
+    sec_n[s] = 0;
+    if (a.sec) {
+      const unsigned long long len2 = cs.len * a.sp / a.s2;
+      const unsigned long long lo2 = len2 * static_cast<unsigned long long>(a.pos2);
+      const unsigned long long x0 = static_cast<unsigned long long>(q) * cs.len + off;
+      const unsigned long long b0 = x0 > lo2 ? x0 : lo2;
+      const unsigned long long b1 = x0 + len < lo2 + len2 ? x0 + len : lo2 + len2;
+      if (b0 < b1) {
+        sec_from[s] = static_cast<uint32_t>(b0 - x0);
+        sec_n[s] = static_cast<uint32_t>(b1 - b0);
+        sec_dst[s] = a.sec + cs.sec + (b0 - lo2);
+      }
+    }
     mbar_expect_tx(&full[s], bytes_of[s]);
     bulk_g2s(buf[s], a.src[q] + cs.src + off, bytes_of[s], &full[s]);
   };
@@ -1223,7 +1248,9 @@ __global__ void __launch_bounds__(32) gather_tma_kernel(const GatherArgs a) {
   for (int i = 0; i < n; ++i) {
     const int s = i % kGatherStages;
     mbar_wait(&full[s], (i / kGatherStages) & 1);
-    bulk_s2g(dst_of[s], buf[s], bytes_of[s]);
+    bulk_s2g_nocommit(dst_of[s], buf[s], bytes_of[s]);
+    if (sec_n[s]) bulk_s2g_nocommit(sec_dst[s], buf[s] + sec_from[s], sec_n[s] * 2);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // one group per tile
     const int j = i - 1 + kGatherStages;  // refill the stage tile i-1 used
     if (i >= 1 && j < n) {
       asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");

@@ -30,6 +30,7 @@ struct Seg {
 // pulls evenly from all peers (no NVLink egress hot spot when ranks drift).
 struct CopySeg {
   unsigned long long dst, src, len, tile0;
+  unsigned long long sec;  // ZeRO++: offset of the tensor's slice in the secondary buffer
 };
 
 struct GatherArgs {
@@ -41,6 +42,12 @@ struct GatherArgs {
   const uint16_t* src[8];  // P shards of the P-group members, position order
   uint16_t* dst;           // gathered unit buffer (local)
   int grid;                // CTAs (0 = 4 per SM)
+  // ZeRO++ forward gather (sec != nullptr): every element of the tensor that
+  // falls in this rank's secondary slice [pos2*L/s2, (pos2+1)*L/s2) is also
+  // stored at sec + seg.sec + (index - pos2*L/s2) -- the secondary refresh
+  // fused into the gather (no second read). L = len * sp; slices 8-aligned.
+  uint16_t* sec;
+  int s2, pos2;
 };
 
 constexpr int kBlock = 256;

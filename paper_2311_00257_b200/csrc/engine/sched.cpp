@@ -540,7 +540,7 @@ struct amsp_sched {
     ++e->launches;
   }
 
-  void gather_tensor(int t, cudaStream_t s, bool secondary = false) {
+  void gather_tensor(int t, cudaStream_t s, bool secondary = false, bool refresh = false) {
     const int n = secondary ? e->s2 : e->sp;
     const amsp::MeshGroup& grp = secondary ? e->sec_group : e->p_group;
     const amsp::PShardMap& map = secondary ? e->smap : e->pmap;
@@ -558,9 +558,15 @@ struct amsp_sched {
                            cudaMemcpyDeviceToDevice, s),
            "gather DMA");
       }
+      if (refresh) e->refresh_secondary_tensor(t, dst, s);
       return;
     }
     amsp::GatherArgs g{};
+    if (refresh && e->sec_fused) {  // the secondary slice stored by the gather itself
+      g.sec = e->sec_of(e->rank);
+      g.s2 = e->s2;
+      g.pos2 = e->sec_group.position;
+    }
     g.segs = (secondary ? d_tcopy2 : d_tcopy) + t;
     g.nseg = 1;
     const unsigned long long len = map.slice_len[t];
@@ -572,6 +578,7 @@ struct amsp_sched {
     g.grid = comm_ctas;
     ck(gather_tma ? amsp::launch_gather_tma(g, s) : amsp::launch_gather(g, s), "sched gather");
     ++e->launches;
+    if (refresh && !e->sec_fused) e->refresh_secondary_tensor(t, gather_dst(t), s);
   }
 
   void run(int step, cudaStream_t main, int mode) {
@@ -625,8 +632,7 @@ struct amsp_sched {
             // ZeRO++: every rank's secondary slices exist before the first
             // gather from the secondary group
             if (w.barrier >= 0) barrier(w.barrier, st);
-            gather_tensor(w.tensor, st, w.secondary);
-            if (w.refresh) e->refresh_secondary_tensor(w.tensor, gather_dst(w.tensor), st);
+            gather_tensor(w.tensor, st, w.secondary, w.refresh);
           }
           break;
         case Work::Reduce:
@@ -1470,13 +1476,14 @@ void build(amsp_sched* s, const amsp_sched_config_t* cfg, const amsp_profile_t* 
   if (e->sp > 1) {
     std::vector<amsp::CopySeg> tc(n);
     for (std::size_t t = 0; t < n; ++t)
-      tc[t] = {0, e->pmap.pshard_offset[t], e->pmap.slice_len[t], 0};
+      tc[t] = {0, e->pmap.pshard_offset[t], e->pmap.slice_len[t], 0,
+               e->s2 > 1 ? e->smap.pshard_offset[t] : 0};
     ck(cudaMalloc(&s->d_tcopy, n * sizeof(amsp::CopySeg)), "cudaMalloc tensor copies");
     ck(cudaMemcpy(s->d_tcopy, tc.data(), n * sizeof(amsp::CopySeg), cudaMemcpyHostToDevice),
        "copy tensor copies");
     if (e->s2 > 1) {
       for (std::size_t t = 0; t < n; ++t)
-        tc[t] = {0, e->smap.pshard_offset[t], e->smap.slice_len[t], 0};
+        tc[t] = {0, e->smap.pshard_offset[t], e->smap.slice_len[t], 0, 0};
       ck(cudaMalloc(&s->d_tcopy2, n * sizeof(amsp::CopySeg)), "cudaMalloc secondary copies");
       ck(cudaMemcpy(s->d_tcopy2, tc.data(), n * sizeof(amsp::CopySeg), cudaMemcpyHostToDevice),
          "copy secondary copies");
