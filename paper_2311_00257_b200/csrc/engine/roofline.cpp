@@ -117,7 +117,23 @@ std::vector<RooflineResult> solve_roofline(const shardplan::ModelSpec& model,
   std::vector<RooflineResult> out;
   shardplan::PlanResult leanest;
   bool any = false;
+  // The reference's candidates, plus (our extension) the ZeRO++ variants of
+  // every parameter-sharded one: a secondary mesh strictly inside the P mesh
+  // for the backward all-gathers (domain.hpp:90-97; the engine runs them).
+  std::vector<ShardingPlan> candidates;
   for (const ShardingPlan& plan : shardplan::enumerate_candidates(cluster)) {
+    candidates.push_back(plan);
+    if (plan.sp() == 1 || plan.secondary_params) continue;
+    for (int a = 1; a <= plan.p.per_node; ++a)
+      for (int b = 1; b <= plan.p.nodes; ++b)
+        if (plan.p.per_node % a == 0 && plan.p.nodes % b == 0 && a * b > 1 &&
+            a * b < plan.sp()) {
+          ShardingPlan z = plan;
+          z.secondary_params = DeviceMesh{a, b};
+          candidates.push_back(z);
+        }
+  }
+  for (const ShardingPlan& plan : candidates) {
     RooflineResult r;
     r.result = shardplan::evaluate_plan(model, cluster, plan, profile, cfg);
     if (!any || r.result.memory.d_total < leanest.memory.d_total) leanest = r.result;
