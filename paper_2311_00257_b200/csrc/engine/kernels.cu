@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(256, MINB) adamw_flat_kernel(const void* __res
           st_stream_v4(m + i + 4, mm[u][1]);
           st_stream_v4(v + i, vv[u][0]);
           st_stream_v4(v + i + 4, vv[u][1]);
-          if (param_out) st_v4(param_out + i, pack8(pf));
+          if (param_out) st_stream_u4(param_out + i, pack8(pf));
         }
       },
       [=](unsigned long long i) {
@@ -642,15 +642,15 @@ __global__ void __launch_bounds__(256) ag_downcast_kernel(const AgArgs a) {
 #pragma unroll
         for (int u = 0; u < kRawU; ++u) {
           if (!ok[u]) continue;
-          x[u][0] = ld_state_v4(a.src + g[u] * 8);
-          x[u][1] = ld_state_v4(a.src + g[u] * 8 + 4);
+          x[u][0] = ld_ro_f4(a.src + g[u] * 8);
+          x[u][1] = ld_ro_f4(a.src + g[u] * 8 + 4);
         }
 #pragma unroll
         for (int u = 0; u < kRawU; ++u) {
           if (!ok[u]) continue;
           const uint4 b = pack8(reinterpret_cast<const float*>(&x[u][0]));
 #pragma unroll
-          for (int d = 0; d < ND; ++d) st_v4(a.dsts[d] + a.dst_offset + g[u] * 8, b);
+          for (int d = 0; d < ND; ++d) st_stream_u4(a.dsts[d] + a.dst_offset + g[u] * 8, b);
         }
       },
       [=](unsigned long long k) {
