@@ -255,36 +255,40 @@ RING_CASES = [
     (8, (2, 4), (1, 1), (2, 4), (2, 4), 2)]   # BASELINE partial: G shard mesh 2x4
 
 
-def _ring_group(cuda, world, dp, p, g, os_, mb, ring):
+def _ring_group(cuda, world, dp, p, g, os_, mb, ring, reduce="sm", p2=None):
     from paper_2311_00257_b200.engine import Scheduler, b200_profile
     model = S.model("tiny", micro_batch_count=mb)
-    plan = S.ShardingPlan(M(*p), M(*g), M(*os_))
+    plan = S.ShardingPlan(M(*p), M(*g), M(*os_), secondary_params=M(*p2) if p2 else None)
     engines = [Engine(model, plan, M(*dp), rank=r, micro_batches=mb, skip_gathers=True,
                       grad_ring=ring) for r in range(world)]
     link_local(engines, sync=True)
     cost = S.CostConfig(bucket_size=1 << 20)
     sim = S.SimConfig(overlap_tier="ag_rs_ar_bc", peak_flops_per_gpu=1e18)
-    scheds = [Scheduler(e, model, b200_profile(), cost, sim, grad_source="synth")
+    scheds = [Scheduler(e, model, b200_profile(), cost, sim, grad_source="synth", reduce=reduce)
               for e in engines]
     return model, plan, engines, scheds
 
 
-@pytest.mark.parametrize("world,dp,p,g,os_,mb", RING_CASES)
-def test_gradient_ring_bit_exact(cuda, world, dp, p, g, os_, mb):
+@pytest.mark.parametrize("world,dp,p,g,os_,mb,reduce,p2", [c + ("sm", None) for c in RING_CASES] + [
+    # the ring under copy-engine staged reduces, and with a ZeRO++ secondary mesh
+    (4, (4, 1), (4, 1), (4, 1), (4, 1), 2, "dma", None),
+    (2, (2, 1), (1, 1), (2, 1), (2, 1), 2, "dma", None),
+    (4, (4, 1), (4, 1), (4, 1), (4, 1), 2, "sm", (2, 1))])
+def test_gradient_ring_bit_exact(cuda, world, dp, p, g, os_, mb, reduce, p2):
     """Pass 1 learns the schedule's smallest ring (info.grad_ring_need) with a
     generous one; pass 2 runs 3 steps in exactly that ring -- maximal slot
     reuse, so every producer's wait on the previous occupant's release is
     exercised -- and must match the oracle bit for bit. Gradient memory drops
     from 2*Phi to the ring (+ the accumulator)."""
     phi = S.model("tiny").total_params
-    _, _, engines, scheds = _ring_group(cuda, world, dp, p, g, os_, mb, 2 * phi)
+    _, _, engines, scheds = _ring_group(cuda, world, dp, p, g, os_, mb, 2 * phi, reduce, p2)
     need = scheds[0].info.grad_ring_need
     assert 0 < need < phi
     for sc in scheds:
         sc.close()
     for e in engines:
         e.close()
-    model, plan, engines, scheds = _ring_group(cuda, world, dp, p, g, os_, mb, need)
+    model, plan, engines, scheds = _ring_group(cuda, world, dp, p, g, os_, mb, need, reduce, p2)
     full = Engine(S.model("tiny", micro_batch_count=mb), plan, M(*dp), rank=0,
                   micro_batches=mb, skip_gathers=True)
     assert engines[0].info.grad_elems == need
