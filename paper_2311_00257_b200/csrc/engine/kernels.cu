@@ -720,43 +720,58 @@ __global__ void __launch_bounds__(kBlock) adam_push_kernel(const AdamPushArgs a)
     const Seg sg = cursor.at(tile);
     const unsigned long long base = (static_cast<unsigned long long>(tile) - sg.tile0) * kTile;
     const bool aligned = ((sg.os | sg.dst) & 7ull) == 0;
-#pragma unroll 1
-    for (int it = 0; it < kVecPerThread; ++it) {
-      const unsigned long long e = base + (static_cast<unsigned long long>(it) * kBlock +
-                                           threadIdx.x) * 8ull;
-      if (e >= sg.len) continue;
-      const unsigned long long o = sg.os + e;
-      if (aligned && e + 8 <= sg.len) {
-        float4 g[2] = {ld_state_v4(a.red + o), ld_state_v4(a.red + o + 4)};
-        float4 p[2] = {ld_state_v4(a.master + o), ld_state_v4(a.master + o + 4)};
-        float4 m[2] = {ld_state_v4(a.exp_avg + o), ld_state_v4(a.exp_avg + o + 4)};
-        float4 v[2] = {ld_state_v4(a.exp_avg_sq + o), ld_state_v4(a.exp_avg_sq + o + 4)};
-        float* gf = reinterpret_cast<float*>(g);
-        float* pf = reinterpret_cast<float*>(p);
-        float* mf = reinterpret_cast<float*>(m);
-        float* vf = reinterpret_cast<float*>(v);
+    // all kVecPerThread vectors' loads in flight before any math (the HBM
+    // latency, not the bandwidth, limited the one-vector-at-a-time loop)
+    unsigned long long e[kVecPerThread];
+    bool full[kVecPerThread];
+    float4 g[kVecPerThread][2], p[kVecPerThread][2], m[kVecPerThread][2], v[kVecPerThread][2];
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+      e[u] = base + (static_cast<unsigned long long>(u) * kBlock + threadIdx.x) * 8ull;
+      full[u] = aligned && e[u] + 8 <= sg.len;
+      if (full[u]) {
+        const unsigned long long o = sg.os + e[u];
+        g[u][0] = ld_state_v4(a.red + o);
+        g[u][1] = ld_state_v4(a.red + o + 4);
+        p[u][0] = ld_state_v4(a.master + o);
+        p[u][1] = ld_state_v4(a.master + o + 4);
+        m[u][0] = ld_state_v4(a.exp_avg + o);
+        m[u][1] = ld_state_v4(a.exp_avg + o + 4);
+        v[u][0] = ld_state_v4(a.exp_avg_sq + o);
+        v[u][1] = ld_state_v4(a.exp_avg_sq + o + 4);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+      if (e[u] >= sg.len) continue;
+      if (full[u]) {
+        const unsigned long long o = sg.os + e[u];
+        float* gf = reinterpret_cast<float*>(g[u]);
+        float* pf = reinterpret_cast<float*>(p[u]);
+        float* mf = reinterpret_cast<float*>(m[u]);
+        float* vf = reinterpret_cast<float*>(v[u]);
         uint32_t packed[4];
 #pragma unroll
         for (int j = 0; j < 8; ++j) adamw(a.s, gf[j], pf[j], mf[j], vf[j]);
 #pragma unroll
         for (int w = 0; w < 4; ++w) packed[w] = pack_bf16x2(pf[2 * w], pf[2 * w + 1]);
-        st_stream_v4(a.master + o, p[0]);
-        st_stream_v4(a.master + o + 4, p[1]);
-        st_stream_v4(a.exp_avg + o, m[0]);
-        st_stream_v4(a.exp_avg + o + 4, m[1]);
-        st_stream_v4(a.exp_avg_sq + o, v[0]);
-        st_stream_v4(a.exp_avg_sq + o + 4, v[1]);
+        st_stream_v4(a.master + o, p[u][0]);
+        st_stream_v4(a.master + o + 4, p[u][1]);
+        st_stream_v4(a.exp_avg + o, m[u][0]);
+        st_stream_v4(a.exp_avg + o + 4, m[u][1]);
+        st_stream_v4(a.exp_avg_sq + o, v[u][0]);
+        st_stream_v4(a.exp_avg_sq + o + 4, v[u][1]);
         const uint4 out = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        for (int d = 0; d < a.ndst; ++d) st_v4(a.dsts[d] + sg.dst + e, out);
+        for (int d = 0; d < a.ndst; ++d) st_v4(a.dsts[d] + sg.dst + e[u], out);
       } else {
-        const unsigned long long end = e + 8 < sg.len ? e + 8 : sg.len;
-        for (unsigned long long k = e; k < end; ++k) {
-          float p = a.master[sg.os + k], m = a.exp_avg[sg.os + k], v = a.exp_avg_sq[sg.os + k];
-          adamw(a.s, a.red[sg.os + k], p, m, v);
-          a.master[sg.os + k] = p;
-          a.exp_avg[sg.os + k] = m;
-          a.exp_avg_sq[sg.os + k] = v;
-          const uint16_t b = to_bf16(p);
+        const unsigned long long end = e[u] + 8 < sg.len ? e[u] + 8 : sg.len;
+        for (unsigned long long k = e[u]; k < end; ++k) {
+          float pp = a.master[sg.os + k], mm = a.exp_avg[sg.os + k], vv = a.exp_avg_sq[sg.os + k];
+          adamw(a.s, a.red[sg.os + k], pp, mm, vv);
+          a.master[sg.os + k] = pp;
+          a.exp_avg[sg.os + k] = mm;
+          a.exp_avg_sq[sg.os + k] = vv;
+          const uint16_t b = to_bf16(pp);
           for (int d = 0; d < a.ndst; ++d) a.dsts[d][sg.dst + k] = b;
         }
       }
@@ -1470,6 +1485,12 @@ cudaError_t launch_reduce(const ReduceArgs& a, int world, int grid, cudaStream_t
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+int adam_push_blocks_per_sm() {
+  int blocks = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, adam_push_kernel, kBlock, 0);
+  return blocks > 0 ? blocks : 1;
 }
 
 cudaError_t launch_adam_push(const AdamPushArgs& a, int grid, cudaStream_t stream) {

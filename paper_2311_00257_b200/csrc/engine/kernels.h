@@ -153,6 +153,7 @@ struct AdamPushArgs {
 };
 cudaError_t launch_reduce(const ReduceArgs& a, int world, int grid, cudaStream_t stream);
 cudaError_t launch_adam_push(const AdamPushArgs& a, int grid, cudaStream_t stream);
+int adam_push_blocks_per_sm();
 // Compute stand-in: `ctas` CTAs, each busy for `ns` nanoseconds of FMA work.
 cudaError_t launch_spin(int ctas, unsigned long long ns, cudaStream_t stream);
 // params[dst+k] = bf16(master_init(flat+k)) over a P-shard segment table.

@@ -720,7 +720,8 @@ struct amsp_sched {
     const int full_grid = e->sms * tail_blocks_per_sm(tv);
     barrier(end_a, main);
     fused(resid, full_grid, main, tv);
-    adam_push(pending, e->sms * 2, main);
+    // one wave of resident CTAs (occupancy of the push kernel)
+    adam_push(pending, e->sms * amsp::adam_push_blocks_per_sm(), main);
     barrier(end_b, main);
   }
 
