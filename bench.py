@@ -83,7 +83,7 @@ def parse():
     ap.add_argument("--bc", default="auto", choices=["auto", "push"],
                     help="overlapped step: mirrored broadcast of updated shards in the next "
                          "forward (auto, tier ag_rs_ar_bc) or push inside the optimizer")
-    ap.add_argument("--step-gather", default="auto", choices=["auto", "sm", "dma", "tma"],
+    ap.add_argument("--step-gather", default="auto", choices=["auto", "sm", "dma", "tma", "push"],
                     help="all-gather implementation inside the pipeline-only step (s_p > 1); "
                          "auto = the engine's default (TMA when the P slices are aligned)")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -560,6 +560,7 @@ def run_ours(args):
              "whole step: " +
              ("2 all-gather passes (" +
               {"sm": "gather_kernel", "dma": "copy engines", "tma": "gather_tma_kernel",
+               "push": "push_tma_kernel (NVLink stores)",
                "auto": "engine default: gather_tma_kernel when aligned"}[args.step_gather] +
               ") + " if info.sp > 1 else "") +
              (f"{MB - 1} G-shard accumulations (accumulate_kernel) + " if MB > 1 else "") +

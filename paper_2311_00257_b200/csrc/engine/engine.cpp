@@ -110,6 +110,25 @@ void plan_units(amsp_engine* e, std::vector<amsp::CopySeg>& copy) {
   }
 }
 
+// Push all-gather tables: each rank handles only its own slice of every
+// tensor of a unit (tile0 counts ceil(len / kTile) tiles per tensor) and
+// stores it into all s_p members' slots.
+void plan_push(amsp_engine* e, std::vector<amsp::CopySeg>& copy) {
+  for (const auto& u : e->units) {
+    GatherUnit v = u;
+    v.seg_begin = static_cast<int>(copy.size());
+    long long tiles = 0;
+    for (int i = 0; i < u.n_tensors; ++i) {
+      amsp::CopySeg c = copy[static_cast<std::size_t>(u.seg_begin + i)];
+      c.tile0 = static_cast<unsigned long long>(tiles);
+      tiles += static_cast<long long>((c.len + amsp::kTile - 1) / amsp::kTile);
+      copy.push_back(c);
+    }
+    v.ntiles = static_cast<int>(tiles);
+    e->units_push.push_back(v);
+  }
+}
+
 // ZeRO++ secondary parameter shard (hpZ; plan.secondary_params, domain.hpp:
 // 90-97): every rank keeps slice `position` of each tensor over its
 // secondary group (Phi/s2 bf16, cost_model.cpp:148-150), refreshed from the
@@ -208,6 +227,7 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   std::vector<amsp::CopySeg> copy;
   plan_units(e.get(), copy);
   plan_secondary(e.get(), dp, plan, copy);
+  plan_push(e.get(), copy);
   // In-step all-gathers default to the TMA bulk-copy kernel when every P
   // slice is 8-element aligned: 640 vs 608 GB/s ingress for the SM kernel
   // and 357 for the copy engines on 13B ZeRO-3 at W = 4
@@ -222,7 +242,11 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   e->off_params = align_up(e->grad_elems * 2);
   e->off_flags = e->off_params + align_up(e->param_elems * 2);
   e->off_sec = e->off_flags + align_up(kFlagBytes);
-  e->off_acc = e->off_sec + align_up(e->s2 > 1 ? e->smap.pshard_elems * 2 : 0);
+  // gather slots in the peer-exported region: the push all-gather stores
+  // every rank's P slice straight into its peers' slots
+  e->off_slots = e->off_sec + align_up(e->s2 > 1 ? e->smap.pshard_elems * 2 : 0);
+  e->slot_bytes = align_up(e->slot_elems * 2);
+  e->off_acc = e->off_slots + 2 * e->slot_bytes;
   // (the accumulator last: its size may differ per rank)
   e->shared_bytes = e->off_acc + align_up(e->acc_elems * 2);
   ck(cudaMalloc(&e->shared, e->shared_bytes), "cudaMalloc shared");
@@ -266,7 +290,6 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   const std::size_t o_pseg = carve(psegs.size() * sizeof(amsp::Seg));
   const std::size_t o_copy = carve(copy.size() * sizeof(amsp::CopySeg));
   const std::size_t o_aseg = carve(asegs.size() * sizeof(amsp::Seg));
-  const std::size_t o_slot0 = carve(e->slot_elems * 2), o_slot1 = carve(e->slot_elems * 2);
   const std::size_t o_stats = carve(kAlign), o_err = carve(kAlign), o_tab = carve(kAlign);
   ck(cudaMalloc(&e->priv, off), "cudaMalloc optimizer state");
   e->master = reinterpret_cast<float*>(e->priv + o_master);
@@ -276,8 +299,8 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   e->d_psegs = reinterpret_cast<amsp::Seg*>(e->priv + o_pseg);
   e->d_copy = reinterpret_cast<amsp::CopySeg*>(e->priv + o_copy);
   e->d_acc_segs = reinterpret_cast<amsp::Seg*>(e->priv + o_aseg);
-  e->slots[0] = reinterpret_cast<uint16_t*>(e->priv + o_slot0);
-  e->slots[1] = reinterpret_cast<uint16_t*>(e->priv + o_slot1);
+  e->slots[0] = e->slot_of(e->rank, 0);
+  e->slots[1] = e->slot_of(e->rank, 1);
   e->stats = reinterpret_cast<float*>(e->priv + o_stats);
   e->err = reinterpret_cast<int*>(e->priv + o_err);
   e->d_peer_flags = reinterpret_cast<uint32_t**>(e->priv + o_tab);
@@ -589,9 +612,10 @@ int amsp_engine_write(amsp_engine_t* e, int which, uint64_t offset, uint64_t cou
 
 int amsp_engine_tune_gather(amsp_engine_t* e, int grid) {
   return amsp::guarded([&] {
-    if (!e || grid < -2) throw Error("engine: bad argument");
-    if (grid == amsp_engine::kGatherTma && !e->copies_aligned())
-      throw Error("engine: the TMA all-gather needs 8-element-aligned P slices");
+    if (!e || grid < -3) throw Error("engine: bad argument");
+    if ((grid == amsp_engine::kGatherTma || grid == amsp_engine::kGatherPush) &&
+        !e->copies_aligned())
+      throw Error("engine: the TMA all-gathers need 8-element-aligned P slices");
     e->gather_grid = grid;
   });
 }

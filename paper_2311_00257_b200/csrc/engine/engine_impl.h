@@ -100,10 +100,12 @@ struct amsp_engine {
   amsp::MeshGroup sec_group;
   amsp::PShardMap smap;
   std::vector<GatherUnit> units2;  // the units' secondary copy tables
+  std::vector<GatherUnit> units_push;  // the units' push tables (own slice only)
 
   // Shared region and its offsets (identical on every rank).
   char* shared = nullptr;
   std::size_t shared_bytes = 0, off_grads = 0, off_params = 0, off_flags = 0, off_sec = 0;
+  std::size_t off_slots = 0, slot_bytes = 0;
   std::uint64_t param_elems = 0;
   void* peer_base[amsp::kMaxRanks] = {};
   bool imported = false;
@@ -129,7 +131,7 @@ struct amsp_engine {
   int grid = 0, variant = 0, sms = 148, gather_grid = 0;
   // gather_grid: > 0 SM-kernel grid, 0 SM kernel with its default grid,
   // kGatherDma copy engines, kGatherTma the bulk-copy kernel.
-  static constexpr int kGatherDma = -1, kGatherTma = -2;
+  static constexpr int kGatherDma = -1, kGatherTma = -2, kGatherPush = -3;
   bool copies_aligned() const {
     for (std::size_t t = 0; t < pmap.slice_len.size(); ++t)
       if ((pmap.slice_len[t] | pmap.pshard_offset[t] | pmap.tensor_offset[t]) & 7u) return false;
@@ -183,6 +185,10 @@ struct amsp_engine {
   }
   uint16_t* params_of(int r) const {
     return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_params);
+  }
+  uint16_t* slot_of(int r, int k) const {
+    return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_slots +
+                                       static_cast<std::size_t>(k & 1) * slot_bytes);
   }
   uint16_t* sec_of(int r) const {
     return reinterpret_cast<uint16_t*>(static_cast<char*>(peer_base[r]) + off_sec);
@@ -402,8 +408,26 @@ struct amsp_engine {
     g.grid = gather_grid > 0 ? gather_grid : 0;
     g.sp = n;
     g.rot = (grp.position + 1) % n;
-    ck(gather_grid == kGatherTma ? amsp::launch_gather_tma(g, s) : amsp::launch_gather(g, s),
-       "gather launch");
+    // (the push mode applies to the step's passes; a single gather pulls)
+    const bool tma = gather_grid == kGatherTma || gather_grid == kGatherPush;
+    ck(tma ? amsp::launch_gather_tma(g, s) : amsp::launch_gather(g, s), "gather launch");
+    ++launches;
+  }
+
+  // Push all-gather of one unit (engine step only): this rank's P slice of
+  // every tensor of the unit into slot `slot` of every P-group member.
+  void push(int unit, int slot, cudaStream_t s) {
+    const GatherUnit& u = units_push[static_cast<std::size_t>(unit)];
+    amsp::PushArgs a{};
+    a.segs = d_copy + u.seg_begin;
+    a.nseg = u.nseg;
+    a.ntiles = u.ntiles;
+    a.sp = sp;
+    a.q = p_group.position;
+    a.src = params_of(rank);
+    for (int j = 0; j < sp; ++j) a.dst[j] = slot_of(p_group.members[j], slot);
+    a.fence_peers = synced() ? 1 : 0;
+    ck(amsp::launch_push_tma(a, s), "push gather launch");
     ++launches;
   }
 
@@ -467,11 +491,19 @@ struct amsp_engine {
       // cost_model.cpp:46-49); RS is fused into the optimizer kernel below.
       cudaEvent_t g_end = record_begin(gather_events, gather_events_used, s);
       const int n = static_cast<int>(units.size());
-      for (int u = 0; u < n; ++u) gather(u, u, s, false, nullptr, s2 > 1);
-      // ZeRO++: every rank's secondary slices are in place before the
-      // backward all-gathers read them from the secondary group
-      if (s2 > 1) barrier(s);
-      for (int u = n - 1; u >= 0; --u) gather(u, u, s, s2 > 1);
+      if (gather_grid == kGatherPush && s2 == 1) {
+        // push all-gather: every rank stores its own slice of each unit into
+        // every P-group member's slot (NVLink stores); the slots are complete
+        // at the barrier that follows the passes
+        for (int u = 0; u < n; ++u) push(u, u, s);
+        for (int u = n - 1; u >= 0; --u) push(u, u, s);
+      } else {
+        for (int u = 0; u < n; ++u) gather(u, u, s, false, nullptr, s2 > 1);
+        // ZeRO++: every rank's secondary slices are in place before the
+        // backward all-gathers read them from the secondary group
+        if (s2 > 1) barrier(s);
+        for (int u = n - 1; u >= 0; --u) gather(u, u, s, s2 > 1);
+      }
       if (g_end) ck(cudaEventRecord(g_end, s), "event record");
     }
     amsp::FusedArgs a{};

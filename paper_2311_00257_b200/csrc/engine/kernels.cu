@@ -1198,6 +1198,60 @@ fused_step_tma_kernel(const FusedArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Push all-gather (engine step, s_p > 1): one thread per CTA; per tile one
+// bulk load of this rank's own slice (local HBM) into a shared-memory stage,
+// then one bulk store per P-group member, destinations rotated from q+1 so
+// the ranks' stores spread over the peers, all in one bulk group. Peer
+// stores ran at 703 GB/s against 667 for pulls (profiles/r01_p2p_4gpu.txt).
+__global__ void __launch_bounds__(32) push_tma_kernel(const PushArgs a) {
+  constexpr int kStages = 5;
+  __shared__ __align__(128) uint16_t buf[kStages][kTile];
+  __shared__ __align__(8) uint64_t full[kStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const int n = a.ntiles > static_cast<int>(blockIdx.x)
+                    ? (a.ntiles - 1 - static_cast<int>(blockIdx.x)) / gridDim.x + 1
+                    : 0;
+  SegCursor<CopySeg, 1> cur;
+  cur.table = a.segs;
+  cur.n = a.nseg;
+  cur.cur = 0;
+  cur.staged = false;
+  unsigned long long dst_off[kStages];
+  uint32_t bytes_of[kStages];
+  auto load = [&](int i) {
+    const int tile = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
+    const CopySeg& cs = cur.at(tile);
+    const unsigned long long off = (static_cast<unsigned long long>(tile) - cs.tile0) * kTile;
+    const unsigned long long len = cs.len - off < kTile ? cs.len - off : kTile;
+    const int s = i % kStages;
+    dst_off[s] = cs.dst + static_cast<unsigned long long>(a.q) * cs.len + off;
+    bytes_of[s] = static_cast<uint32_t>(len * 2);
+    mbar_expect_tx(&full[s], bytes_of[s]);
+    bulk_g2s(buf[s], a.src + cs.src + off, bytes_of[s], &full[s]);
+  };
+  for (int i = 0; i < n && i < kStages; ++i) load(i);
+  for (int i = 0; i < n; ++i) {
+    const int s = i % kStages;
+    mbar_wait(&full[s], (i / kStages) & 1);
+    for (int j = 0; j < a.sp; ++j) {
+      const int d = (a.q + 1 + j) % a.sp;
+      bulk_s2g_nocommit(a.dst[d] + dst_off[s], buf[s], bytes_of[s]);
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    const int k = i - 1 + kStages;  // refill the stage tile i-1 used
+    if (i >= 1 && k < n) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      load(k);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  // peer stores visible system-wide before the barrier after the passes
+  if (a.fence_peers) __threadfence_system();
+}
+
+// ---------------------------------------------------------------------------
 // TMA all-gather of one unit (s_p > 1): one thread per CTA drives a ring of
 // kGatherStages 8 KB shared-memory stages. Each tile is one bulk load
 // (cp.async.bulk, peer P shard over NVLink -> shared memory, completion on an
@@ -1523,6 +1577,13 @@ cudaError_t launch_gather(const GatherArgs& a, cudaStream_t stream) {
   if (a.ntiles == 0) return cudaSuccess;
   const int grid = a.grid > 0 ? a.grid : sm_count() * 4;
   gather_kernel<<<std::min(a.ntiles, grid), 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_push_tma(const PushArgs& a, cudaStream_t stream) {
+  if (a.ntiles == 0) return cudaSuccess;
+  if (a.sp < 1 || a.sp > kMaxRanks) return cudaErrorInvalidValue;
+  push_tma_kernel<<<std::min(a.ntiles, sm_count() * 4), 32, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

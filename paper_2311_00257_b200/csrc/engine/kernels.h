@@ -50,6 +50,20 @@ struct GatherArgs {
   int s2, pos2;
 };
 
+// Push all-gather of one unit: this rank's slice q of every tensor (segs:
+// dst = tensor offset in the unit, src = slice offset in the P shard, len =
+// slice length, tile0 over ceil(len / kTile) tiles per tensor) is stored at
+// dst[j] + seg.dst + q * len for every P-group member j (local or peer).
+struct PushArgs {
+  const CopySeg* segs;
+  int nseg;
+  int ntiles;
+  int sp, q;
+  const uint16_t* src;  // this rank's P shard (local HBM)
+  uint16_t* dst[8];     // the members' slots, position order
+  int fence_peers;
+};
+
 constexpr int kBlock = 256;
 constexpr int kVecPerThread = 2;               // 8-element vectors per thread per tile
 constexpr unsigned long long kTile = kBlock * 8ull * kVecPerThread;  // 4096
@@ -163,6 +177,8 @@ cudaError_t launch_gather(const GatherArgs& a, cudaStream_t stream);
 // Bulk-copy (TMA) variant of launch_gather: 32-thread CTAs, every CopySeg
 // 8-element aligned (see kernels.cu gather_tma_kernel).
 cudaError_t launch_gather_tma(const GatherArgs& a, cudaStream_t stream);
+// Push all-gather (TMA bulk copies: local load, NVLink bulk stores).
+cudaError_t launch_push_tma(const PushArgs& a, cudaStream_t stream);
 cudaError_t launch_init_state(const Seg* segs, int nseg, int ntiles, float* master,
                               float* m, float* v, uint64_t seed, int grid,
                               cudaStream_t stream);

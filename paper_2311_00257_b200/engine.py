@@ -158,9 +158,10 @@ class Engine:
 
     def tune_gather(self, mode) -> None:
         """All-gather implementation of engine.step / gather(): an SM-kernel
-        grid (int > 0), "sm" (default grid), "dma" (copy engines) or "tma"
-        (bulk-copy kernel)."""
-        grid = {"sm": 0, "dma": -1, "tma": -2}.get(mode, mode)
+        grid (int > 0), "sm" (default grid), "dma" (copy engines), "tma"
+        (bulk-copy kernel, pulls) or "push" (the step's passes store each
+        rank's slice into its peers' slots; a single gather() still pulls)."""
+        grid = {"sm": 0, "dma": -1, "tma": -2, "push": -3}.get(mode, mode)
         N.check(N.lib().amsp_engine_tune_gather(self._h, int(grid)))
 
     def time_kernel(self, enable: bool = True) -> None:

@@ -387,7 +387,7 @@ def test_scheduler_real_gemm_compute(cuda, world, p):
     (2, 2, 2, "greedy", "sm"), (4, 4, 4, "greedy", "sm"), (4, 2, 4, "greedy", "sm"),
     (4, 2, 2, "greedy", "sm"), (4, 2, 4, "contiguous", "sm"), (8, 8, 8, "greedy", "sm"),
     (2, 2, 2, "greedy", "tma"), (4, 4, 4, "greedy", "tma"), (8, 8, 8, "greedy", "tma"),
-    (4, 2, 4, "greedy", "dma")])
+    (4, 2, 4, "greedy", "dma"), (4, 4, 4, "greedy", "push"), (8, 8, 8, "greedy", "push")])
 def test_emulated_parameter_sharding_bit_exact(cuda, world, p, os_k, layout, gather):
     """s_p > 1 (ZeRO-3 / AMSP-13B-style): intra-tensor P shards, forward and
     backward all-gathers inside the step, RS fused into the optimizer kernel;

@@ -507,3 +507,39 @@ def test_zeropp_scheduler(cuda, world, p, sec, mb):
         sc.close()
     for e in engines:
         e.close()
+
+
+@pytest.mark.parametrize("world,p,os_k", [(2, 2, 2), (4, 4, 4), (4, 2, 4), (8, 8, 8)])
+def test_push_all_gather_step(cuda, world, p, os_k):
+    """The step's all-gather passes in push mode (every rank stores its P
+    slice into its peers' slots over NVLink): bit-exact state, and after the
+    last step every rank's slots hold the step's input parameters, complete
+    from all peers' stores (the release fence + the barrier after the passes)."""
+    model = S.model("tiny")
+    plan = S.ShardingPlan(M(p, 1), M(p, 1), M(os_k, 1))
+    engines = [Engine(model, plan, M(world, 1), rank=r) for r in range(world)]
+    link_local(engines, sync=True)
+    streams = _streams(cuda, world)
+    for e, s in zip(engines, streams):
+        e.tune_gather("push")
+        e.init_state(s)
+    steps = 3
+    for t in range(1, steps + 1):
+        for r, (e, s) in enumerate(zip(engines, streams)):
+            if r > 0:
+                _delay(s, 300_000)
+            e.synth_grads(t, s)
+            e.step(t, s)
+    phi = model.total_params
+    want = O.trajectory_range(0, phi, DEFAULT_SEED, steps, world, H)
+    prev = O.trajectory_range(0, phi, DEFAULT_SEED, steps - 1, world, H)
+    offsets = np.cumsum([0] + engines[0].tensor_sizes)
+    for e in engines:
+        e.stats()
+        _check_rank(e, want, f"rank {e.rank}")
+        for u in range(min(2, e.info.n_units)):
+            first, n, elems = e.unit(u)
+            lo = offsets[first]
+            assert np.array_equal(e.read(f"slot{u}", 0, elems), prev[3][lo:lo + elems]), (e.rank, u)
+    for e in engines:
+        e.close()
