@@ -561,7 +561,7 @@ def run_ours(args):
              ("2 all-gather passes (" +
               {"sm": "gather_kernel", "dma": "copy engines", "tma": "gather_tma_kernel",
                "push": "push_tma_kernel (NVLink stores)",
-               "auto": "engine default: gather_tma_kernel when aligned"}[args.step_gather] +
+               "auto": "engine default: push_tma_kernel when aligned"}[args.step_gather] +
               ") + " if info.sp > 1 else "") +
              (f"{MB - 1} G-shard accumulations (accumulate_kernel) + " if MB > 1 else "") +
              "fused reduce/AdamW + barriers")

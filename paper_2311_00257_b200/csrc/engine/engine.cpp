@@ -228,11 +228,14 @@ void create_engine(const amsp_engine_config_t* cfg, amsp_engine_t** out) {
   plan_units(e.get(), copy);
   plan_secondary(e.get(), dp, plan, copy);
   plan_push(e.get(), copy);
-  // In-step all-gathers default to the TMA bulk-copy kernel when every P
-  // slice is 8-element aligned: 640 vs 608 GB/s ingress for the SM kernel
-  // and 357 for the copy engines on 13B ZeRO-3 at W = 4
-  // (profiles/r01_tune_gather_tma.jsonl).
-  if (e->sp > 1 && e->copies_aligned()) e->gather_grid = amsp_engine::kGatherTma;
+  // In-step all-gathers default to the TMA bulk-copy push kernel when every P
+  // slice is 8-element aligned: on 13B ZeRO-3 the two passes take 57.7 ms
+  // pushing vs 61.1 ms pulling at W = 4 (39.1 vs 40.8 at W = 2,
+  // profiles/r02_gather_push_ab_13b.jsonl); the TMA pull kernel had beaten
+  // the SM kernel (640 vs 608 GB/s) and the copy engines (357,
+  // profiles/r01_tune_gather_tma.jsonl). Single gathers (and the ZeRO++
+  // secondary passes) pull.
+  if (e->sp > 1 && e->copies_aligned()) e->gather_grid = amsp_engine::kGatherPush;
 
   e->use_device();
   ck(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "stream");
