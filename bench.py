@@ -85,7 +85,8 @@ def parse():
                          "forward (auto, tier ag_rs_ar_bc) or push inside the optimizer")
     ap.add_argument("--step-gather", default="auto", choices=["auto", "sm", "dma", "tma", "push"],
                     help="all-gather implementation inside the pipeline-only step (s_p > 1); "
-                         "auto = the engine's default (TMA when the P slices are aligned)")
+                         "auto = the engine's default (the TMA push kernel when the P slices are "
+                         "aligned)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--grad-ring", action=argparse.BooleanOptionalAction, default=True,
