@@ -716,7 +716,8 @@ def run_ours(args):
         flops = {"model_6PhiBS_plus_attention": 6.0 * phi * toks + attn,
                  "total": (6.0 * lin_params * toks + attn) if compute == "gemm"
                  else 6.0 * phi * toks + attn}
-        flops["executed_over_model"] = round(flops["total"] / flops["model_6PhiBS_plus_attention"], 4)
+        flops["executed_over_model"] = round(
+            flops["total"] / flops["model_6PhiBS_plus_attention"], 4)
         timed(True, args.warmup)
         t_b = timed(True, args.steps)
         t_c = timed(False, args.steps)
@@ -848,7 +849,8 @@ def run_ours(args):
                         "elements) on a copy stream, each chunk's fused update (W > 1: after a "
                         "cross-GPU barrier) behind it -> D2H stats"
                         if info.sp == 1 else
-                        "amsp_engine_step_host: pinned host bf16 grads -> H2D -> step -> D2H stats"),
+                        "amsp_engine_step_host: pinned host bf16 grads -> H2D -> step -> "
+                        "D2H stats"),
                "direction": "host gradients in, updated parameters stay on the device (the "
                             "D2H bytes are the step statistics)"}
         del host
