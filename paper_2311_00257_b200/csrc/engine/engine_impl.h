@@ -97,6 +97,7 @@ struct amsp_engine {
   // group's backward all-gathers.
   int s2 = 1;
   bool sec_fused = false;  // forward gathers store the secondary slice themselves
+  std::vector<int> p_pos2;  // secondary position of each P-group member
   amsp::MeshGroup sec_group;
   amsp::PShardMap smap;
   std::vector<GatherUnit> units2;  // the units' secondary copy tables
@@ -416,7 +417,7 @@ struct amsp_engine {
 
   // Push all-gather of one unit (engine step only): this rank's P slice of
   // every tensor of the unit into slot `slot` of every P-group member.
-  void push(int unit, int slot, cudaStream_t s) {
+  void push(int unit, int slot, cudaStream_t s, bool refresh = false) {
     const GatherUnit& u = units_push[static_cast<std::size_t>(unit)];
     amsp::PushArgs a{};
     a.segs = d_copy + u.seg_begin;
@@ -427,6 +428,13 @@ struct amsp_engine {
     a.src = params_of(rank);
     for (int j = 0; j < sp; ++j) a.dst[j] = slot_of(p_group.members[j], slot);
     a.fence_peers = synced() ? 1 : 0;
+    if (refresh) {
+      a.s2 = s2;
+      for (int j = 0; j < sp; ++j) {
+        a.pos2[j] = p_pos2[static_cast<std::size_t>(j)];
+        a.sec[j] = sec_of(p_group.members[j]);
+      }
+    }
     ck(amsp::launch_push_tma(a, s), "push gather launch");
     ++launches;
   }
@@ -497,6 +505,12 @@ struct amsp_engine {
         // at the barrier that follows the passes
         for (int u = 0; u < n; ++u) push(u, u, s);
         for (int u = n - 1; u >= 0; --u) push(u, u, s);
+      } else if (gather_grid == kGatherPush && sec_fused) {
+        // ZeRO++: the forward pushes also store into every member's
+        // secondary slice; the backward pass pulls from the secondary group
+        for (int u = 0; u < n; ++u) push(u, u, s, true);
+        barrier(s);
+        for (int u = n - 1; u >= 0; --u) gather(u, u, s, true);
       } else {
         for (int u = 0; u < n; ++u) gather(u, u, s, false, nullptr, s2 > 1);
         // ZeRO++: every rank's secondary slices are in place before the

@@ -42,7 +42,7 @@ def main():
     ap.add_argument("--ring", action="store_true",
                     help="scheduler + s_g > 1: the gradient buffer is the schedule's smallest "
                          "ring (learned from a first engine with a generous ring)")
-    ap.add_argument("--gather", default="sm", choices=["sm", "tma", "dma"])
+    ap.add_argument("--gather", default="sm", choices=["sm", "tma", "dma", "push"])
     ap.add_argument("--reduce", default="sm", choices=["sm", "dma"],
                     help="scheduler gradient reduce: SM NVLink pulls / copy-engine staged")
     ap.add_argument("--model", default="tiny")

@@ -90,6 +90,9 @@ CASES = [c + (0,) for c in CASES] + [
     (4, "2x2", "2x2", "greedy", "g=2x2+mb=2+sched+synth+ring", 0),
     # ZeRO++ secondary parameter mesh (backward all-gathers from the secondary group)
     (4, "4x1", None, "greedy", "4x1+p2=2x1", 0),
+    (4, "4x1", None, "greedy", "4x1+p2=2x1+push", 0),
+    (4, "4x1", None, "greedy", "4x1+push", 0),
+    (2, "2x1", None, "greedy", "2x1+push", 0),
     (4, "4x1", None, "greedy", "4x1+p2=2x1+sched+synth", 0),
     (4, "4x1", None, "greedy", "4x1+p2=2x1+mb=2+sched+synth", 0)]
 
@@ -133,6 +136,8 @@ def test_torchrun_group(world, os_mesh, dp_mesh, layout, p_mesh, variant):
         cmd += ["--host", "--model", "chunky", "--steps", "2"]
     if tma:
         cmd += ["--gather", "tma"]
+    if "push" in words:
+        cmd += ["--gather", "push"]
     if "dmared" in words:
         cmd += ["--reduce", "dma"]
     if "g" in opts:

@@ -426,8 +426,9 @@ def test_synced_scheduler_real_gemm_micro_batches(cuda, world, g, mb, opt_overla
 # plan.secondary_params (domain.hpp:90-97): the backward all-gathers read the
 # secondary group's slices (overlap_sim.cpp:222-230, cost_model.cpp:41), each
 # rank keeping Phi/s2 more bf16 (cost_model.cpp:148-150).
+@pytest.mark.parametrize("gather", ["tma", "push"])
 @pytest.mark.parametrize("world,p,sec", [(4, 4, 2), (8, 8, 2), (8, 8, 4), (4, 2, 2)])
-def test_zeropp_secondary_shard(cuda, world, p, sec):
+def test_zeropp_secondary_shard(cuda, world, p, sec, gather):
     model = S.model("tiny")
     plan = S.ShardingPlan(M(p, 1), M(p, 1), M(world, 1) if p < world else M(p, 1),
                           secondary_params=M(sec, 1))
@@ -441,7 +442,7 @@ def test_zeropp_secondary_shard(cuda, world, p, sec):
     plain.close()
     streams = _streams(cuda, world)
     for e, s in zip(engines, streams):
-        e.tune_gather("tma")
+        e.tune_gather(gather)
         e.init_state(s)
     steps = 3
     for t in range(1, steps + 1):
