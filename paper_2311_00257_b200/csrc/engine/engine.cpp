@@ -143,8 +143,6 @@ void plan_secondary(amsp_engine* e, const DeviceMesh& dp, const shardplan::Shard
   e->s2 = plan.secondary_params->size();
   if (e->s2 > e->world) throw Error("engine: secondary parameter mesh larger than the DP mesh");
   e->sec_group = amsp::mesh_group(dp, *plan.secondary_params, e->rank);
-  for (int m : e->p_group.members)  // every P-group member's secondary position
-    e->p_pos2.push_back(amsp::mesh_group(dp, *plan.secondary_params, m).position);
   e->smap = amsp::pshard_map(e->tensor_sizes, e->s2);
   // the forward gathers write the secondary slice as they go (GatherArgs::sec)
   // when every primary and secondary slice is 8-element aligned

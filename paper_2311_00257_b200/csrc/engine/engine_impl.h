@@ -97,7 +97,6 @@ struct amsp_engine {
   // group's backward all-gathers.
   int s2 = 1;
   bool sec_fused = false;  // forward gathers store the secondary slice themselves
-  std::vector<int> p_pos2;  // secondary position of each P-group member
   amsp::MeshGroup sec_group;
   amsp::PShardMap smap;
   std::vector<GatherUnit> units2;  // the units' secondary copy tables
@@ -417,7 +416,7 @@ struct amsp_engine {
 
   // Push all-gather of one unit (engine step only): this rank's P slice of
   // every tensor of the unit into slot `slot` of every P-group member.
-  void push(int unit, int slot, cudaStream_t s, bool refresh = false) {
+  void push(int unit, int slot, cudaStream_t s) {
     const GatherUnit& u = units_push[static_cast<std::size_t>(unit)];
     amsp::PushArgs a{};
     a.segs = d_copy + u.seg_begin;
@@ -428,13 +427,6 @@ struct amsp_engine {
     a.src = params_of(rank);
     for (int j = 0; j < sp; ++j) a.dst[j] = slot_of(p_group.members[j], slot);
     a.fence_peers = synced() ? 1 : 0;
-    if (refresh) {
-      a.s2 = s2;
-      for (int j = 0; j < sp; ++j) {
-        a.pos2[j] = p_pos2[static_cast<std::size_t>(j)];
-        a.sec[j] = sec_of(p_group.members[j]);
-      }
-    }
     ck(amsp::launch_push_tma(a, s), "push gather launch");
     ++launches;
   }
@@ -505,13 +497,11 @@ struct amsp_engine {
         // at the barrier that follows the passes
         for (int u = 0; u < n; ++u) push(u, u, s);
         for (int u = n - 1; u >= 0; --u) push(u, u, s);
-      } else if (gather_grid == kGatherPush && sec_fused) {
-        // ZeRO++: the forward pushes also store into every member's
-        // secondary slice; the backward pass pulls from the secondary group
-        for (int u = 0; u < n; ++u) push(u, u, s, true);
-        barrier(s);
-        for (int u = n - 1; u >= 0; --u) gather(u, u, s, true);
       } else {
+        // (ZeRO++ pulls: the receiver keeps its secondary slice from its own
+        // gathered tensor, a local store; pushing it into the members'
+        // secondary buffers doubled the NVLink egress -- 97.4 vs 80.0 ms on
+        // 13B at W = 4, profiles/r02_zeropp_push_vs_pull_13b.jsonl)
         for (int u = 0; u < n; ++u) gather(u, u, s, false, nullptr, s2 > 1);
         // ZeRO++: every rank's secondary slices are in place before the
         // backward all-gathers read them from the secondary group

@@ -1218,7 +1218,7 @@ __global__ void __launch_bounds__(32) push_tma_kernel(const PushArgs a) {
   cur.n = a.nseg;
   cur.cur = 0;
   cur.staged = false;
-  unsigned long long dst_off[kStages], seg_len[kStages], seg_sec[kStages], seg_dst[kStages];
+  unsigned long long dst_off[kStages];
   uint32_t bytes_of[kStages];
   auto load = [&](int i) {
     const int tile = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
@@ -1226,9 +1226,6 @@ __global__ void __launch_bounds__(32) push_tma_kernel(const PushArgs a) {
     const unsigned long long off = (static_cast<unsigned long long>(tile) - cs.tile0) * kTile;
     const unsigned long long len = cs.len - off < kTile ? cs.len - off : kTile;
     const int s = i % kStages;
-    seg_len[s] = cs.len;
-    seg_sec[s] = cs.sec;
-    seg_dst[s] = cs.dst;
     dst_off[s] = cs.dst + static_cast<unsigned long long>(a.q) * cs.len + off;
     bytes_of[s] = static_cast<uint32_t>(len * 2);
     mbar_expect_tx(&full[s], bytes_of[s]);
@@ -1241,17 +1238,6 @@ __global__ void __launch_bounds__(32) push_tma_kernel(const PushArgs a) {
     for (int j = 0; j < a.sp; ++j) {
       const int d = (a.q + 1 + j) % a.sp;
       bulk_s2g_nocommit(a.dst[d] + dst_off[s], buf[s], bytes_of[s]);
-      if (a.s2 > 0) {  // the part of the tile inside member d's secondary slice
-        const unsigned long long len2 = seg_len[s] * a.sp / a.s2;
-        const unsigned long long lo2 = len2 * static_cast<unsigned long long>(a.pos2[d]);
-        const unsigned long long x0 = dst_off[s] - seg_dst[s];  // tensor-local index
-        const unsigned long long x1 = x0 + bytes_of[s] / 2;
-        const unsigned long long b0 = x0 > lo2 ? x0 : lo2;
-        const unsigned long long b1 = x1 < lo2 + len2 ? x1 : lo2 + len2;
-        if (b0 < b1)
-          bulk_s2g_nocommit(a.sec[d] + seg_sec[s] + (b0 - lo2), buf[s] + (b0 - x0),
-                            static_cast<uint32_t>((b1 - b0) * 2));
-      }
     }
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     const int k = i - 1 + kStages;  // refill the stage tile i-1 used

@@ -62,12 +62,6 @@ struct PushArgs {
   const uint16_t* src;  // this rank's P shard (local HBM)
   uint16_t* dst[8];     // the members' slots, position order
   int fence_peers;
-  // ZeRO++ forward pass (s2 > 0): the part of the slice inside member j's
-  // secondary slice [pos2[j]*L/s2, +L/s2) of each tensor (L = len * sp) is
-  // also stored at sec[j] + seg.sec + (index - pos2[j]*L/s2)
-  int s2;
-  int pos2[8];
-  uint16_t* sec[8];
 };
 
 constexpr int kBlock = 256;
