@@ -30,3 +30,6 @@ ALGKEY=algorithmic_bytes_accumulate run staged_accumulate_w2_1b accumulate_kerne
 run staged_fused_w2_1b fused_step 0 python tools/ncu_targets.py staged --world 2 --steps 2
 run staged_fused_w4_1b fused_step 0 python tools/ncu_targets.py staged --world 4 --steps 2
 ls -la gpurun_out/ncu
+# the step's push all-gather (s_p > 1 default), ZeRO-3 W=4 emulated
+run push_w4_1b push_tma 0 python tools/ncu_targets.py push --world 4 --steps 2
+ls -la gpurun_out/ncu

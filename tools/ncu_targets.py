@@ -6,6 +6,8 @@ are the multi-GPU kernel's HBM + NVLink bytes landing on one device).
 
   python tools/ncu_targets.py fused  --world W [--model llama-1b] [--variant 0]
   python tools/ncu_targets.py gather --world W [--model llama-1b]   (ZeRO-3, TMA gather)
+  python tools/ncu_targets.py push --world W [--model llama-1b]     (ZeRO-3 step: the
+      push all-gather of unit 0, push_tma_kernel)
   python tools/ncu_targets.py staged --world W [--model llama-1b]   (ZeRO-2, M=2: the
       accumulate_kernel of micro-batch 0, then the fused update with accumulator sources)
 
@@ -27,7 +29,7 @@ from paper_2311_00257_b200.engine import Engine, link_local  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["fused", "gather", "staged"])
+    ap.add_argument("what", choices=["fused", "gather", "staged", "push"])
     ap.add_argument("--model", default="llama-1b")
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--variant", type=int, default=0)
@@ -58,7 +60,22 @@ def main():
     info = engines[0]._info()
     out = {"what": args.what, "model": args.model, "phi": phi, "world": W,
            "variant": info.variant, "grid": info.grid}
-    if args.what == "staged":
+    if args.what == "push":
+        # one launch = this rank's slice of unit 0 read locally (2 B x unit / W)
+        # and stored into the W members' slots (2 B x unit)
+        ue = engines[0].unit(0)[2]
+        out["algorithmic_bytes_per_launch"] = 2 * ue // W + 2 * ue
+        for e in engines:
+            e.time_kernel(True)
+        for t in range(1, args.steps + 1):
+            for e in engines:
+                e.synth_grads(t)
+            for e in engines:
+                e.step(t)
+        torch.cuda.synchronize()
+        gms, gn = engines[0].gather_ms()
+        out["gather_passes_ms"] = gms / max(gn, 1)
+    elif args.what == "staged":
         # accumulate (rank 0): acc_elems x (2 B from each of the W G-block
         # ranks + 2 B accumulator write; first micro-batch: no read); fused:
         # owned x (2 B x W holders' accumulators... here W/s_g = 1 holder:
