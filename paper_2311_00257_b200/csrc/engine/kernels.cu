@@ -1583,7 +1583,13 @@ cudaError_t launch_gather(const GatherArgs& a, cudaStream_t stream) {
 cudaError_t launch_push_tma(const PushArgs& a, cudaStream_t stream) {
   if (a.ntiles == 0) return cudaSuccess;
   if (a.sp < 1 || a.sp > kMaxRanks) return cudaErrorInvalidValue;
-  push_tma_kernel<<<std::min(a.ntiles, sm_count() * 4), 32, 0, stream>>>(a);
+  // CTAs per SM (tuning hook AMSP_PUSH_CTAS; 2 / 4 / 5 give 57.4 / 57.7 / 58.0 ms
+  // for 13B's passes at W = 4, profiles/r02_push_ctas_13b_w4.jsonl: saturated)
+  static const int per_sm = [] {
+    const char* x = std::getenv("AMSP_PUSH_CTAS");
+    return x && std::atoi(x) > 0 ? std::atoi(x) : 4;
+  }();
+  push_tma_kernel<<<std::min(a.ntiles, sm_count() * per_sm), 32, 0, stream>>>(a);
   return cudaGetLastError();
 }
 
